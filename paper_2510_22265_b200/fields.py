@@ -1,0 +1,129 @@
+"""Seeded synthetic stand-ins for the ERA5 fields named in BASELINE.json.
+
+ERA5 itself is not available offline; these generators reproduce the shapes
+and value distributions of the five BASELINE.json configurations (SURVEY.md
+§8(d)).  Every field is a Gaussian random field with an isotropic power-law
+spectrum drawn from ``numpy.random.default_rng(seed)`` and synthesised with an
+inverse FFT, then standardised and rescaled.  Generation is never timed.
+
+The spectral convention (DC bin pinned to 1 before the power law, complex
+normal spectrum, real part of the inverse FFT, zero-mean unit-variance
+standardisation) follows the reference's synthetic-field generator
+(pkg/src/ebcc/bench/fields.py:30-41) so the fields have the same statistics.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+GRID_025 = (721, 1440)       # 0.25 degree global lat-lon
+GRID_0625 = (2881, 5760)     # 1/16 degree global lat-lon
+
+
+def power_law_grf(rows: int, cols: int, seed: int, beta: float) -> np.ndarray:
+    """Unit-variance float64 GRF whose power spectrum falls as k**-beta."""
+    gen = np.random.default_rng(seed)
+    fy = np.fft.fftfreq(rows).reshape(rows, 1)
+    fx = np.fft.fftfreq(cols).reshape(1, cols)
+    kmag = np.hypot(fy, fx)
+    kmag[0, 0] = 1.0
+    amp = np.power(kmag, -0.5 * beta)
+    re = gen.standard_normal((rows, cols))
+    im = gen.standard_normal((rows, cols))
+    g = np.fft.ifft2((re + 1j * im) * amp).real
+    g = g - g.mean()
+    sd = g.std()
+    return g / sd if sd > 0 else g
+
+
+def temperature_like(rows: int, cols: int, seed: int = 0, mean: float = 280.0,
+                     std: float = 15.0, beta: float = 3.0) -> np.ndarray:
+    """Config 1: smooth k^-3 field rescaled to (mean, std), float32."""
+    return (power_law_grf(rows, cols, seed, beta) * std + mean).astype(np.float32)
+
+
+def precip_like(rows: int, cols: int, seed: int, beta: float = 2.5,
+                dry_percentile: float = 60.0) -> np.ndarray:
+    """Config 3: exp of a k^-2.5 GRF with the lowest 60% set to zero."""
+    f = np.exp(power_law_grf(rows, cols, seed, beta))
+    cut = np.percentile(f, dry_percentile)
+    f[f < cut] = 0.0
+    return f.astype(np.float32)
+
+
+def config1_field() -> np.ndarray:
+    """Single 721x1440 temperature-like field (BASELINE.json configs[0])."""
+    return temperature_like(*GRID_025, seed=0)
+
+
+def config2_levels(levels: int = 37, rows: int = GRID_025[0],
+                   cols: int = GRID_025[1]) -> np.ndarray:
+    """37 independent k^-3 levels, mean 200..300, std 2..20 (configs[1]).
+
+    Returns (1, levels, rows, cols) float32.
+    """
+    out = np.empty((1, levels, rows, cols), dtype=np.float32)
+    for lev in range(levels):
+        frac = lev / max(1, levels - 1)
+        out[0, lev] = temperature_like(rows, cols, seed=1000 + lev,
+                                       mean=200.0 + 100.0 * frac,
+                                       std=2.0 + 18.0 * frac)
+    return out
+
+
+def config3_precip(steps: int = 24, rows: int = GRID_025[0],
+                   cols: int = GRID_025[1]) -> np.ndarray:
+    """24 precipitation-like time steps, (steps, 1, rows, cols) (configs[2])."""
+    out = np.empty((steps, 1, rows, cols), dtype=np.float32)
+    for t in range(steps):
+        out[t, 0] = precip_like(rows, cols, seed=2000 + t)
+    return out
+
+
+def config4_fields(nvars: int = 10, rows: int = GRID_0625[0],
+                   cols: int = GRID_0625[1]):
+    """Ten 2881x5760 variables: 6 smooth k^-3 + 4 wind-like k^-5/3 (configs[3]).
+
+    Yields (var_index, float32 field) so callers never hold all of them.
+    """
+    for v in range(nvars):
+        gen = np.random.default_rng(3000 + v)
+        if v < 6:
+            mean = float(gen.uniform(0.0, 300.0))
+            std = float(gen.uniform(1.0, 20.0))
+            yield v, temperature_like(rows, cols, seed=3000 + v, mean=mean, std=std)
+        else:
+            yield v, temperature_like(rows, cols, seed=3000 + v, mean=0.0, std=10.0,
+                                      beta=5.0 / 3.0)
+
+
+def config5_field(field_id: int, rows: int = GRID_025[0],
+                  cols: int = GRID_025[1]) -> np.ndarray:
+    """One field of the 8 var x 37 level x 8 step sweep (configs[4])."""
+    gen = np.random.default_rng(4000 + field_id)
+    mean = float(gen.uniform(200.0, 300.0))
+    std = float(gen.uniform(2.0, 20.0))
+    return temperature_like(rows, cols, seed=4000 + field_id, mean=mean, std=std)
+
+
+CONFIG5_FIELDS = 8 * 37 * 8
+
+
+def small_field(kind: str, rows: int, cols: int, seed: int) -> np.ndarray:
+    """Small test fields: 'smooth', 'spiky' (isolated heavy-tailed outliers),
+    'precip' (intermittent), 'noise' (white) — float32."""
+    if kind == "smooth":
+        return temperature_like(rows, cols, seed=seed, mean=0.0, std=1.0)
+    if kind == "precip":
+        return precip_like(rows, cols, seed=seed)
+    if kind == "noise":
+        return np.random.default_rng(seed).standard_normal((rows, cols)).astype(np.float32)
+    if kind == "spiky":
+        f = power_law_grf(rows, cols, seed, 3.0)
+        gen = np.random.default_rng(seed + 7919)
+        n = rows * cols
+        k = max(1, n // 4000)
+        at = gen.choice(n, size=k, replace=False)
+        f.reshape(-1)[at] += gen.choice([-1.0, 1.0], size=k) * np.exp(gen.normal(2.0, 0.7, size=k))
+        return f.astype(np.float32)
+    raise ValueError(f"unknown kind {kind!r}")
