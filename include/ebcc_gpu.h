@@ -1,0 +1,133 @@
+/* ebcc_gpu.h — C ABI of the B200-native EBCC chunk path (libebcc_gpu.so).
+ *
+ * The library replaces the reference's per-chunk pipeline behind its own
+ * Python API: everything above the two batch calls (ebcc.api.compress /
+ * decompress, the container writer/reader, tiling and ingest validation)
+ * stays host Python, byte-identical to the reference.
+ *
+ *   ebcc_compress    replaces pipeline.compress_grid's per-chunk loop
+ *                    (pkg/src/ebcc/pipeline.py:358-367) over a batch of
+ *                    same-shape chunks: compress_chunk (pipeline.py:277-329)
+ *                    with its base-quantile search (142-199), pure-base search
+ *                    (215-236), residual encode + truncation search (243-254,
+ *                    303-309) and candidate choice (315-329), all on device.
+ *   ebcc_decompress  replaces pipeline.decompress_grid's per-chunk loop
+ *                    (pipeline.py:370-379) -> decompress_chunk (332-355).
+ *
+ * Plain pointers and sizes only; no exceptions cross the boundary.  Every
+ * call returns an EBCC_* status; ebcc_last_error() has the message.
+ */
+#ifndef EBCC_GPU_H
+#define EBCC_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EBCC_ABI_VERSION 1
+
+/* status codes (mirroring pkg/src/ebcc/errors.py) */
+#define EBCC_OK 0
+#define EBCC_E_ARGUMENT 1      /* ArgumentError  (pipeline.py:54-62)            */
+#define EBCC_E_FORMAT 2        /* FormatError    (pipeline.py:336-353)          */
+#define EBCC_E_RESIDUAL 3      /* ResidualInsufficient (pipeline.py:322-325)    */
+#define EBCC_E_CAPACITY 4      /* payload buffer too small; see payload_total  */
+#define EBCC_E_CUDA 5          /* CUDA runtime failure -> EbccError              */
+#define EBCC_E_NOMEM 6         /* device allocation failed                     */
+
+/* flags */
+#define EBCC_INPUT_ON_DEVICE 1   /* `fields` / `payload` are device pointers  */
+#define EBCC_OUTPUT_ON_DEVICE 2  /* `payload` / `out` are device pointers     */
+
+/* Chunk modes (pipeline.py:38-41). */
+#define EBCC_MODE_CONSTANT 0
+#define EBCC_MODE_PURE_BASE 1
+#define EBCC_MODE_TWO_LAYER 2
+
+/* One chunk's record: the container record fields (container.py:26-27)
+ * plus search statistics. */
+typedef struct {
+  int32_t mode;
+  int32_t status;          /* per-chunk status (EBCC_OK / EBCC_E_RESIDUAL)   */
+  double vmin, vmax;       /* chunk extrema (float32 values held as double)  */
+  int64_t base_len;        /* bytes of base stream in the payload            */
+  int64_t resid_len;       /* bytes of residual stream in the payload        */
+  int32_t n_base_probes;   /* distinct base budgets evaluated (P_base)       */
+  int32_t n_trunc_probes;  /* residual truncation evaluations (P_trunc)      */
+  int32_t resid_planes;    /* 24 or 32 when TWO_LAYER                        */
+  int32_t reserved;
+} ebcc_chunk_rec;
+
+typedef struct ebcc_ctx ebcc_ctx;
+
+int ebcc_abi_version(void);
+
+/* One context per device (and per host thread using it). */
+int ebcc_create(int32_t device, ebcc_ctx **out);
+void ebcc_destroy(ebcc_ctx *ctx);
+/* Run on this cudaStream_t (default: the context's own stream). */
+int ebcc_set_stream(ebcc_ctx *ctx, void *cuda_stream);
+const char *ebcc_last_error(const ebcc_ctx *ctx);
+
+/* Compress `nfields` row-major float32 chunks of rows x cols each, laid out
+ * back to back (chunk i at fields + i*rows*cols).  Parameters are the
+ * reference's EbccParams as Python doubles (pipeline.py:44-62).
+ * Payload of chunk i is written at payload + payload_offsets[i]
+ * (base_len + resid_len bytes); payload_total receives the sum.  When
+ * payload_cap is too small the call returns EBCC_E_CAPACITY with records and
+ * payload_total filled; call ebcc_fetch_payload with a larger buffer.
+ * A chunk for which no candidate reaches the bound has status
+ * EBCC_E_RESIDUAL and the call returns EBCC_E_RESIDUAL. */
+int ebcc_compress(ebcc_ctx *ctx, const float *fields, int64_t nfields, int32_t rows,
+                  int32_t cols, double eps_rel, double q, double r0, double search_tol,
+                  int32_t flags, ebcc_chunk_rec *recs, uint8_t *payload, int64_t payload_cap,
+                  int64_t *payload_offsets, int64_t *payload_total);
+
+/* Copy the payload of the last ebcc_compress call. */
+int ebcc_fetch_payload(ebcc_ctx *ctx, uint8_t *payload, int64_t payload_cap, int32_t flags);
+
+/* Decompress `nfields` same-shape chunks.  recs[i].mode/vmin/vmax/base_len/
+ * resid_len come from the container; chunk i's payload starts at
+ * payload + payload_offsets[i].  `levels` is the level count stored in the
+ * streams' headers.  Writes nfields*rows*cols float32 to `out`. */
+int ebcc_decompress(ebcc_ctx *ctx, const uint8_t *payload, const int64_t *payload_offsets,
+                    const ebcc_chunk_rec *recs, int64_t nfields, int32_t rows, int32_t cols,
+                    int32_t levels, int32_t flags, float *out);
+
+/* Unit-level entry points (host pointers), each the device counterpart of a
+ * reference function, used by the parity tests:
+ *   ebcc_dwt          dwt.forward_dwt / dwt.inverse_dwt (dwt.py:178-216) on
+ *                     nfields rows x cols float64 arrays; `levels` as given
+ *                     (forward clamps like clamp_levels).
+ *   ebcc_spiht_encode spiht.spiht_encode(pyramid, planes=planes) unbudgeted
+ *                     (spiht.py:271-358); budgeted streams are byte prefixes.
+ *   ebcc_spiht_decode spiht.decode_with_plane(data, prefix_len)
+ *                     (spiht.py:403-482): coefficients + n_last (-999: None). */
+int ebcc_dwt(ebcc_ctx *ctx, const double *in, double *out, int64_t nfields, int32_t rows,
+             int32_t cols, int32_t levels, int32_t inverse);
+int ebcc_spiht_encode(ebcc_ctx *ctx, const double *coeffs, int32_t rows, int32_t cols,
+                      int32_t levels, int32_t planes, uint8_t *out, int64_t cap, int64_t *len);
+int ebcc_spiht_decode(ebcc_ctx *ctx, const uint8_t *data, int64_t len, int64_t prefix_len,
+                      int32_t rows, int32_t cols, double *coeffs_out, int32_t *n_last);
+
+/* Instrumentation for bench.py: kernels launched and device milliseconds
+ * (CUDA events on the library stream) of the last call, split by stage. */
+typedef struct {
+  int64_t kernel_launches;
+  double ms_total;
+  double ms_encode;     /* DWT + SPIHT encodes                       */
+  double ms_probe;      /* feedback probes (decode + IDWT + reduce)  */
+  double ms_other;
+  int64_t probe_launches;     /* probe steps (batched over fields)   */
+  double ms_probe_kernel;     /* summed duration of the dominant probe kernels */
+  int64_t probe_kernel_count;
+} ebcc_stats;
+
+int ebcc_get_stats(const ebcc_ctx *ctx, ebcc_stats *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1157 @@
+// Host runtime of the EBCC B200 path: device workspace, the batched feedback
+// controller, and the C ABI declared in include/ebcc_gpu.h.
+//
+// Controller design.  The reference's searches (pipeline.py:142-254) are
+// sequential and data dependent, and the emitted bytes depend on visiting
+// exactly the same budgets in the same order.  Each chunk's
+// search is therefore written here as ordinary straight-line code over a
+// memo, restated from the reference; a memo miss throws NeedProbe.  Every
+// step the controller *replays* each chunk's search from the top against its
+// memo (microseconds of host work), collects the one missing probe per chunk,
+// runs all of them as ONE batched device probe (decode -> IDWT -> reduction
+// for every chunk at once), stores the two scalars per chunk, and repeats.
+// The memo keeps insertion order so that replays see the exact snapshot the
+// reference's dict iteration would (pipeline.py:193-198, 227-234).
+//
+// Phase order per chunk: base search, pure-base search, residual encode,
+// truncation search.  The reference runs the truncation search before the
+// pure search, but the truncation search never touches the base memo, so
+// the order is observably identical, and running both base-memo searches
+// first lets the residual encode reuse the base coefficient metadata arrays.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/ebcc_gpu.h"
+#include "dwt.cuh"
+#include "probe.cuh"
+#include "spiht.cuh"
+
+using namespace ebcc;
+
+namespace {
+
+constexpr int kBasePlanes = 24;   // spiht.DEFAULT_PLANES
+constexpr int kDeepPlanes = 32;   // spiht.DEEP_PLANES
+
+struct CudaFail {
+  cudaError_t e;
+  const char* what;
+};
+
+#define CK(x)                                            \
+  do {                                                   \
+    cudaError_t e_ = (x);                                \
+    if (e_ != cudaSuccess) throw CudaFail{e_, #x};       \
+  } while (0)
+
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(&p, sizeof(T) * count);
+  if (e != cudaSuccess) throw CudaFail{e, "cudaMalloc"};
+  return static_cast<T*>(p);
+}
+
+// CPython float floor division (Objects/floatobject.c float_divmod), used by
+// base_codec.budget_for_ratio: int(raw // ratio) is NOT floor(raw / ratio).
+double py_floordiv(double vx, double wx) {
+  double mod = std::fmod(vx, wx);
+  double div = (vx - mod) / wx;
+  if (mod != 0.0 && ((wx < 0) != (mod < 0))) div -= 1.0;
+  double fl;
+  if (div != 0.0) {
+    fl = std::floor(div);
+    if (div - fl > 0.5) fl += 1.0;
+  } else {
+    fl = std::copysign(0.0, vx / wx);
+  }
+  return fl;
+}
+
+struct NeedBase { int64_t budget; };
+struct NeedTrunc { int planes; int64_t t; };
+
+// ---------------------------------------------------------------------------
+// per-chunk search state (a restatement of pipeline._ChunkCoder + searches)
+struct Entry {
+  int64_t budget, len;
+  uint64_t count;
+  double maxerr;
+};
+
+struct ChunkSearch {
+  int64_t n = 0, raw = 0;
+  double q = 0, r0 = 0, tol = 0, eps_abs = 0;
+  uint64_t T_base = 0;                 // bits of the full 24-plane base stream
+  std::vector<Entry> memo;             // insertion order = seq
+  std::unordered_map<int64_t, int> at; // budget -> memo index
+  size_t vsize = 0;                    // replay timeline position
+  std::unordered_map<int64_t, double> trunc[2];  // (24|32) t -> err
+
+  bool constant = false, failed = false;
+  int phase = 0;                       // 0 base, 1 pure, 2 trunc, 3 done
+  int64_t base_budget = -1, pure_budget = -1;
+  int64_t trunc_t = -1;
+  int trunc_planes = 0;
+  int n_trunc_calls = 0;
+
+  int64_t clamp_budget(int64_t b) const {
+    if (b > raw) b = raw;
+    if (b < kHeader) b = kHeader;
+    return b;
+  }
+  int64_t stream_len(int64_t b) const {
+    int64_t full = kHeader + (int64_t)((T_base + 7) / 8);
+    return b < full ? b : full;
+  }
+  // _ChunkCoder.at_budget with the replay timeline
+  const Entry& at_budget(int64_t b) {
+    b = clamp_budget(b);
+    auto it = at.find(b);
+    if (it == at.end()) throw NeedBase{b};
+    size_t seq = (size_t)it->second;
+    if (seq == vsize) vsize++;
+    return memo[seq];
+  }
+  double q_of(const Entry& e) const { return (double)e.count / (double)n; }
+  int64_t budget_for_ratio(double ratio) const {
+    double raw_f = (double)raw;
+    int64_t b = (int64_t)py_floordiv(raw_f, ratio);
+    return b > kHeader ? b : kHeader;
+  }
+  const Entry& at_ratio(double ratio) { return at_budget(budget_for_ratio(ratio)); }
+  bool pure_ok(int64_t b) { return at_budget(b).maxerr <= eps_abs; }
+
+  // pipeline._bisect_min_feasible
+  template <class F>
+  static int64_t bisect(int64_t lo, int64_t hi, F feasible) {
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) / 2;
+      if (feasible(mid)) hi = mid;
+      else lo = mid;
+    }
+    return hi;
+  }
+
+  // pipeline._search_base (pipeline.py:142-199) -> chosen budget
+  int64_t search_base() {
+    vsize = 0;
+    double r_cap = std::max(1.0, (double)raw / (double)kHeader);
+    double r0c = std::min(std::max(r0, 1.0), r_cap);
+    double q_a0 = q_of(at_ratio(r0c));
+    double r_low = r0c, r_high = r0c;
+    bool have = q_a0 >= q;
+    double q_a = q_a0;
+    while (q_a < q && r_low > 1.0) {
+      r_low = std::max(1.0, r_low / 2.0);
+      q_a = q_of(at_ratio(r_low));
+    }
+    if (q_a >= q) { at_ratio(r_low); have = true; }
+    if (!have) return at_ratio(1.0).budget;
+    q_a = q_a0;
+    while (q_a > q && r_high < r_cap) {
+      r_high = std::min(r_cap, r_high * 2.0);
+      q_a = q_of(at_ratio(r_high));
+    }
+    while (r_high - r_low > tol) {
+      double r_mid = 0.5 * (r_low + r_high);
+      if (q_of(at_ratio(r_mid)) < q) r_high = r_mid;
+      else r_low = r_mid;
+    }
+    int64_t hi = -1, lo = kHeader - 1;
+    for (size_t i = 0; i < vsize; i++)
+      if (q_of(memo[i]) >= q && (hi < 0 || memo[i].budget < hi)) hi = memo[i].budget;
+    for (size_t i = 0; i < vsize; i++)
+      if (q_of(memo[i]) < q && memo[i].budget < hi) lo = std::max(lo, memo[i].budget);
+    int64_t best = bisect(lo, hi, [&](int64_t b) { return q_of(at_budget(b)) >= q; });
+    return at_budget(best).budget;
+  }
+
+  // pipeline._search_pure (pipeline.py:215-236) -> budget or -1
+  int64_t search_pure(size_t base_entries) {
+    vsize = base_entries;
+    if (pure_ok(kHeader)) return at_budget(kHeader).budget;
+    if (!pure_ok(raw)) return -1;
+    int64_t lo = kHeader, hi = raw;
+    std::vector<int64_t> cached;
+    for (size_t i = 0; i < vsize; i++) cached.push_back(memo[i].budget);
+    std::sort(cached.begin(), cached.end());
+    for (int64_t b : cached)
+      if (pure_ok(b)) hi = std::min(hi, b);
+    for (int64_t b : cached)
+      if (b < hi && !pure_ok(b)) lo = std::max(lo, b);
+    int64_t best = bisect(lo, hi, [&](int64_t b) { return pure_ok(b); });
+    return at_budget(best).budget;
+  }
+
+  // pipeline._truncation_search for one planes variant -> t or -1
+  int64_t search_trunc(int pi, int64_t total) {
+    auto err_at = [&](int64_t t) -> double {
+      auto it = trunc[pi].find(t);
+      if (it == trunc[pi].end()) throw NeedTrunc{pi, t};
+      n_trunc_calls++;
+      return it->second;
+    };
+    n_trunc_calls = 0;
+    if (err_at(0) <= eps_abs) return 0;
+    if (err_at(total) > eps_abs) return -1;
+    return bisect(0, total, [&](int64_t t) { return err_at(t) <= eps_abs; });
+  }
+};
+
+// ---------------------------------------------------------------------------
+struct Workspace {
+  Geo g{};
+  int cap = 0;  // fields
+  float* x32 = nullptr;
+  double *norm = nullptr, *A = nullptr, *B = nullptr, *base_dec = nullptr;
+  int16_t *ec = nullptr, *ed = nullptr, *el = nullptr;
+  uint32_t *mant = nullptr, *sign_pos = nullptr, *lsp_rank = nullptr;
+  uint8_t* pinfo = nullptr;
+  uint32_t *lip = nullptr, *lis0 = nullptr, *lis1 = nullptr, *w0 = nullptr, *w1 = nullptr,
+           *lsp = nullptr;
+  uint32_t *bits_base = nullptr, *bits_res = nullptr;
+  int64_t words_base = 0, words_res = 0;
+  PlaneRec *pl_base = nullptr, *pl_res = nullptr;
+  MachineOut *mo_base = nullptr, *mo_res = nullptr;
+  FieldScal* fs = nullptr;
+  ProbeParam* prm = nullptr;
+  ProbeResult* res = nullptr;
+  uint64_t* limit = nullptr;
+  uint8_t* active = nullptr;
+  TreeTables tt{};
+  bool has_tt = false;
+
+  void release() {
+    void* ptrs[] = {x32, norm, A, B, base_dec, ec, ed, el, mant, sign_pos, lsp_rank, pinfo,
+                    lip, lis0, lis1, w0, w1, lsp, bits_base, bits_res, pl_base, pl_res,
+                    mo_base, mo_res, fs, prm, res, limit, active};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (has_tt) free_tree_tables(tt);
+    *this = Workspace{};
+  }
+};
+
+int64_t words_for(int64_t n, int planes) {
+  // per plane <= |LIP|+|LSP| (<= n) + LIS bits (<= 2n/3); plus children and
+  // sign bits (<= 2n over the whole stream)
+  int64_t bits = (int64_t)planes * (n + (2 * n) / 3 + 8) + 2 * n + 1024;
+  return bits / 32 + 64;
+}
+
+}  // namespace
+
+struct ebcc_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  Workspace ws;
+  // last compress result
+  uint8_t* d_payload = nullptr;
+  int64_t payload_cap = 0, payload_total = 0;
+  PackPart* d_parts = nullptr;
+  int parts_cap = 0;
+  uint8_t* d_stage = nullptr;
+  int64_t stage_cap = 0;
+  float* d_out = nullptr;
+  int64_t out_cap = 0;
+  ebcc_stats stats{};
+  cudaEvent_t ev[8] = {};
+};
+
+namespace {
+
+void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
+  Workspace& w = c->ws;
+  bool same_geo = w.g.rows == g.rows && w.g.cols == g.cols && w.g.levels == g.levels;
+  if (same_geo && w.cap >= nfields) return;
+  int cap = std::max(nfields, same_geo ? w.cap : 0);
+  w.release();
+  w.g = g;
+  w.cap = cap;
+  const int64_t N = g.n * cap;
+  w.x32 = dalloc<float>(N);
+  w.norm = dalloc<double>(N);
+  w.A = dalloc<double>(N);
+  w.B = dalloc<double>(N);
+  w.base_dec = dalloc<double>(N);
+  w.ec = dalloc<int16_t>(N);
+  w.ed = dalloc<int16_t>(N);
+  w.el = dalloc<int16_t>(N);
+  w.mant = dalloc<uint32_t>(N);
+  w.sign_pos = dalloc<uint32_t>(N);
+  w.lsp_rank = dalloc<uint32_t>(N);
+  w.pinfo = dalloc<uint8_t>(N);
+  w.lip = dalloc<uint32_t>(N);
+  w.lis0 = dalloc<uint32_t>(N);
+  w.lis1 = dalloc<uint32_t>(N);
+  w.w0 = dalloc<uint32_t>(N);
+  w.w1 = dalloc<uint32_t>(N);
+  w.lsp = dalloc<uint32_t>(N);
+  w.words_base = words_for(g.n, kBasePlanes);
+  w.words_res = words_for(g.n, kMaxDecodePlanes > kDeepPlanes ? kDeepPlanes : kDeepPlanes);
+  w.bits_base = dalloc<uint32_t>(w.words_base * cap);
+  w.bits_res = dalloc<uint32_t>(w.words_res * cap);
+  w.pl_base = dalloc<PlaneRec>((size_t)kMaxPlaneRecs * cap);
+  w.pl_res = dalloc<PlaneRec>((size_t)kMaxPlaneRecs * cap);
+  w.mo_base = dalloc<MachineOut>(cap);
+  w.mo_res = dalloc<MachineOut>(cap);
+  w.fs = dalloc<FieldScal>(cap);
+  w.prm = dalloc<ProbeParam>(cap);
+  w.res = dalloc<ProbeResult>(cap);
+  w.limit = dalloc<uint64_t>(cap);
+  w.active = dalloc<uint8_t>(cap);
+  build_tree_tables(g, w.tt, c->stream);
+  w.has_tt = true;
+}
+
+MachineBufs machine_bufs(Workspace& w, int nfields, bool residual) {
+  MachineBufs mb{};
+  mb.nfields = nfields;
+  mb.stride = w.g.n;
+  mb.bit_stride = residual ? w.words_res : w.words_base;
+  mb.ec = w.ec; mb.ed = w.ed; mb.el = w.el;
+  mb.mant = w.mant; mb.sign_pos = w.sign_pos; mb.lsp_rank = w.lsp_rank; mb.pinfo = w.pinfo;
+  mb.lip = w.lip; mb.lis0 = w.lis0; mb.lis1 = w.lis1; mb.w0 = w.w0; mb.w1 = w.w1; mb.lsp = w.lsp;
+  mb.bits = residual ? w.bits_res : w.bits_base;
+  mb.planes = residual ? w.pl_res : w.pl_base;
+  mb.out = residual ? w.mo_res : w.mo_base;
+  mb.limit = w.limit;
+  mb.active = w.active;
+  return mb;
+}
+
+Meta meta_of(Workspace& w, bool residual) {
+  Meta m{};
+  m.mant = w.mant; m.sign_pos = w.sign_pos; m.lsp_rank = w.lsp_rank; m.pinfo = w.pinfo;
+  m.planes = residual ? w.pl_res : w.pl_base;
+  m.mo = residual ? w.mo_res : w.mo_base;
+  m.stride = w.g.n;
+  return m;
+}
+
+// encode the pyramid currently in w.A (all fields): exponents, machine,
+// refinement.  Returns per-field machine summaries and plane records.
+void encode_pyramids(ebcc_ctx* c, int nfields, bool residual, int planes,
+                     const std::vector<uint8_t>& active, std::vector<MachineOut>& mo,
+                     std::vector<PlaneRec>& pl) {
+  Workspace& w = c->ws;
+  cudaStream_t st = c->stream;
+  MachineBufs mb = machine_bufs(w, nfields, residual);
+  std::vector<MachineOut> init(nfields);
+  for (auto& m : init) { m = MachineOut{}; m.n_max = kExpNone; }
+  CK(cudaMemcpyAsync(mb.out, init.data(), sizeof(MachineOut) * nfields, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(mb.bits, 0, sizeof(uint32_t) * mb.bit_stride * nfields, st));
+  coef_prepare(w.A, w.g.n, mb, w.g, st);
+  subtree_exponents(mb, w.g, w.tt, st);
+  c->stats.kernel_launches += 2 + w.g.levels;
+  // fields whose pyramid is all zero (n_max sentinel) skip the machine
+  CK(cudaMemcpyAsync(mo.data(), mb.out, sizeof(MachineOut) * nfields, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<uint8_t> act(nfields);
+  for (int f = 0; f < nfields; f++) act[f] = active[f] && mo[f].n_max != kExpNone;
+  CK(cudaMemcpyAsync(w.active, act.data(), nfields, cudaMemcpyHostToDevice, st));
+  run_machine(false, mb, w.g, w.tt, planes, st);
+  write_refinement(mb, planes, st);
+  c->stats.kernel_launches += 2;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(mo.data(), mb.out, sizeof(MachineOut) * nfields, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(pl.data(), mb.planes, sizeof(PlaneRec) * kMaxPlaneRecs * nfields,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int f = 0; f < nfields; f++)
+    if (act[f] && mo[f].overflow) throw CudaFail{cudaErrorMemoryAllocation, "machine capacity"};
+}
+
+// midpoint stopping plane of a decode of B bits of the `planes`-plane variant
+// (decode_with_plane, spiht.py:426-478, incl. zero-padded phantom planes)
+int n_last_of(const MachineOut& mo, const PlaneRec* pl, int planes, uint64_t B, uint64_t T) {
+  if (B == 0) return mo.n_max;
+  if (B <= T) {
+    int p = 0;
+    for (int k = 0; k < planes; k++)
+      if (pl[k].start < B) p = k;
+    return mo.n_max - p;
+  }
+  uint64_t L = pl[planes - 1].lists_end;
+  int jmax;
+  if (L == 0) jmax = (kMaxDecodePlanes - 1) - planes;
+  else {
+    uint64_t j = (B - T + L - 1) / L - 1;  // last j with T + j*L < B
+    jmax = (int)std::min<uint64_t>(j, (uint64_t)((kMaxDecodePlanes - 1) - planes));
+  }
+  return mo.n_max - (planes + jmax);
+}
+
+void put_header(uint8_t* h, int n_max, int levels, int rows, int cols) {
+  h[0] = 'S'; h[1] = 'P';
+  h[2] = (uint8_t)(int8_t)n_max;
+  h[3] = (uint8_t)levels;
+  uint32_t r = (uint32_t)rows, cc = (uint32_t)cols;
+  memcpy(h + 4, &r, 4);
+  memcpy(h + 8, &cc, 4);
+}
+
+struct EventTimer {
+  ebcc_ctx* c;
+  cudaEvent_t a, b;
+  double* acc;
+  EventTimer(ebcc_ctx* c_, double* acc_) : c(c_), acc(acc_) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, c->stream);
+  }
+  ~EventTimer() {
+    cudaEventRecord(b, c->stream);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    *acc += ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+// one compress batch of nfields (<= workspace capacity); x already in w.x32
+int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0, double tol,
+                   ebcc_chunk_rec* recs, int64_t out_base_off, std::vector<PackPart>& parts,
+                   std::vector<int64_t>& sizes) {
+  Workspace& w = c->ws;
+  const Geo& g = w.g;
+  cudaStream_t st = c->stream;
+  const int64_t N = g.n;
+
+  // ---- ingest + normalise (core.normalize) ----
+  ingest_normalize(w.x32, N, nfields, w.norm, w.fs, eps_rel, st);
+  c->stats.kernel_launches += 3;
+  std::vector<FieldScal> fs(nfields);
+  CK(cudaMemcpyAsync(fs.data(), w.fs, sizeof(FieldScal) * nfields, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+
+  std::vector<ChunkSearch> cs(nfields);
+  std::vector<uint8_t> active(nfields);
+  for (int f = 0; f < nfields; f++) {
+    ChunkSearch& s = cs[f];
+    s.n = N; s.raw = N * 4; s.q = q; s.r0 = r0; s.tol = tol; s.eps_abs = fs[f].eps_abs;
+    s.constant = fs[f].constant != 0;
+    active[f] = !s.constant;
+    if (s.constant) s.phase = 3;
+  }
+
+  // ---- base pyramid + full 24-plane encode (once; every budget is a prefix) ----
+  std::vector<MachineOut> mo(nfields);
+  std::vector<PlaneRec> pl((size_t)kMaxPlaneRecs * nfields);
+  {
+    EventTimer t(c, &c->stats.ms_encode);
+    CK(cudaMemcpyAsync(w.A, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
+    forward_dwt(w.A, w.B, N, nfields, g, st);
+    c->stats.kernel_launches += 2 * g.levels;
+    encode_pyramids(c, nfields, false, kBasePlanes, active, mo, pl);
+  }
+  for (int f = 0; f < nfields; f++) cs[f].T_base = active[f] ? mo[f].total_bits : 0;
+  std::vector<int> base_nmax(nfields);
+  for (int f = 0; f < nfields; f++) base_nmax[f] = mo[f].n_max;
+
+  std::vector<ProbeParam> prm(nfields);
+  std::vector<ProbeResult> res(nfields);
+  Meta mbase = meta_of(w, false);
+
+  // ---- base-memo searches (phase 0: quantile search, phase 1: pure) ----
+  std::vector<size_t> base_entries(nfields, 0);
+  for (int phase = 0; phase < 2; phase++) {
+    for (;;) {
+      bool any = false;
+      for (int f = 0; f < nfields; f++) {
+        ChunkSearch& s = cs[f];
+        prm[f] = ProbeParam{};
+        if (s.constant) continue;
+        try {
+          if (phase == 0) s.base_budget = s.search_base();
+          else s.pure_budget = s.search_pure(base_entries[f]);
+        } catch (NeedBase& nb) {
+          int64_t len = s.stream_len(nb.budget);
+          uint64_t B = (uint64_t)(len - kHeader) * 8;
+          if (B > s.T_base) B = s.T_base;
+          prm[f].B = B;
+          prm[f].planes = kBasePlanes;
+          prm[f].active = 1;
+          any = true;
+        }
+      }
+      if (!any) break;
+      EventTimer t(c, &c->stats.ms_probe);
+      CK(cudaMemcpyAsync(w.prm, prm.data(), sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
+      probe_base(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.x32, w.fs, w.res, st);
+      c->stats.kernel_launches += 1 + 2 * g.levels;
+      c->stats.probe_launches++;
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(res.data(), w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int f = 0; f < nfields; f++) {
+        if (!prm[f].active) continue;
+        ChunkSearch& s = cs[f];
+        // recover the budget this probe answered (same replay throws the same)
+        int64_t b;
+        try {
+          if (phase == 0) s.search_base(); else s.search_pure(base_entries[f]);
+          continue;  // unreachable
+        } catch (NeedBase& nb) { b = nb.budget; }
+        Entry e;
+        e.budget = b;
+        e.len = s.stream_len(b);
+        e.count = res[f].count;
+        uint64_t bitsv = res[f].maxerr;
+        memcpy(&e.maxerr, &bitsv, 8);
+        s.at[b] = (int)s.memo.size();
+        s.memo.push_back(e);
+      }
+    }
+    if (phase == 0)
+      for (int f = 0; f < nfields; f++) base_entries[f] = cs[f].memo.size();
+  }
+
+  // ---- residue = norm - base decode at the chosen budget; residual encode ----
+  for (int f = 0; f < nfields; f++) {
+    prm[f] = ProbeParam{};
+    if (cs[f].constant) continue;
+    int64_t len = cs[f].stream_len(cs[f].base_budget);
+    uint64_t B = (uint64_t)(len - kHeader) * 8;
+    if (B > cs[f].T_base) B = cs[f].T_base;
+    prm[f].B = B; prm[f].planes = kBasePlanes; prm[f].active = 1;
+  }
+  std::vector<MachineOut> rmo(nfields);
+  std::vector<PlaneRec> rpl((size_t)kMaxPlaneRecs * nfields);
+  {
+    EventTimer t(c, &c->stats.ms_encode);
+    CK(cudaMemcpyAsync(w.prm, prm.data(), sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
+    // resid overwrites norm in place (norm is not needed after the base searches)
+    base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
+    c->stats.kernel_launches += 1 + 2 * g.levels;
+    CK(cudaMemcpyAsync(w.A, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
+    forward_dwt(w.A, w.B, N, nfields, g, st);
+    c->stats.kernel_launches += 2 * g.levels;
+    encode_pyramids(c, nfields, true, kDeepPlanes, active, rmo, rpl);
+  }
+  Meta mres = meta_of(w, true);
+  // stream totals of the 24- and 32-plane variants
+  std::vector<uint64_t> T24(nfields, 0), T32(nfields, 0);
+  for (int f = 0; f < nfields; f++) {
+    if (!active[f] || rmo[f].n_max == kExpNone) continue;
+    const PlaneRec* p = &rpl[(size_t)f * kMaxPlaneRecs];
+    T32[f] = rmo[f].total_bits;
+    T24[f] = p[kBasePlanes].start;
+  }
+  auto total_bytes = [&](int f, int pi) -> int64_t {
+    uint64_t T = pi == 0 ? T24[f] : T32[f];
+    return (int64_t)((T + 7) / 8);
+  };
+
+  // ---- truncation search (24 planes, then 32) ----
+  std::vector<int> pass(nfields, 0);
+  std::vector<int> trunc_calls(nfields, 0);
+  for (;;) {
+    bool any = false;
+    for (int f = 0; f < nfields; f++) {
+      ChunkSearch& s = cs[f];
+      prm[f] = ProbeParam{};
+      if (s.constant || s.trunc_planes || pass[f] > 1) continue;
+      for (;;) {
+        try {
+          int64_t t = s.search_trunc(pass[f], total_bytes(f, pass[f]));
+          if (t >= 0) {
+            s.trunc_t = t;
+            s.trunc_planes = pass[f] == 0 ? kBasePlanes : kDeepPlanes;
+            trunc_calls[f] += s.n_trunc_calls;
+            break;
+          }
+          trunc_calls[f] += s.n_trunc_calls;
+          pass[f]++;
+          if (pass[f] > 1) break;
+        } catch (NeedTrunc& nt) {
+          int P = nt.planes == 0 ? kBasePlanes : kDeepPlanes;
+          uint64_t T = nt.planes == 0 ? T24[f] : T32[f];
+          uint64_t Bfull = (uint64_t)nt.t * 8;
+          prm[f].B = Bfull < T ? Bfull : T;
+          prm[f].planes = P;
+          prm[f].midpoint = 1;
+          prm[f].n_last = rmo[f].n_max == kExpNone
+                              ? 0
+                              : n_last_of(rmo[f], &rpl[(size_t)f * kMaxPlaneRecs], P, Bfull, T);
+          prm[f].active = 1;
+          any = true;
+          break;
+        }
+      }
+    }
+    if (!any) break;
+    EventTimer t(c, &c->stats.ms_probe);
+    CK(cudaMemcpyAsync(w.prm, prm.data(), sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
+    probe_trunc(mres, w.prm, w.A, w.B, g, nfields, w.base_dec, w.x32, w.fs, w.res, st);
+    c->stats.kernel_launches += 1 + 2 * g.levels;
+    c->stats.probe_launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(res.data(), w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int f = 0; f < nfields; f++) {
+      if (!prm[f].active) continue;
+      ChunkSearch& s = cs[f];
+      try {
+        s.search_trunc(pass[f], total_bytes(f, pass[f]));
+      } catch (NeedTrunc& nt) {
+        double e;
+        uint64_t bitsv = res[f].maxerr;
+        memcpy(&e, &bitsv, 8);
+        s.trunc[nt.planes][nt.t] = e;
+      }
+    }
+  }
+
+  // ---- candidate choice (pipeline.py:315-329) + payload parts ----
+  int status = EBCC_OK;
+  for (int f = 0; f < nfields; f++) {
+    ebcc_chunk_rec& r = recs[f];
+    ChunkSearch& s = cs[f];
+    memset(&r, 0, sizeof(r));
+    r.vmin = fs[f].vmin;
+    r.vmax = fs[f].vmax;
+    r.n_base_probes = (int32_t)s.memo.size();
+    r.n_trunc_probes = trunc_calls[f];
+    if (s.constant) {
+      r.mode = EBCC_MODE_CONSTANT;
+      sizes.push_back(0);
+      continue;
+    }
+    int64_t pure_len = s.pure_budget >= 0 ? s.stream_len(s.pure_budget) : -1;
+    int64_t base_len = s.stream_len(s.base_budget);
+    int64_t two_len = s.trunc_t >= 0 ? base_len + kHeader + s.trunc_t : -1;
+    if (pure_len < 0 && two_len < 0) {
+      r.status = EBCC_E_RESIDUAL;
+      status = EBCC_E_RESIDUAL;
+      sizes.push_back(0);
+      continue;
+    }
+    if (base_nmax[f] < -128 || base_nmax[f] > 127 ||
+        (rmo[f].n_max != kExpNone && (rmo[f].n_max < -128 || rmo[f].n_max > 127)))
+      throw CudaFail{cudaErrorInvalidValue, "stream exponent out of int8 range"};
+    int64_t off = out_base_off;
+    for (int64_t z : sizes) off += z;
+    PackPart bp{};
+    bp.src = w.bits_base + (int64_t)f * w.words_base;
+    bp.bit_limit = ~0ull;
+    put_header(bp.hdr, base_nmax[f], g.levels, g.rows, g.cols);
+    if (pure_len >= 0 && (two_len < 0 || pure_len <= two_len)) {
+      r.mode = EBCC_MODE_PURE_BASE;
+      r.base_len = pure_len;
+      r.resid_len = 0;
+      bp.dst_off = (uint64_t)off;
+      bp.nbytes = (uint64_t)pure_len;
+      parts.push_back(bp);
+      sizes.push_back(pure_len);
+    } else {
+      r.mode = EBCC_MODE_TWO_LAYER;
+      r.base_len = base_len;
+      r.resid_len = kHeader + s.trunc_t;
+      r.resid_planes = s.trunc_planes;
+      bp.dst_off = (uint64_t)off;
+      bp.nbytes = (uint64_t)base_len;
+      parts.push_back(bp);
+      PackPart rp{};
+      rp.src = w.bits_res + (int64_t)f * w.words_res;
+      rp.dst_off = (uint64_t)(off + base_len);
+      rp.nbytes = (uint64_t)(kHeader + s.trunc_t);
+      rp.bit_limit = s.trunc_planes == kBasePlanes ? T24[f] : T32[f];
+      int rn = rmo[f].n_max == kExpNone ? kZeroSentinel : rmo[f].n_max;
+      put_header(rp.hdr, rn, g.levels, g.rows, g.cols);
+      parts.push_back(rp);
+      sizes.push_back(two_len);
+    }
+  }
+  return status;
+}
+
+int fail(ebcc_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+extern "C" {
+
+int ebcc_abi_version(void) { return EBCC_ABI_VERSION; }
+
+int ebcc_create(int32_t device, ebcc_ctx** out) {
+  if (!out) return EBCC_E_ARGUMENT;
+  *out = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return EBCC_E_CUDA;
+  ebcc_ctx* c = new ebcc_ctx();
+  c->device = device;
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { delete c; return EBCC_E_CUDA; }
+  c->own_stream = true;
+  *out = c;
+  return EBCC_OK;
+}
+
+void ebcc_destroy(ebcc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  c->ws.release();
+  if (c->d_payload) cudaFree(c->d_payload);
+  if (c->d_parts) cudaFree(c->d_parts);
+  if (c->d_stage) cudaFree(c->d_stage);
+  if (c->d_out) cudaFree(c->d_out);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int ebcc_set_stream(ebcc_ctx* c, void* s) {
+  if (!c) return EBCC_E_ARGUMENT;
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  c->stream = static_cast<cudaStream_t>(s);
+  c->own_stream = false;
+  return EBCC_OK;
+}
+
+const char* ebcc_last_error(const ebcc_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int ebcc_get_stats(const ebcc_ctx* c, ebcc_stats* out) {
+  if (!c || !out) return EBCC_E_ARGUMENT;
+  *out = c->stats;
+  return EBCC_OK;
+}
+
+int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t rows, int32_t cols,
+                  double eps_rel, double q, double r0, double search_tol, int32_t flags,
+                  ebcc_chunk_rec* recs, uint8_t* payload, int64_t payload_cap,
+                  int64_t* payload_offsets, int64_t* payload_total) {
+  if (!c || !fields || !recs || nfields < 0 || rows < 1 || cols < 1)
+    return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  // EbccParams.validate (pipeline.py:54-62)
+  if (!(eps_rel > 0.0 && eps_rel < 1.0))
+    return fail(c, EBCC_E_ARGUMENT, "epsilon_rel must be in (0, 1)");
+  if (!(q > 0.0 && q <= 1.0)) return fail(c, EBCC_E_ARGUMENT, "q must be in (0, 1]");
+  if (r0 < 1.0) return fail(c, EBCC_E_ARGUMENT, "r0 must be >= 1");
+  if (!(search_tol > 0.0)) return fail(c, EBCC_E_ARGUMENT, "search_tol must be positive");
+  if ((int64_t)rows * cols >= (1ll << 31)) return fail(c, EBCC_E_ARGUMENT, "chunk too large");
+  c->stats = ebcc_stats{};
+  c->err.clear();
+  try {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    int levels = clamp_levels(rows, cols, default_levels(rows, cols));
+    Geo g = make_geo(rows, cols, levels);
+    // batch capacity from free memory (~100 B per point per field in flight)
+    size_t freeb = 0, totalb = 0;
+    CK(cudaMemGetInfo(&freeb, &totalb));
+    int64_t per_field = g.n * 104 + 4096;
+    int64_t cap = (int64_t)((freeb * 0.6) / per_field);
+    if (cap < 1) cap = 1;
+    if (cap > nfields) cap = nfields;
+    if (cap > 4096) cap = 4096;
+    cudaEvent_t t0, t1;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, st);
+    std::vector<PackPart> parts;
+    std::vector<int64_t> sizes;
+    int status = EBCC_OK;
+    for (int64_t f0 = 0; f0 < nfields; f0 += cap) {
+      int nb = (int)std::min<int64_t>(cap, nfields - f0);
+      ensure_workspace(c, g, nb);
+      CK(cudaMemcpyAsync(c->ws.x32, fields + f0 * g.n, sizeof(float) * g.n * nb,
+                         (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
+                                                        : cudaMemcpyHostToDevice,
+                         st));
+      std::vector<PackPart> bparts;
+      int64_t done = 0;
+      for (int64_t z : sizes) done += z;
+      std::vector<int64_t> bsizes;
+      int s = compress_batch(c, nb, eps_rel, q, r0, search_tol, recs + f0, done, bparts, bsizes);
+      if (s != EBCC_OK) status = s;
+      // pack this batch now: the stream buffers are reused by the next batch
+      int64_t bytes = done;
+      for (int64_t z : bsizes) bytes += z;
+      if (bytes > c->payload_cap) {
+        // grow, preserving what earlier batches packed
+        uint8_t* nbuf = dalloc<uint8_t>((size_t)std::max<int64_t>(bytes * 2, 1 << 20));
+        if (c->d_payload && done) CK(cudaMemcpyAsync(nbuf, c->d_payload, done, cudaMemcpyDeviceToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        if (c->d_payload) cudaFree(c->d_payload);
+        c->d_payload = nbuf;
+        c->payload_cap = std::max<int64_t>(bytes * 2, 1 << 20);
+      }
+      if (!bparts.empty()) {
+        if ((int)bparts.size() > c->parts_cap) {
+          if (c->d_parts) cudaFree(c->d_parts);
+          c->parts_cap = (int)bparts.size() * 2;
+          c->d_parts = dalloc<PackPart>(c->parts_cap);
+        }
+        CK(cudaMemcpyAsync(c->d_parts, bparts.data(), sizeof(PackPart) * bparts.size(),
+                           cudaMemcpyHostToDevice, st));
+        pack_parts(c->d_parts, (int)bparts.size(), c->d_payload, st);
+        c->stats.kernel_launches++;
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+      }
+      sizes.insert(sizes.end(), bsizes.begin(), bsizes.end());
+    }
+    int64_t total = 0;
+    for (int64_t f = 0; f < nfields; f++) {
+      if (payload_offsets) payload_offsets[f] = total;
+      total += sizes[f];
+    }
+    c->payload_total = total;
+    if (payload_total) *payload_total = total;
+    cudaEventRecord(t1, st);
+    cudaEventSynchronize(t1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    c->stats.ms_total = ms;
+    c->stats.ms_other = ms - c->stats.ms_encode - c->stats.ms_probe;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    if (status != EBCC_OK) {
+      for (int64_t f = 0; f < nfields; f++)
+        if (recs[f].status == EBCC_E_RESIDUAL)
+          return fail(c, EBCC_E_RESIDUAL,
+                      "chunk " + std::to_string(f) + ": no encoding reaches epsilon_rel");
+    }
+    if (payload && total > 0) {
+      if (total > payload_cap) return fail(c, EBCC_E_CAPACITY, "payload buffer too small");
+      CK(cudaMemcpyAsync(payload, c->d_payload, total,
+                         (flags & EBCC_OUTPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
+                                                         : cudaMemcpyDeviceToHost,
+                         st));
+      CK(cudaStreamSynchronize(st));
+    }
+    return EBCC_OK;
+  } catch (CudaFail& e) {
+    cudaGetLastError();
+    return fail(c, e.e == cudaErrorMemoryAllocation ? EBCC_E_NOMEM : EBCC_E_CUDA,
+                std::string(e.what) + ": " + cudaGetErrorString(e.e));
+  } catch (std::exception& e) {
+    return fail(c, EBCC_E_CUDA, e.what());
+  }
+}
+
+int ebcc_fetch_payload(ebcc_ctx* c, uint8_t* payload, int64_t cap, int32_t flags) {
+  if (!c || !payload) return EBCC_E_ARGUMENT;
+  if (cap < c->payload_total) return fail(c, EBCC_E_CAPACITY, "payload buffer too small");
+  if (!c->payload_total) return EBCC_OK;
+  cudaError_t e = cudaMemcpyAsync(payload, c->d_payload, c->payload_total,
+                                  (flags & EBCC_OUTPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
+                                                                  : cudaMemcpyDeviceToHost,
+                                  c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  return e == cudaSuccess ? EBCC_OK : fail(c, EBCC_E_CUDA, cudaGetErrorString(e));
+}
+
+int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
+                    const ebcc_chunk_rec* recs, int64_t nfields, int32_t rows, int32_t cols,
+                    int32_t levels, int32_t flags, float* out) {
+  if (!c || !recs || !out || nfields < 0 || rows < 1 || cols < 1 || levels < 1 ||
+      levels > kMaxLevels)
+    return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  c->stats = ebcc_stats{};
+  c->err.clear();
+  try {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    Geo g = make_geo(rows, cols, levels);
+    cudaEvent_t t0, t1;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, st);
+    size_t freeb = 0, totalb = 0;
+    CK(cudaMemGetInfo(&freeb, &totalb));
+    int64_t per_field = g.n * 104 + 4096;
+    int64_t cap = (int64_t)((freeb * 0.6) / per_field);
+    if (cap < 1) cap = 1;
+    if (cap > nfields) cap = nfields;
+    if (cap > 4096) cap = 4096;
+    for (int64_t f0 = 0; f0 < nfields; f0 += cap) {
+      int nb = (int)std::min<int64_t>(cap, nfields - f0);
+      ensure_workspace(c, g, nb);
+      Workspace& w = c->ws;
+      // gather this batch's payload bytes into a staging buffer
+      int64_t lo = INT64_MAX, hi = 0;
+      for (int i = 0; i < nb; i++) {
+        const ebcc_chunk_rec& r = recs[f0 + i];
+        if (r.mode == EBCC_MODE_CONSTANT) continue;
+        int64_t o = offsets[f0 + i];
+        lo = std::min(lo, o);
+        hi = std::max(hi, o + r.base_len + r.resid_len);
+      }
+      std::vector<UnpackPart> up;
+      std::vector<MachineOut> bmo(nb), rmo(nb);
+      std::vector<uint64_t> blim(nb, 0), rlim(nb, 0);
+      std::vector<uint8_t> bact(nb, 0), ract(nb, 0), pure(nb, 0), cst(nb, 0);
+      std::vector<FieldScal> fsv(nb);
+      for (int i = 0; i < nb; i++) {
+        const ebcc_chunk_rec& r = recs[f0 + i];
+        fsv[i] = FieldScal{};
+        fsv[i].vmin = r.vmin; fsv[i].vmax = r.vmax; fsv[i].range = r.vmax - r.vmin;
+        bmo[i] = MachineOut{}; rmo[i] = MachineOut{};
+        bmo[i].n_max = kExpNone; rmo[i].n_max = kExpNone;
+        if (r.mode == EBCC_MODE_CONSTANT) { cst[i] = 1; continue; }
+        if (r.base_len < kHeader || (r.mode == EBCC_MODE_TWO_LAYER && r.resid_len > 0 && r.resid_len < kHeader))
+          return fail(c, EBCC_E_FORMAT, "stream shorter than header");
+        const uint8_t* bh = nullptr;
+        uint8_t hb[kHeader], hr[kHeader];
+        if (flags & EBCC_INPUT_ON_DEVICE) {
+          CK(cudaMemcpy(hb, payload + offsets[f0 + i], kHeader, cudaMemcpyDeviceToHost));
+          bh = hb;
+        } else {
+          bh = payload + offsets[f0 + i];
+        }
+        int nb_max = (int8_t)bh[2];
+        bmo[i].n_max = nb_max == kZeroSentinel ? kExpNone : nb_max;
+        blim[i] = (uint64_t)(r.base_len - kHeader) * 8;
+        bact[i] = nb_max != kZeroSentinel;
+        up.push_back(UnpackPart{(uint64_t)(offsets[f0 + i] + kHeader - lo),
+                                (uint64_t)(r.base_len - kHeader),
+                                w.bits_base + (int64_t)i * w.words_base});
+        if (r.mode == EBCC_MODE_TWO_LAYER && r.resid_len > 0) {
+          const uint8_t* rh;
+          if (flags & EBCC_INPUT_ON_DEVICE) {
+            CK(cudaMemcpy(hr, payload + offsets[f0 + i] + r.base_len, kHeader, cudaMemcpyDeviceToHost));
+            rh = hr;
+          } else {
+            rh = payload + offsets[f0 + i] + r.base_len;
+          }
+          int rn = (int8_t)rh[2];
+          rmo[i].n_max = rn == kZeroSentinel ? kExpNone : rn;
+          rlim[i] = (uint64_t)(r.resid_len - kHeader) * 8;
+          ract[i] = 1;
+          up.push_back(UnpackPart{(uint64_t)(offsets[f0 + i] + r.base_len + kHeader - lo),
+                                  (uint64_t)(r.resid_len - kHeader),
+                                  w.bits_res + (int64_t)i * w.words_res});
+        } else {
+          pure[i] = 1;
+        }
+        if ((int64_t)((r.base_len - kHeader + 3) / 4) + 2 > w.words_base ||
+            (ract[i] && (int64_t)((r.resid_len - kHeader + 3) / 4) + 2 > w.words_res))
+          return fail(c, EBCC_E_FORMAT, "stream longer than any encoder output");
+      }
+      CK(cudaMemcpyAsync(w.fs, fsv.data(), sizeof(FieldScal) * nb, cudaMemcpyHostToDevice, st));
+      if (hi > lo) {
+        int64_t span = hi - lo;
+        if (span > c->stage_cap) {
+          if (c->d_stage) cudaFree(c->d_stage);
+          c->d_stage = dalloc<uint8_t>(span);
+          c->stage_cap = span;
+        }
+        CK(cudaMemcpyAsync(c->d_stage, payload + lo, span,
+                           (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
+                                                          : cudaMemcpyHostToDevice,
+                           st));
+        UnpackPart* dup = nullptr;
+        dup = dalloc<UnpackPart>(up.size());
+        CK(cudaMemcpyAsync(dup, up.data(), sizeof(UnpackPart) * up.size(), cudaMemcpyHostToDevice, st));
+        unpack_parts(dup, (int)up.size(), c->d_stage, st);
+        c->stats.kernel_launches++;
+        CK(cudaStreamSynchronize(st));
+        cudaFree(dup);
+      }
+      std::vector<ProbeParam> prm(nb);
+      float* dst = out + f0 * g.n;
+      float* out_dev = dst;
+      if (!(flags & EBCC_OUTPUT_ON_DEVICE)) {
+        if (c->out_cap < g.n * nb) {
+          if (c->d_out) cudaFree(c->d_out);
+          c->d_out = dalloc<float>(g.n * nb);
+          c->out_cap = g.n * nb;
+        }
+        out_dev = c->d_out;
+      }
+      // two decodes: base (lower bound) then residual (midpoint)
+      for (int layer = 0; layer < 2; layer++) {
+        bool resl = layer == 1;
+        std::vector<uint8_t>& act = resl ? ract : bact;
+        bool any = false;
+        for (int i = 0; i < nb; i++) any |= act[i] != 0;
+        if (resl && !any) break;
+        MachineBufs mb = machine_bufs(w, nb, resl);
+        CK(cudaMemcpyAsync(mb.out, resl ? rmo.data() : bmo.data(), sizeof(MachineOut) * nb,
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(w.limit, resl ? rlim.data() : blim.data(), sizeof(uint64_t) * nb,
+                           cudaMemcpyHostToDevice, st));
+        std::vector<uint8_t> mact(nb);
+        for (int i = 0; i < nb; i++)
+          mact[i] = act[i] && (resl ? rmo[i].n_max : bmo[i].n_max) != kExpNone;
+        CK(cudaMemcpyAsync(w.active, mact.data(), nb, cudaMemcpyHostToDevice, st));
+        decode_init(mb, st);
+        run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
+        gather_refinement(mb, st);
+        c->stats.kernel_launches += 3;
+        for (int i = 0; i < nb; i++) {
+          prm[i] = ProbeParam{};
+          prm[i].B = ~0ull;
+          prm[i].planes = -1;
+          prm[i].midpoint = resl ? 1 : 0;
+          prm[i].active = resl ? act[i] : !cst[i];
+        }
+        CK(cudaMemcpyAsync(w.prm, prm.data(), sizeof(ProbeParam) * nb, cudaMemcpyHostToDevice, st));
+        Meta m = meta_of(w, resl);
+        if (!resl) {
+          decode_field(m, w.prm, w.A, w.B, g, nb, w.base_dec, st);
+        } else {
+          decode_field_add_denorm(m, w.prm, w.A, w.B, g, nb, w.base_dec, w.fs, out_dev, st);
+        }
+        c->stats.kernel_launches += 1 + 2 * g.levels;
+        CK(cudaGetLastError());
+      }
+      CK(cudaMemcpyAsync(w.active, pure.data(), nb, cudaMemcpyHostToDevice, st));
+      denorm_only(w.base_dec, w.fs, w.active, g.n, nb, out_dev, st);
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpyAsync(w.active, cst.data(), nb, cudaMemcpyHostToDevice, st));
+      fill_constant(w.fs, w.active, g.n, nb, out_dev, st);
+      c->stats.kernel_launches += 2;
+      CK(cudaGetLastError());
+      if (!(flags & EBCC_OUTPUT_ON_DEVICE))
+        CK(cudaMemcpyAsync(dst, out_dev, sizeof(float) * g.n * nb, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    cudaEventRecord(t1, st);
+    cudaEventSynchronize(t1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    c->stats.ms_total = ms;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    return EBCC_OK;
+  } catch (CudaFail& e) {
+    cudaGetLastError();
+    return fail(c, e.e == cudaErrorMemoryAllocation ? EBCC_E_NOMEM : EBCC_E_CUDA,
+                std::string(e.what) + ": " + cudaGetErrorString(e.e));
+  } catch (std::exception& e) {
+    return fail(c, EBCC_E_CUDA, e.what());
+  }
+}
+
+int ebcc_dwt(ebcc_ctx* c, const double* in, double* out, int64_t nfields, int32_t rows,
+             int32_t cols, int32_t levels, int32_t inverse) {
+  if (!c || !in || !out || nfields < 1 || rows < 1 || cols < 1 || levels < 1 ||
+      levels > kMaxLevels)
+    return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  try {
+    CK(cudaSetDevice(c->device));
+    if (!inverse) levels = clamp_levels(rows, cols, levels);
+    Geo g = make_geo(rows, cols, levels);
+    ensure_workspace(c, g, (int)nfields);
+    Workspace& w = c->ws;
+    CK(cudaMemcpyAsync(w.A, in, sizeof(double) * g.n * nfields, cudaMemcpyHostToDevice, c->stream));
+    if (inverse) inverse_dwt(w.A, w.B, g.n, (int)nfields, g, c->stream);
+    else forward_dwt(w.A, w.B, g.n, (int)nfields, g, c->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, w.A, sizeof(double) * g.n * nfields, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return EBCC_OK;
+  } catch (CudaFail& e) {
+    cudaGetLastError();
+    return fail(c, EBCC_E_CUDA, std::string(e.what) + ": " + cudaGetErrorString(e.e));
+  }
+}
+
+int ebcc_spiht_encode(ebcc_ctx* c, const double* coeffs, int32_t rows, int32_t cols,
+                      int32_t levels, int32_t planes, uint8_t* out, int64_t cap, int64_t* len) {
+  if (!c || !coeffs || !out || rows < 1 || cols < 1 || levels < 1 || levels > kMaxLevels ||
+      planes < 1 || planes > kDeepPlanes || cap < kHeader)
+    return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  try {
+    CK(cudaSetDevice(c->device));
+    Geo g = make_geo(rows, cols, levels);
+    ensure_workspace(c, g, 1);
+    Workspace& w = c->ws;
+    CK(cudaMemcpyAsync(w.A, coeffs, sizeof(double) * g.n, cudaMemcpyHostToDevice, c->stream));
+    std::vector<uint8_t> act(1, 1);
+    std::vector<MachineOut> mo(1);
+    std::vector<PlaneRec> pl(kMaxPlaneRecs);
+    encode_pyramids(c, 1, true, planes, act, mo, pl);
+    uint8_t hdr[kHeader];
+    if (mo[0].n_max == kExpNone) {
+      put_header(hdr, kZeroSentinel, levels, rows, cols);
+      memcpy(out, hdr, kHeader);
+      *len = kHeader;
+      return EBCC_OK;
+    }
+    int64_t nbytes = kHeader + (int64_t)((mo[0].total_bits + 7) / 8);
+    *len = nbytes;
+    if (nbytes > cap) return fail(c, EBCC_E_CAPACITY, "output buffer too small");
+    put_header(out, mo[0].n_max, levels, rows, cols);
+    if (nbytes > kHeader)
+      CK(cudaMemcpy(out + kHeader, w.bits_res, nbytes - kHeader, cudaMemcpyDeviceToHost));
+    return EBCC_OK;
+  } catch (CudaFail& e) {
+    cudaGetLastError();
+    return fail(c, EBCC_E_CUDA, std::string(e.what) + ": " + cudaGetErrorString(e.e));
+  }
+}
+
+int ebcc_spiht_decode(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t prefix_len,
+                      int32_t rows, int32_t cols, double* coeffs_out, int32_t* n_last) {
+  if (!c || !data || !coeffs_out || !n_last || rows < 1 || cols < 1)
+    return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  if (len < kHeader || data[0] != 'S' || data[1] != 'P') return fail(c, EBCC_E_FORMAT, "bad header");
+  int levels = data[3];
+  uint32_t hr, hc;
+  memcpy(&hr, data + 4, 4);
+  memcpy(&hc, data + 8, 4);
+  if ((int)hr != rows || (int)hc != cols || levels < 1 || levels > kMaxLevels)
+    return fail(c, EBCC_E_FORMAT, "header does not match");
+  if (prefix_len < 0 || prefix_len > len) prefix_len = len;
+  try {
+    CK(cudaSetDevice(c->device));
+    Geo g = make_geo(rows, cols, levels);
+    ensure_workspace(c, g, 1);
+    Workspace& w = c->ws;
+    cudaStream_t st = c->stream;
+    int nm = (int8_t)data[2];
+    std::vector<MachineOut> mo(1);
+    mo[0] = MachineOut{};
+    mo[0].n_max = nm == kZeroSentinel ? kExpNone : nm;
+    uint64_t lim = prefix_len > kHeader ? (uint64_t)(prefix_len - kHeader) * 8 : 0;
+    int64_t pbytes = prefix_len > kHeader ? prefix_len - kHeader : 0;
+    if ((pbytes + 3) / 4 + 2 > w.words_res) return fail(c, EBCC_E_FORMAT, "stream too long");
+    CK(cudaMemsetAsync(w.bits_res, 0, sizeof(uint32_t) * w.words_res, st));
+    if (pbytes) CK(cudaMemcpyAsync(w.bits_res, data + kHeader, pbytes, cudaMemcpyHostToDevice, st));
+    MachineBufs mb = machine_bufs(w, 1, true);
+    CK(cudaMemcpyAsync(mb.out, mo.data(), sizeof(MachineOut), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.limit, &lim, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    uint8_t act = nm != kZeroSentinel;
+    CK(cudaMemcpyAsync(w.active, &act, 1, cudaMemcpyHostToDevice, st));
+    decode_init(mb, st);
+    run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
+    gather_refinement(mb, st);
+    ProbeParam p{};
+    p.B = ~0ull; p.planes = -1; p.active = 1;
+    CK(cudaMemcpyAsync(w.prm, &p, sizeof(p), cudaMemcpyHostToDevice, st));
+    decode_coeffs(meta_of(w, true), w.prm, w.A, g.n, 1, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(coeffs_out, w.A, sizeof(double) * g.n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(mo.data(), mb.out, sizeof(MachineOut), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (nm == kZeroSentinel) *n_last = -999;
+    else *n_last = mo[0].planes_run > 0 ? nm - (mo[0].planes_run - 1) : nm;
+    return EBCC_OK;
+  } catch (CudaFail& e) {
+    cudaGetLastError();
+    return fail(c, EBCC_E_CUDA, std::string(e.what) + ": " + cudaGetErrorString(e.e));
+  }
+}
+
+}  // extern "C"

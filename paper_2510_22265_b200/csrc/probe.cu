@@ -1,0 +1,364 @@
+// Field-level kernels of the EBCC path: the closed-form prefix decode and the
+// feedback probes built on the lifting passes.
+//
+// Closed form: decoding B stream bits leaves coefficient c at
+//   0                                   if its sign bit offset >= B
+//   sign * floor(|c| / 2^m) * 2^m       otherwise,
+// where m is the lowest plane whose refinement bit for c lies below B.  The
+// refinement bit of plane p for LSP rank r is at refine_start[p] + r, so m is
+// found by walking up from the significance plane through a 64-entry table.
+// The result is an exact float64 built from the top `kept` mantissa bits.
+// A probe = that decode + the inverse DWT + a reduction fused into the last
+// row pass; no intermediate field is written at level 0.
+#include "lift.cuh"
+#include "probe.cuh"
+
+namespace ebcc {
+
+namespace {
+
+__device__ __forceinline__ unsigned int f32_key(float v) {
+  unsigned int u = __float_as_uint(v);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key_f32(unsigned int k) {
+  unsigned int u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
+}
+
+__global__ void minmax_kernel(const float* __restrict__ x, int64_t n, unsigned int* mm) {
+  const int f = blockIdx.y;
+  const float* xf = x + (int64_t)f * n;
+  unsigned int lo = 0xffffffffu, hi = 0u;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned int k = f32_key(xf[i]);
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
+  }
+  for (int o = 16; o; o >>= 1) {
+    unsigned int a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[2 * f], lo);
+    atomicMax(&mm[2 * f + 1], hi);
+  }
+}
+
+// core.normalize (core.py:161-180) + _ChunkCoder.eps_abs (pipeline.py:98)
+__global__ void scalars_kernel(const unsigned int* mm, int nfields, double eps_rel, FieldScal* fs) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nfields) return;
+  double vmin = (double)key_f32(mm[2 * f]), vmax = (double)key_f32(mm[2 * f + 1]);
+  double range = __dsub_rn(vmax, vmin);
+  FieldScal s;
+  s.vmin = vmin; s.vmax = vmax; s.range = range;
+  s.eps_rel = eps_rel;
+  s.eps_abs = __dmul_rn(eps_rel, range);
+  s.constant = range < 1e-30;
+  s.pad = 0;
+  fs[f] = s;
+}
+
+__global__ void normalize_kernel(const float* __restrict__ x, int64_t n, const FieldScal* fs,
+                                 double* __restrict__ norm) {
+  const int f = blockIdx.y;
+  const FieldScal s = fs[f];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = (double)x[(int64_t)f * n + i];
+    norm[(int64_t)f * n + i] = s.constant ? 0.0 : __ddiv_rn(__dsub_rn(v, s.vmin), s.range);
+  }
+}
+
+__global__ void decode_coeffs_kernel(Meta m, const ProbeParam* __restrict__ prm,
+                                     double* __restrict__ out, int64_t n) {
+  const int f = blockIdx.y;
+  const ProbeParam P = prm[f];
+  if (!P.active) return;
+  __shared__ uint32_t rs[kMaxPlaneRecs];
+  const PlaneRec* pr = m.planes + (int64_t)f * kMaxPlaneRecs;
+  const int n_max = m.mo[f].n_max;
+  int planes = P.planes, n_last = P.n_last;
+  if (planes < 0) {  // decoder path: planes entered and n_last come from the machine
+    planes = m.mo[f].planes_run;
+    n_last = planes > 0 ? n_max - (planes - 1) : n_max;
+  }
+  for (int p = threadIdx.x; p < kMaxPlaneRecs; p += blockDim.x)
+    rs[p] = p < planes ? pr[p].refine_start : 0xffffffffu;
+  __syncthreads();
+  const int64_t fo = (int64_t)f * m.stride;
+  const double off = P.midpoint ? scalbn(0.5, n_last) : 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t sp = m.sign_pos[fo + i];
+    double v = 0.0;
+    if (sp != kNone && (uint64_t)sp < P.B) {
+      uint8_t pi = m.pinfo[fo + i];
+      int ps = pi & 0x3f;
+      uint64_t rank = m.lsp_rank[fo + i];
+      int lim = planes - 1 < ps + 31 ? planes - 1 : ps + 31;
+      int pm = ps;
+      while (pm < lim && (uint64_t)rs[pm + 1] + rank < P.B) pm++;
+      int kept = pm - ps + 1;
+      uint32_t K = m.mant[fo + i] >> (32 - kept);
+      v = scalbn((double)K, n_max - pm);
+      bool neg = pi & 0x80;
+      if (neg) v = -v;
+      if (P.midpoint) v = __dadd_rn(v, neg ? -off : off);
+    }
+    out[(int64_t)f * n + i] = v;
+  }
+}
+
+// ---- epilogues for the last (level-0 row) pass -----------------------------
+
+__device__ __forceinline__ double denorm_err(const FieldScal& s, double dec, float orig) {
+  // pipeline.py:116-119: rec = f32(vmin + dec*range); |f64(rec) - f64(orig)|
+  float rec = __double2float_rn(__dadd_rn(s.vmin, __dmul_rn(dec, s.range)));
+  return fabs(__dsub_rn((double)rec, (double)orig));
+}
+
+__device__ __forceinline__ void warp_flush(ProbeResult* r, unsigned long long cnt, double mx,
+                                           bool do_count) {
+  unsigned long long mxb = (unsigned long long)__double_as_longlong(mx);
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    unsigned long long y = __shfl_xor_sync(0xffffffffu, mxb, o);
+    mxb = y > mxb ? y : mxb;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (do_count && cnt) atomicAdd(&r->count, cnt);
+    atomicMax(&r->maxerr, mxb);
+  }
+}
+
+struct BaseProbeEpi {
+  const double* norm; const float* orig; const FieldScal* fs; const ProbeParam* prm;
+  ProbeResult* res; int64_t n;
+  unsigned long long cnt; double mx; FieldScal s;
+  __device__ bool begin(int f) {
+    cnt = 0; mx = 0.0;
+    if (!prm[f].active) return false;
+    s = fs[f];
+    return true;
+  }
+  __device__ void store(double*, int f, int64_t off, double dec) {
+    double nv = norm[(int64_t)f * n + off];
+    cnt += fabs(__dsub_rn(dec, nv)) <= s.eps_rel;
+    double e = denorm_err(s, dec, orig[(int64_t)f * n + off]);
+    mx = e > mx ? e : mx;
+  }
+  __device__ void finish(int f) { warp_flush(&res[f], cnt, mx, true); }
+};
+
+struct TruncProbeEpi {
+  const double* base; const float* orig; const FieldScal* fs; const ProbeParam* prm;
+  ProbeResult* res; int64_t n;
+  double mx; FieldScal s;
+  __device__ bool begin(int f) {
+    mx = 0.0;
+    if (!prm[f].active) return false;
+    s = fs[f];
+    return true;
+  }
+  __device__ void store(double*, int f, int64_t off, double v) {
+    double rec = __dadd_rn(base[(int64_t)f * n + off], v);  // base_field + dequantized
+    double e = denorm_err(s, rec, orig[(int64_t)f * n + off]);
+    mx = e > mx ? e : mx;
+  }
+  __device__ void finish(int f) { warp_flush(&res[f], 0, mx, false); }
+};
+
+struct ResidueEpi {
+  const double* norm; double* base_dec; double* resid; const ProbeParam* prm; int64_t n;
+  __device__ bool begin(int f) { return prm[f].active != 0; }
+  __device__ void store(double*, int f, int64_t off, double dec) {
+    int64_t o = (int64_t)f * n + off;
+    base_dec[o] = dec;
+    resid[o] = __dsub_rn(norm[o], dec);  // nc.values - base_enc.decoded
+  }
+  __device__ void finish(int) {}
+};
+
+struct StoreFieldEpi {
+  double* out; const ProbeParam* prm; int64_t n;
+  __device__ bool begin(int f) { return prm[f].active != 0; }
+  __device__ void store(double*, int f, int64_t off, double v) { out[(int64_t)f * n + off] = v; }
+  __device__ void finish(int) {}
+};
+
+struct AddDenormEpi {
+  const double* base; const FieldScal* fs; const ProbeParam* prm; float* out32; int64_t n;
+  FieldScal s;
+  __device__ bool begin(int f) {
+    if (!prm[f].active) return false;
+    s = fs[f];
+    return true;
+  }
+  __device__ void store(double*, int f, int64_t off, double v) {
+    int64_t o = (int64_t)f * n + off;
+    double fld = __dadd_rn(base[o], v);
+    out32[o] = __double2float_rn(__dadd_rn(s.vmin, __dmul_rn(fld, s.range)));
+  }
+  __device__ void finish(int) {}
+};
+
+// levels L-1..1 fully, then level 0 columns; leaves the level-0 row pass to
+// the caller's epilogue.  a holds coefficients on entry.
+void inverse_all_but_last(double* a, double* b, const Geo& g, int nfields, cudaStream_t st) {
+  for (int k = g.levels - 1; k >= 1; k--) {
+    inverse_level_cols(a, b, g.n, nfields, g, k, st);
+    inverse_level_rows(b, a, g.n, nfields, g, k, st);
+  }
+  inverse_level_cols(a, b, g.n, nfields, g, 0, st);
+}
+
+template <class Epi>
+void last_rows(const double* b, double* a, const Geo& g, int nfields, cudaStream_t st,
+               const Epi& epi) {
+  lift::launch_pass_epi<true, Epi>(b, a, g.n, nfields, g.cols, g.rows, g.cols, false, st, epi);
+}
+
+int grid_for(int64_t n, int cap = 2048) {
+  int64_t b = (n + 255) / 256;
+  return (int)(b > cap ? cap : (b < 1 ? 1 : b));
+}
+
+__global__ void denorm_kernel(const double* base, const FieldScal* fs, const uint8_t* active,
+                              int64_t n, float* out32) {
+  const int f = blockIdx.y;
+  if (!active[f]) return;
+  const FieldScal s = fs[f];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = (int64_t)f * n + i;
+    out32[o] = __double2float_rn(__dadd_rn(s.vmin, __dmul_rn(base[o], s.range)));
+  }
+}
+
+__global__ void fill_kernel(const FieldScal* fs, const uint8_t* active, int64_t n, float* out32) {
+  const int f = blockIdx.y;
+  if (!active[f]) return;
+  const float v = (float)fs[f].vmin;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out32[(int64_t)f * n + i] = v;
+}
+
+// one CTA per part; bytes are MSB-first stream bytes = little-endian words
+__global__ void pack_kernel(const PackPart* parts, uint8_t* out) {
+  const PackPart P = parts[blockIdx.x];
+  uint8_t* d = out + P.dst_off;
+  const uint8_t* s = reinterpret_cast<const uint8_t*>(P.src);
+  for (uint64_t i = threadIdx.x; i < P.nbytes; i += blockDim.x) {
+    uint8_t v;
+    if (i < (uint64_t)kHeader) {
+      v = P.hdr[i];
+    } else {
+      uint64_t j = i - kHeader;
+      v = s[j];
+      uint64_t bit0 = j * 8;
+      if (bit0 + 8 > P.bit_limit) {
+        int keep = bit0 >= P.bit_limit ? 0 : (int)(P.bit_limit - bit0);
+        v &= (uint8_t)(0xff00u >> keep);
+      }
+    }
+    d[i] = v;
+  }
+}
+
+__global__ void unpack_kernel(const UnpackPart* parts, const uint8_t* in) {
+  const UnpackPart P = parts[blockIdx.x];
+  uint8_t* d = reinterpret_cast<uint8_t*>(P.dst);
+  uint64_t padded = (P.nbytes + 7) & ~7ull;
+  for (uint64_t i = threadIdx.x; i < padded; i += blockDim.x)
+    d[i] = i < P.nbytes ? in[P.src_off + i] : 0;
+}
+
+}  // namespace
+
+void ingest_normalize(const float* x, int64_t n, int nfields, double* norm, FieldScal* fs,
+                      double eps_rel, cudaStream_t st) {
+  unsigned int* mm = nullptr;
+  cudaMallocAsync(&mm, sizeof(unsigned int) * 2 * nfields, st);
+  // lo starts at 0xffffffff, hi at 0
+  cudaMemsetAsync(mm, 0, sizeof(unsigned int) * 2 * nfields, st);
+  // set lo slots to all ones
+  for (int f = 0; f < nfields; f++) cudaMemsetAsync(mm + 2 * f, 0xff, sizeof(unsigned int), st);
+  minmax_kernel<<<dim3(grid_for(n, 512), nfields), 256, 0, st>>>(x, n, mm);
+  scalars_kernel<<<(nfields + 127) / 128, 128, 0, st>>>(mm, nfields, eps_rel, fs);
+  normalize_kernel<<<dim3(grid_for(n, 1024), nfields), 256, 0, st>>>(x, n, fs, norm);
+  cudaFreeAsync(mm, st);
+}
+
+void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, int nfields,
+                   cudaStream_t st) {
+  decode_coeffs_kernel<<<dim3(grid_for(n, 1024), nfields), 256, 0, st>>>(m, prm, a, n);
+}
+
+void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
+                int nfields, const double* norm, const float* orig, const FieldScal* fs,
+                ProbeResult* res, cudaStream_t st) {
+  decode_coeffs(m, prm, a, g.n, nfields, st);
+  inverse_all_but_last(a, b, g, nfields, st);
+  BaseProbeEpi e{norm, orig, fs, prm, res, g.n, 0, 0.0, FieldScal{}};
+  last_rows(b, a, g, nfields, st, e);
+}
+
+void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
+                 int nfields, const double* base_dec, const float* orig, const FieldScal* fs,
+                 ProbeResult* res, cudaStream_t st) {
+  decode_coeffs(m, prm, a, g.n, nfields, st);
+  inverse_all_but_last(a, b, g, nfields, st);
+  TruncProbeEpi e{base_dec, orig, fs, prm, res, g.n, 0.0, FieldScal{}};
+  last_rows(b, a, g, nfields, st, e);
+}
+
+void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
+                     int nfields, const double* norm, double* base_dec, double* resid,
+                     cudaStream_t st) {
+  decode_coeffs(m, prm, a, g.n, nfields, st);
+  inverse_all_but_last(a, b, g, nfields, st);
+  ResidueEpi e{norm, base_dec, resid, prm, g.n};
+  last_rows(b, a, g, nfields, st, e);
+}
+
+void decode_field(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
+                  int nfields, double* out, cudaStream_t st) {
+  decode_coeffs(m, prm, a, g.n, nfields, st);
+  inverse_all_but_last(a, b, g, nfields, st);
+  StoreFieldEpi e{out, prm, g.n};
+  last_rows(b, a, g, nfields, st, e);
+}
+
+void decode_field_add_denorm(const Meta& m, const ProbeParam* prm, double* a, double* b,
+                             const Geo& g, int nfields, const double* base, const FieldScal* fs,
+                             float* out32, cudaStream_t st) {
+  decode_coeffs(m, prm, a, g.n, nfields, st);
+  inverse_all_but_last(a, b, g, nfields, st);
+  AddDenormEpi e{base, fs, prm, out32, g.n, FieldScal{}};
+  last_rows(b, a, g, nfields, st, e);
+}
+
+void denorm_only(const double* base, const FieldScal* fs, const uint8_t* active, int64_t n,
+                 int nfields, float* out32, cudaStream_t st) {
+  denorm_kernel<<<dim3(grid_for(n, 1024), nfields), 256, 0, st>>>(base, fs, active, n, out32);
+}
+
+void fill_constant(const FieldScal* fs, const uint8_t* active, int64_t n, int nfields,
+                   float* out32, cudaStream_t st) {
+  fill_kernel<<<dim3(grid_for(n, 1024), nfields), 256, 0, st>>>(fs, active, n, out32);
+}
+
+void pack_parts(const PackPart* parts, int nparts, uint8_t* out, cudaStream_t st) {
+  if (nparts) pack_kernel<<<nparts, 256, 0, st>>>(parts, out);
+}
+
+void unpack_parts(const UnpackPart* parts, int nparts, const uint8_t* in, cudaStream_t st) {
+  if (nparts) unpack_kernel<<<nparts, 256, 0, st>>>(parts, in);
+}
+
+}  // namespace ebcc

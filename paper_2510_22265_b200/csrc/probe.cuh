@@ -1,0 +1,98 @@
+// Field-level kernels: ingest/normalise, closed-form prefix decode, the
+// feedback probes (decode -> IDWT -> fused reduction), residue formation,
+// decompress tails and payload (un)packing (probe.cu).
+#pragma once
+#include "common.cuh"
+#include "spiht.cuh"
+
+namespace ebcc {
+
+// per-field scalars shared by all probes
+struct FieldScal {
+  double vmin, vmax, range;  // range = vmax - vmin (float64, like the reference)
+  double eps_rel, eps_abs;
+  int32_t constant;
+  int32_t pad;
+};
+
+// what one probe decodes
+struct ProbeParam {
+  uint64_t B;          // stream bits available: positions < B were read
+  int32_t planes;      // refinement planes present (24/32 variant); -1: take
+                       // planes_run / n_last from the decoder machine
+  int32_t midpoint;    // add sign * 2^(n_last-1) (residual layer)
+  int32_t n_last;
+  int32_t active;
+};
+
+struct ProbeResult {
+  unsigned long long count;   // #points with |dec - norm| <= eps_rel (base probes)
+  unsigned long long maxerr;  // bits of max |f32(denorm(rec)) - orig| (non-negative double)
+};
+
+struct Meta {  // per-coefficient closed-form metadata (one field = `stride` entries)
+  const uint32_t* mant;
+  const uint32_t* sign_pos;
+  const uint32_t* lsp_rank;
+  const uint8_t* pinfo;
+  const PlaneRec* planes;
+  const MachineOut* mo;
+  int64_t stride;
+};
+
+// f32 input -> per-field vmin/vmax/constant flag and float64 normalised field
+void ingest_normalize(const float* x, int64_t n, int nfields, double* norm, FieldScal* fs,
+                      double eps_rel, cudaStream_t st);
+
+// closed-form prefix decode into coefficient buffer `a`
+void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, int nfields,
+                   cudaStream_t st);
+
+// base probe: decode (lower bound) -> IDWT -> count & max error
+void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
+                int nfields, const double* norm, const float* orig, const FieldScal* fs,
+                ProbeResult* res, cudaStream_t st);
+
+// residual probe: decode (midpoint) -> IDWT -> + base -> max error
+void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
+                 int nfields, const double* base_dec, const float* orig, const FieldScal* fs,
+                 ProbeResult* res, cudaStream_t st);
+
+// decode the chosen base prefix; write base_dec and resid = norm - base_dec
+void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
+                     int nfields, const double* norm, double* base_dec, double* resid,
+                     cudaStream_t st);
+
+// decompress: decode a stream to a float64 field (out), optionally midpoint
+void decode_field(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
+                  int nfields, double* out, cudaStream_t st);
+// decompress: residual decode fused with base add + denormalise to f32
+void decode_field_add_denorm(const Meta& m, const ProbeParam* prm, double* a, double* b,
+                             const Geo& g, int nfields, const double* base, const FieldScal* fs,
+                             float* out32, cudaStream_t st);
+// decompress: f32(vmin + base*range) for fields without residual (gate: active)
+void denorm_only(const double* base, const FieldScal* fs, const uint8_t* active, int64_t n,
+                 int nfields, float* out32, cudaStream_t st);
+// decompress: constant chunks (gate: active)
+void fill_constant(const FieldScal* fs, const uint8_t* active, int64_t n, int nfields,
+                   float* out32, cudaStream_t st);
+
+// payload pack: for each part, copy header (12 B from hdr) + stream bytes
+struct PackPart {
+  uint64_t dst_off;      // byte offset in the packed output
+  uint64_t nbytes;       // total bytes incl. 12-byte header
+  uint64_t bit_limit;    // stream bits >= this are zeroed (padding of a shorter variant)
+  const uint32_t* src;   // stream words
+  uint8_t hdr[16];
+};
+void pack_parts(const PackPart* parts, int nparts, uint8_t* out, cudaStream_t st);
+
+// payload unpack: scatter stream bytes (after the header) into word buffers
+struct UnpackPart {
+  uint64_t src_off;      // offset of the stream's first payload byte in `in`
+  uint64_t nbytes;       // payload bytes (excluding header)
+  uint32_t* dst;         // word buffer (zero-padded to a word)
+};
+void unpack_parts(const UnpackPart* parts, int nparts, const uint8_t* in, cudaStream_t st);
+
+}  // namespace ebcc

@@ -1,0 +1,698 @@
+// Data-parallel SPIHT coder for sm_100a (spiht.py:81-482 restated).
+//
+// The reference's coder is a list machine: per bit plane a LIP pass, LIS
+// "waves" and a refinement pass, each a batch of list operations.  Here:
+//
+// * exponents replace magnitude compares: |c| >= 2^n  <=>  floor(log2|c|) >= n,
+//   and the subtree maxima become integer max over exponents (e_d, e_l);
+// * the machine (one CTA per field, 512 threads x 4 entries per tile) walks
+//   the lists in order with block-wide scans, emitting significance/sign bits
+//   at their exact stream offsets and recording, per coefficient, its LSP rank,
+//   significance plane and sign-bit offset;
+// * refinement bits are NOT produced by the machine: bit p of coefficient c
+//   sits at refine_start[p] + lsp_rank[c], so a separate fully parallel kernel
+//   writes (encode) or gathers (decode) them afterwards.
+//
+// The same machine runs as encoder (significance from exponents) or decoder
+// (significance read from the stream at the offset the scan assigns), which is
+// how the reference keeps encoder and decoder in lockstep.
+#include <vector>
+
+#include "spiht.cuh"
+
+namespace ebcc {
+
+namespace {
+
+constexpr int MT = 512;          // machine threads
+constexpr int MI = 4;            // entries per thread per tile
+constexpr int TILE = MT * MI;    // 2048
+constexpr int NW = MT / 32;
+constexpr int STAGE_BITS = TILE * 4 + 64;  // children segment can be 4x the tile
+constexpr int STAGE_WORDS = STAGE_BITS / 32 + 2;
+constexpr uint32_t TYPE_B = 0x80000000u;
+
+// ---------------------------------------------------------------------------
+// tree tables
+__global__ void tree_flags_kernel(Geo g, uint8_t* flags) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.n) return;
+  int r = (int)(idx / g.cols), c = (int)(idx - (int64_t)r * g.cols);
+  uint32_t ch[4];
+  int nc = tree_children(g, r, c, ch);
+  int gc = 0;
+  for (int s = 0; s < nc; s++) {
+    uint32_t cc[4];
+    int rr = (int)(ch[s] / g.cols), c2 = (int)(ch[s] - (uint32_t)rr * g.cols);
+    gc |= tree_children(g, rr, c2, cc) > 0;
+  }
+  flags[idx] = (uint8_t)(nc | (gc << 3));
+}
+
+// host replica of the children count (for the initial LIS)
+int host_nchild(const Geo& g, int r, int c) {
+  const int L = g.levels;
+  if (r < g.lr[L] && c < g.lc[L]) {
+    int m = 0;
+    for (int o = 0; o < 3; o++) {
+      Rect R = detail_rect(g, L, o);
+      if (R.h > 0 && R.w > 0 && r < R.h && c < R.w) m++;
+    }
+    return m;
+  }
+  int k = 1;
+  for (int kk = L; kk >= 1; kk--)
+    if (r < g.lr[kk - 1] && c < g.lc[kk - 1]) { k = kk; break; }
+  if (k < 2) return 0;
+  int o = (r < g.lr[k]) ? 0 : ((c < g.lc[k]) ? 1 : 2);
+  Rect P = detail_rect(g, k, o), C = detail_rect(g, k - 1, o);
+  int i = r - P.r0, j = c - P.c0, m = 0;
+  for (int a = 0; a < 2; a++)
+    for (int b = 0; b < 2; b++) m += (2 * i + a < C.h && 2 * j + b < C.w);
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// coefficient preparation: exponents, mantissas, signs, n_max
+__global__ void coef_prepare_kernel(const double* __restrict__ coef, int64_t cstride, int64_t n,
+                                    int16_t* ec, int16_t* ed, int16_t* el, uint32_t* mant,
+                                    uint32_t* sign_pos, uint8_t* pinfo, int64_t stride,
+                                    MachineOut* out) {
+  const int f = blockIdx.y;
+  const double* cf = coef + f * cstride;
+  int best = kExpNone;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = cf[i];
+    int16_t e = exp_of(v);
+    int64_t o = f * stride + i;
+    ec[o] = e;
+    ed[o] = kExpNone;
+    el[o] = kExpNone;
+    mant[o] = v == 0.0 ? 0u : mant32_of(v);
+    sign_pos[o] = kNone;
+    pinfo[o] = v < 0.0 ? 0x80 : 0;
+    best = e > best ? e : best;
+  }
+  for (int o = 16; o; o >>= 1) {
+    int y = __shfl_xor_sync(0xffffffffu, best, o);
+    best = y > best ? y : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(&out[f].n_max, best);
+}
+
+// e_d / e_l for the parents of one level (spiht.py:182-195 over exponents)
+__global__ void subtree_kernel(Geo g, int level, int16_t* ec, int16_t* ed, int16_t* el,
+                               int64_t stride, int nfields) {
+  // level >= 2: detail nodes of `level`; level == 0: the LL band
+  int R, C;
+  if (level == 0) { R = g.lr[g.levels]; C = g.lc[g.levels]; }
+  else { R = g.lr[level - 1]; C = g.lc[level - 1]; }
+  int64_t cnt = (int64_t)R * C;
+  int f = blockIdx.y;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < cnt;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(idx / C), c = (int)(idx - (int64_t)r * C);
+    if (level != 0 && r < g.lr[level] && c < g.lc[level]) continue;  // inside the coarser box
+    uint32_t ch[4];
+    int nc = tree_children(g, r, c, ch);
+    int dm = kExpNone, lm = kExpNone;
+    int64_t fo = (int64_t)f * stride;
+    for (int s = 0; s < nc; s++) {
+      int a = ec[fo + ch[s]], b = ed[fo + ch[s]];
+      int m = a > b ? a : b;
+      dm = m > dm ? m : dm;
+      lm = b > lm ? b : lm;
+    }
+    int64_t o = fo + (int64_t)r * g.cols + c;
+    ed[o] = (int16_t)dm;
+    el[o] = (int16_t)lm;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// block scan of packed 4 x 16-bit counters (per-tile totals stay < 65536)
+struct ScanSmem {
+  uint64_t warp[NW + 1];
+};
+
+__device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t& total,
+                                                         ScanSmem& sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm.warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t w = lane < NW ? sm.warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NW) sm.warp[lane] = w;
+  }
+  __syncthreads();
+  uint64_t before = wid ? sm.warp[wid - 1] : 0;
+  total = sm.warp[NW - 1];
+  __syncthreads();
+  return before + x - v;
+}
+
+__device__ __forceinline__ uint32_t lane16(uint64_t v, int k) { return (uint32_t)(v >> (16 * k)) & 0xffffu; }
+
+// bit staging for one contiguous output segment [seg_start, seg_start + len)
+struct Stage {
+  uint32_t w[STAGE_WORDS];
+};
+
+__device__ __forceinline__ void stage_clear(Stage& s) {
+  for (int i = threadIdx.x; i < STAGE_WORDS; i += MT) s.w[i] = 0;
+}
+__device__ __forceinline__ void stage_set(Stage& s, uint64_t seg_start, uint64_t p) {
+  uint64_t w0 = seg_start >> 5;
+  atomicOr(&s.w[(p >> 5) - w0], bit_mask_in_word(p));
+}
+__device__ __forceinline__ void stage_flush(Stage& s, uint64_t seg_start, uint64_t len,
+                                            uint32_t* gw) {
+  if (!len) return;
+  uint64_t w0 = seg_start >> 5, w1 = (seg_start + len - 1) >> 5;
+  for (uint64_t i = threadIdx.x; i <= w1 - w0; i += MT) {
+    uint32_t v = s.w[i];
+    if (v) atomicOr(gw + w0 + i, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the machine
+template <bool DECODE>
+__global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, TreeTables tt,
+                                                        int planes) {
+  const int f = blockIdx.x;
+  if (mb.active && !mb.active[f]) return;
+  __shared__ ScanSmem ssm;
+  __shared__ Stage st_a, st_b, st_c;
+  __shared__ uint64_t red_sm[NW];
+
+  const int64_t fo = (int64_t)f * mb.stride;
+  const int16_t* ec = mb.ec + fo;
+  const int16_t* ed = mb.ed + fo;
+  const int16_t* el = mb.el + fo;
+  uint32_t* sign_pos = mb.sign_pos + fo;
+  uint32_t* lsp_rank = mb.lsp_rank + fo;
+  uint8_t* pinfo = mb.pinfo + fo;
+  uint32_t* lip = mb.lip + fo;
+  uint32_t* lis_old = mb.lis0 + fo;
+  uint32_t* lis_new = mb.lis1 + fo;
+  uint32_t* wav_a = mb.w0 + fo;
+  uint32_t* wav_b = mb.w1 + fo;
+  uint32_t* lsp = mb.lsp + fo;
+  uint32_t* bits = mb.bits + (int64_t)f * mb.bit_stride;
+  PlaneRec* prec = mb.planes + (int64_t)f * kMaxPlaneRecs;
+  const int n_max = mb.out[f].n_max;
+  const uint64_t limit = DECODE ? mb.limit[f] : ~0ull;
+  const uint64_t bit_cap = (uint64_t)mb.bit_stride * 32;
+  const uint64_t cap = (uint64_t)mb.stride;
+
+  // initial lists (spiht.py:300-303)
+  for (int64_t i = threadIdx.x; i < tt.nroots; i += MT) lip[i] = tt.roots[i];
+  for (int64_t i = threadIdx.x; i < tt.nlis_roots; i += MT) lis_old[i] = tt.lis_roots[i];
+  uint64_t nlip = tt.nroots, nlis = tt.nlis_roots, nlsp = 0, pos = 0;
+  int overflow = 0;
+  int p = 0;
+  __syncthreads();
+
+  for (; p < planes; p++) {
+    if (DECODE && pos >= limit) break;  // `while not src.depleted`
+    const int n = n_max - p;
+    const uint64_t refine_len = nlsp;
+    if (threadIdx.x == 0) prec[p].start = (uint32_t)pos;
+
+    // ---------------- LIP pass -------------------------------------------
+    {
+      uint64_t K = 0;  // newly significant so far
+      for (uint64_t base = 0; base < nlip; base += TILE) {
+        uint32_t node[MI];
+        int sig[MI];
+        int cnt_sig = 0;
+        const uint64_t i0 = base + (uint64_t)threadIdx.x * MI;
+#pragma unroll
+        for (int k = 0; k < MI; k++) {
+          uint64_t i = i0 + k;
+          sig[k] = 0;
+          node[k] = 0;
+          if (i < nlip) {
+            node[k] = lip[i];
+            sig[k] = DECODE ? read_bit(bits, pos + i, limit) : (ec[node[k]] >= n);
+            cnt_sig += sig[k];
+          }
+        }
+        uint64_t tot;
+        uint64_t ex = block_exclusive_scan((uint64_t)cnt_sig, tot, ssm);
+        const uint64_t tile_len = (nlip - base) < TILE ? (nlip - base) : TILE;
+        if (!DECODE) {
+          stage_clear(st_a);
+          stage_clear(st_b);
+          __syncthreads();
+          uint64_t sig_seg = pos + base, sgn_seg = pos + nlip + K;
+          uint32_t r = (uint32_t)ex;
+#pragma unroll
+          for (int k = 0; k < MI; k++) {
+            if (!sig[k]) continue;
+            stage_set(st_a, sig_seg, pos + i0 + k);
+            if (pinfo[node[k]] & 0x80) stage_set(st_b, sgn_seg, sgn_seg + r);
+            r++;
+          }
+          __syncthreads();
+          stage_flush(st_a, sig_seg, tile_len, bits);
+          stage_flush(st_b, sgn_seg, tot, bits);
+        }
+        // newly significant -> LSP, metadata; survivors compacted in place
+        uint32_t r = (uint32_t)ex;
+        uint64_t keep_before = (i0 - base) - ex;  // kept entries before mine in this tile
+        __syncthreads();  // all reads of lip[] in this tile done before compaction writes
+#pragma unroll
+        for (int k = 0; k < MI; k++) {
+          uint64_t i = i0 + k;
+          if (i >= nlip) break;
+          if (sig[k]) {
+            uint64_t rank = nlsp + K + r;
+            uint64_t sp = pos + nlip + K + r;
+            uint32_t c = node[k];
+            lsp[rank] = c;
+            lsp_rank[c] = (uint32_t)rank;
+            if (DECODE) {
+              if (sp < limit) {
+                sign_pos[c] = (uint32_t)sp;
+                pinfo[c] = (uint8_t)(p | (read_bit(bits, sp, limit) << 7));
+              } else {
+                pinfo[c] = (uint8_t)p;
+              }
+            } else {
+              sign_pos[c] = (uint32_t)sp;
+              pinfo[c] = (uint8_t)((pinfo[c] & 0x80) | p);
+            }
+            r++;
+          } else {
+            lip[base - K + keep_before] = node[k];
+            keep_before++;
+          }
+        }
+        K += tot;
+        __syncthreads();
+      }
+      pos += nlip + K;
+      nlsp += K;
+      nlip -= K;
+    }
+
+    // ---------------- LIS waves ------------------------------------------
+    {
+      uint64_t nkeep = 0;
+      const uint32_t* src = lis_old;
+      uint32_t* dst = wav_a;
+      uint64_t cnt = nlis;
+      while (cnt) {
+        // prepass: total children bits of significant type-A entries
+        uint64_t TC = 0;
+        for (uint64_t base = 0; base < cnt; base += TILE) {
+          uint64_t local = 0;
+          const uint64_t i0 = base + (uint64_t)threadIdx.x * MI;
+#pragma unroll
+          for (int k = 0; k < MI; k++) {
+            uint64_t i = i0 + k;
+            if (i >= cnt) break;
+            uint32_t e = src[i];
+            if (e & TYPE_B) continue;
+            uint32_t nd_ = e;
+            int s = DECODE ? read_bit(bits, pos + i, limit) : (ed[nd_] >= n);
+            if (s) local += tt.flags[nd_] & 7;
+          }
+          for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+          if ((threadIdx.x & 31) == 0) red_sm[threadIdx.x >> 5] = local;
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            uint64_t s = 0;
+            for (int w = 0; w < NW; w++) s += red_sm[w];
+            red_sm[0] = s;
+          }
+          __syncthreads();
+          TC += red_sm[0];
+          __syncthreads();
+        }
+        const uint64_t ch_seg0 = pos + cnt;       // children significance bits
+        const uint64_t sg_seg0 = pos + cnt + TC;  // their sign bits
+        uint64_t ch_off = 0, sig_off = 0, nxt_off = 0;
+        for (uint64_t base = 0; base < cnt; base += TILE) {
+          uint32_t ent[MI];
+          int sig[MI], nch[MI], nxt[MI];
+          uint32_t keep = 0, nchs = 0, nxts = 0;
+          const uint64_t i0 = base + (uint64_t)threadIdx.x * MI;
+#pragma unroll
+          for (int k = 0; k < MI; k++) {
+            uint64_t i = i0 + k;
+            sig[k] = 0; nch[k] = 0; nxt[k] = 0; ent[k] = 0;
+            if (i >= cnt) continue;
+            uint32_t e = src[i];
+            ent[k] = e;
+            uint32_t nd_ = e & ~TYPE_B;
+            bool isb = e & TYPE_B;
+            sig[k] = DECODE ? read_bit(bits, pos + i, limit) : ((isb ? el[nd_] : ed[nd_]) >= n);
+            if (!sig[k]) { keep++; continue; }
+            uint8_t fl = tt.flags[nd_];
+            if (!isb) {
+              nch[k] = fl & 7;
+              nxt[k] = (fl >> 3) & 1;
+            } else {
+              uint32_t ch[4];
+              int r = (int)(nd_ / g.cols), c = (int)(nd_ - (uint32_t)r * g.cols);
+              int m = tree_children(g, r, c, ch);
+              int q = 0;
+              for (int s = 0; s < m; s++) q += (tt.flags[ch[s]] & 7) != 0;
+              nxt[k] = q;
+            }
+            nchs += nch[k];
+            nxts += nxt[k];
+          }
+          uint64_t tot1;
+          uint64_t ex1 = block_exclusive_scan((uint64_t)keep | ((uint64_t)nchs << 16) |
+                                                  ((uint64_t)nxts << 32), tot1, ssm);
+          // children significance
+          uint32_t chn[MI][4];
+          uint8_t chs[MI];  // bitmask of significant children
+          uint32_t nsig = 0;
+          {
+            uint64_t cpos = ch_seg0 + ch_off + lane16(ex1, 1);
+#pragma unroll
+            for (int k = 0; k < MI; k++) {
+              chs[k] = 0;
+              if (!nch[k]) continue;
+              uint32_t nd_ = ent[k];
+              int r = (int)(nd_ / g.cols), c = (int)(nd_ - (uint32_t)r * g.cols);
+              tree_children(g, r, c, chn[k]);
+              for (int s = 0; s < nch[k]; s++) {
+                int cs = DECODE ? read_bit(bits, cpos, limit) : (ec[chn[k][s]] >= n);
+                chs[k] |= (uint8_t)(cs << s);
+                nsig += cs;
+                cpos++;
+              }
+            }
+          }
+          uint64_t tot2;
+          uint64_t ex2 = block_exclusive_scan((uint64_t)nsig, tot2, ssm);
+          const uint64_t tile_len = (cnt - base) < TILE ? (cnt - base) : TILE;
+          const uint64_t tile_ch = lane16(tot1, 1);
+          if (!DECODE) {
+            stage_clear(st_a);
+            stage_clear(st_b);
+            stage_clear(st_c);
+            __syncthreads();
+            uint64_t seg_a = pos + base, seg_b = ch_seg0 + ch_off, seg_c = sg_seg0 + sig_off;
+            uint64_t cpos = seg_b + lane16(ex1, 1);
+            uint64_t spos = seg_c + ex2;
+#pragma unroll
+            for (int k = 0; k < MI; k++) {
+              if (sig[k]) stage_set(st_a, seg_a, pos + i0 + k);
+              for (int s = 0; s < nch[k]; s++) {
+                if ((chs[k] >> s) & 1) {
+                  stage_set(st_b, seg_b, cpos);
+                  if (pinfo[chn[k][s]] & 0x80) stage_set(st_c, seg_c, spos);
+                  spos++;
+                }
+                cpos++;
+              }
+            }
+            __syncthreads();
+            stage_flush(st_a, seg_a, tile_len, bits);
+            stage_flush(st_b, seg_b, tile_ch, bits);
+            stage_flush(st_c, seg_c, tot2, bits);
+          }
+          // list updates
+          {
+            uint64_t kp = nkeep + lane16(ex1, 0);
+            uint64_t nx = nxt_off + lane16(ex1, 2);
+            uint64_t sg = sig_off + ex2;                       // rank among sig children
+            uint64_t ins = (ch_off + lane16(ex1, 1)) - sg;     // rank among insig children
+#pragma unroll
+            for (int k = 0; k < MI; k++) {
+              uint64_t i = i0 + k;
+              if (i >= cnt) break;
+              uint32_t e = ent[k];
+              uint32_t nd_ = e & ~TYPE_B;
+              if (!sig[k]) {
+                if (kp < cap) lis_new[kp] = e; else overflow = 1;
+                kp++;
+                continue;
+              }
+              for (int s = 0; s < nch[k]; s++) {
+                uint32_t c = chn[k][s];
+                if ((chs[k] >> s) & 1) {
+                  uint64_t rank = nlsp + sg;
+                  uint64_t sp = sg_seg0 + sg;
+                  lsp[rank] = c;
+                  lsp_rank[c] = (uint32_t)rank;
+                  if (DECODE) {
+                    if (sp < limit) {
+                      sign_pos[c] = (uint32_t)sp;
+                      pinfo[c] = (uint8_t)(p | (read_bit(bits, sp, limit) << 7));
+                    } else {
+                      pinfo[c] = (uint8_t)p;
+                    }
+                  } else {
+                    sign_pos[c] = (uint32_t)sp;
+                    pinfo[c] = (uint8_t)((pinfo[c] & 0x80) | p);
+                  }
+                  sg++;
+                } else {
+                  uint64_t li = nlip + ins;
+                  if (li < cap) lip[li] = c; else overflow = 1;
+                  ins++;
+                }
+              }
+              if (nxt[k]) {
+                if (!(e & TYPE_B)) {
+                  if (nx < cap) dst[nx] = nd_ | TYPE_B; else overflow = 1;
+                  nx++;
+                } else {
+                  uint32_t ch[4];
+                  int r = (int)(nd_ / g.cols), c = (int)(nd_ - (uint32_t)r * g.cols);
+                  int m = tree_children(g, r, c, ch);
+                  for (int s = 0; s < m; s++)
+                    if (tt.flags[ch[s]] & 7) {
+                      if (nx < cap) dst[nx] = ch[s]; else overflow = 1;
+                      nx++;
+                    }
+                }
+              }
+            }
+          }
+          nkeep += lane16(tot1, 0);
+          ch_off += lane16(tot1, 1);
+          nxt_off += lane16(tot1, 2);
+          sig_off += tot2;
+          __syncthreads();
+        }
+        pos += cnt + TC + sig_off;
+        nlsp += sig_off;
+        nlip += TC - sig_off;
+        cnt = nxt_off;
+        src = dst;
+        dst = (dst == wav_a) ? wav_b : wav_a;
+        __syncthreads();
+      }
+      nlis = nkeep;
+      uint32_t* t = lis_old; lis_old = lis_new; lis_new = t;
+    }
+
+    // ---------------- refinement (positions only) ------------------------
+    if (threadIdx.x == 0) {
+      prec[p].refine_start = (uint32_t)pos;
+      prec[p].refine_len = (uint32_t)refine_len;
+    }
+    pos += refine_len;
+    if (threadIdx.x == 0) prec[p].lists_end = (uint32_t)(nlip + nlis + nlsp);
+    if (!DECODE && pos > bit_cap) { overflow = 1; }
+    if (pos > 0xffffffffull) overflow = 1;
+    overflow = __syncthreads_or(overflow);
+    if (overflow) { p++; break; }
+  }
+  if (threadIdx.x == 0) {
+    mb.out[f].planes_run = p;
+    mb.out[f].total_bits = (uint32_t)(pos > 0xffffffffull ? 0xffffffffull : pos);
+    mb.out[f].overflow = overflow;
+    mb.out[f].lsp_count = (uint32_t)nlsp;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// encoder refinement: warp per 32 consecutive LSP ranks, ballot per plane.
+// Refinement bit of plane p for rank i sits at refine_start[p] + i, for every
+// plane p after the coefficient's significance plane (i < refine_len[p]).
+__global__ void refine_write_kernel(MachineBufs mb, int planes) {
+  const int f = blockIdx.y;
+  if (mb.active && !mb.active[f]) return;
+  const int64_t fo = (int64_t)f * mb.stride;
+  const PlaneRec* prec = mb.planes + (int64_t)f * kMaxPlaneRecs;
+  const int pr = mb.out[f].planes_run < planes ? mb.out[f].planes_run : planes;
+  if (pr < 2) return;
+  uint32_t* bits = mb.bits + (int64_t)f * mb.bit_stride;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t maxlen = prec[pr - 1].refine_len;  // non-decreasing in p
+  for (int64_t w = warp_global; w * 32 < (int64_t)maxlen; w += nwarps) {
+    uint32_t i = (uint32_t)(w * 32 + lane);
+    uint32_t m = 0;
+    int ps = 64;
+    if (i < maxlen) {
+      uint32_t c = mb.lsp[fo + i];
+      m = mb.mant[fo + c];
+      ps = mb.pinfo[fo + c] & 0x3f;
+    }
+    for (int p = 1; p < pr; p++) {
+      uint32_t len = prec[p].refine_len;
+      if ((uint32_t)(w * 32) >= len) continue;  // warp-uniform
+      int b = (i < len && p > ps) ? (int)((m >> (31 - (p - ps))) & 1u) : 0;
+      uint64_t q0 = (uint64_t)prec[p].refine_start + (uint64_t)w * 32;
+      uint64_t q = q0 + lane;
+      uint32_t word0 = (uint32_t)(q0 >> 5);
+      uint32_t mine = b ? bit_mask_in_word(q) : 0u;
+      bool second = ((q >> 5) != word0);
+      uint32_t v0 = __reduce_or_sync(0xffffffffu, second ? 0u : mine);
+      uint32_t v1 = __reduce_or_sync(0xffffffffu, second ? mine : 0u);
+      if (lane == 0 && v0) atomicOr(bits + word0, v0);
+      if (lane == 1 && v1) atomicOr(bits + word0 + 1, v1);
+    }
+  }
+}
+
+// decoder refinement gather: thread per LSP rank; bits past the stream
+// limit read as zero exactly like _BitSource.take
+__global__ void refine_gather_kernel(MachineBufs mb) {
+  const int f = blockIdx.y;
+  if (mb.active && !mb.active[f]) return;
+  const int64_t fo = (int64_t)f * mb.stride;
+  const PlaneRec* prec = mb.planes + (int64_t)f * kMaxPlaneRecs;
+  const int pr = mb.out[f].planes_run;
+  const uint32_t nlsp = mb.out[f].lsp_count;
+  const uint64_t limit = mb.limit[f];
+  const uint32_t* bits = mb.bits + (int64_t)f * mb.bit_stride;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)nlsp;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c = mb.lsp[fo + i];
+    if (mb.sign_pos[fo + c] == kNone) continue;  // sign never read: not placed
+    int ps = mb.pinfo[fo + c] & 0x3f;
+    uint32_t m = 0x80000000u;
+    for (int p = ps + 1; p < pr && p - ps <= 31; p++) {
+      if ((uint32_t)i >= prec[p].refine_len) break;
+      uint64_t q = (uint64_t)prec[p].refine_start + (uint64_t)i;
+      if (q >= limit) break;
+      m |= (uint32_t)read_bit(bits, q, limit) << (31 - (p - ps));
+    }
+    mb.mant[fo + c] = m;
+  }
+}
+
+// decoder init: nothing placed yet
+__global__ void decode_init_kernel(MachineBufs mb) {
+  const int f = blockIdx.y;
+  const int64_t fo = (int64_t)f * mb.stride;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < mb.stride;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    mb.sign_pos[fo + i] = kNone;
+    mb.pinfo[fo + i] = 0;
+    mb.mant[fo + i] = 0;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+void build_tree_tables(const Geo& g, TreeTables& t, cudaStream_t st) {
+  cudaMalloc(&t.flags, g.n);
+  tree_flags_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, st>>>(g, t.flags);
+  // roots: LL row-major, then orphans per level L-1..1 and orientation (spiht.py:164-178)
+  std::vector<uint32_t> roots, lis;
+  int llr = g.lr[g.levels], llc = g.lc[g.levels];
+  for (int i = 0; i < llr; i++)
+    for (int j = 0; j < llc; j++) roots.push_back((uint32_t)(i * g.cols + j));
+  for (int k = g.levels - 1; k >= 1; k--)
+    for (int o = 0; o < 3; o++) {
+      Rect C = detail_rect(g, k, o), P = detail_rect(g, k + 1, o);
+      if (C.h <= 0 || C.w <= 0) continue;
+      for (int i = 0; i < C.h; i++)
+        for (int j = 0; j < C.w; j++)
+          if (i / 2 >= P.h || j / 2 >= P.w) roots.push_back((uint32_t)((C.r0 + i) * g.cols + C.c0 + j));
+    }
+  for (uint32_t r : roots) {
+    int rr = (int)(r / g.cols), cc = (int)(r % g.cols);
+    if (host_nchild(g, rr, cc) > 0) lis.push_back(r);
+  }
+  t.nroots = (int64_t)roots.size();
+  t.nlis_roots = (int64_t)lis.size();
+  cudaMalloc(&t.roots, sizeof(uint32_t) * (roots.size() + 1));
+  cudaMalloc(&t.lis_roots, sizeof(uint32_t) * (lis.size() + 1));
+  cudaMemcpyAsync(t.roots, roots.data(), sizeof(uint32_t) * roots.size(), cudaMemcpyHostToDevice, st);
+  if (!lis.empty())
+    cudaMemcpyAsync(t.lis_roots, lis.data(), sizeof(uint32_t) * lis.size(), cudaMemcpyHostToDevice, st);
+  cudaStreamSynchronize(st);
+}
+
+void free_tree_tables(TreeTables& t) {
+  cudaFree(t.flags); cudaFree(t.roots); cudaFree(t.lis_roots);
+  t = TreeTables{};
+}
+
+void coef_prepare(const double* coef, int64_t field_stride, MachineBufs& mb, const Geo& g,
+                  cudaStream_t st) {
+  int blocks = (int)((g.n + 255) / 256);
+  if (blocks > 1024) blocks = 1024;
+  dim3 grid(blocks, mb.nfields);
+  coef_prepare_kernel<<<grid, 256, 0, st>>>(coef, field_stride, g.n, mb.ec, mb.ed, mb.el, mb.mant,
+                                            mb.sign_pos, mb.pinfo, mb.stride, mb.out);
+}
+
+void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables&, cudaStream_t st) {
+  for (int k = 2; k <= g.levels; k++) {
+    int64_t cnt = (int64_t)g.lr[k - 1] * g.lc[k - 1];
+    int blocks = (int)((cnt + 255) / 256);
+    if (blocks > 1024) blocks = 1024;
+    subtree_kernel<<<dim3(blocks, mb.nfields), 256, 0, st>>>(g, k, mb.ec, mb.ed, mb.el, mb.stride,
+                                                             mb.nfields);
+  }
+  int64_t cnt = (int64_t)g.lr[g.levels] * g.lc[g.levels];
+  int blocks = (int)((cnt + 255) / 256);
+  subtree_kernel<<<dim3(blocks, mb.nfields), 256, 0, st>>>(g, 0, mb.ec, mb.ed, mb.el, mb.stride,
+                                                           mb.nfields);
+}
+
+void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& tt, int planes,
+                 cudaStream_t st) {
+  if (decode) machine_kernel<true><<<mb.nfields, MT, 0, st>>>(mb, g, tt, planes);
+  else machine_kernel<false><<<mb.nfields, MT, 0, st>>>(mb, g, tt, planes);
+}
+
+void write_refinement(MachineBufs& mb, int planes, cudaStream_t st) {
+  int blocks = (int)((mb.stride / 32 + 7) / 8);
+  if (blocks > 512) blocks = 512;
+  if (blocks < 1) blocks = 1;
+  refine_write_kernel<<<dim3(blocks, mb.nfields), 256, 0, st>>>(mb, planes);
+}
+
+void decode_init(MachineBufs& mb, cudaStream_t st) {
+  int blocks = (int)((mb.stride + 255) / 256);
+  if (blocks > 1024) blocks = 1024;
+  decode_init_kernel<<<dim3(blocks, mb.nfields), 256, 0, st>>>(mb);
+}
+
+void gather_refinement(MachineBufs& mb, cudaStream_t st) {
+  int blocks = (int)((mb.stride + 255) / 256);
+  if (blocks > 1024) blocks = 1024;
+  refine_gather_kernel<<<dim3(blocks, mb.nfields), 256, 0, st>>>(mb);
+}
+
+}  // namespace ebcc

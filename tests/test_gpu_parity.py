@@ -1,0 +1,203 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden fixtures and against the CPU oracle.  Bit-exact throughout: float64
+coefficients compared as bytes, streams and containers byte for byte.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import golden_inputs as gi
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2510_22265_b200 import _lib
+    return _lib.context(0)
+
+
+@pytest.fixture(scope="module")
+def ebcc():
+    import paper_2510_22265_b200 as e
+    return e
+
+
+def _same(a, b):
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    return a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+def test_dwt_bitwise(ctx, golden_dwt):
+    bad = []
+    for i, (r, c, levels, dflt) in enumerate(golden_dwt["meta"]):
+        x = gi.dwt_input(i)
+        got = ctx.dwt(x, int(levels), inverse=False)[0]
+        if not _same(got, golden_dwt[f"c{i}"]):
+            bad.append(("fwd", int(r), int(c), float(np.abs(got - golden_dwt[f"c{i}"]).max())))
+        y = ctx.dwt(golden_dwt[f"c{i}"], int(levels), inverse=True)[0]
+        if not _same(y, golden_dwt[f"y{i}"]):
+            bad.append(("inv", int(r), int(c), float(np.abs(y - golden_dwt[f"y{i}"]).max())))
+    assert not bad, bad
+
+
+def test_dwt_batched_matches_single(ctx):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((5, 37, 53)) * 100
+    batch = ctx.dwt(x, 3, inverse=False)
+    for k in range(5):
+        assert _same(batch[k], ctx.dwt(x[k], 3, inverse=False)[0])
+
+
+def test_spiht_streams_bitwise(ctx, golden_spiht):
+    bad = []
+    for i, (r, c, seed, levels) in enumerate(golden_spiht["meta"]):
+        coef = golden_spiht[f"coef{i}"]
+        full = ctx.spiht_encode(coef, int(levels), 24)
+        if full != golden_spiht[f"full{i}"].tobytes():
+            bad.append(("full", i, len(full), golden_spiht[f"full{i}"].size))
+        deep = ctx.spiht_encode(coef, int(levels), 32)
+        if deep != golden_spiht[f"deep{i}"].tobytes():
+            bad.append(("deep", i, len(deep), golden_spiht[f"deep{i}"].size))
+        for b in golden_spiht[f"budgets{i}"]:
+            ref = golden_spiht[f"bud{i}_{int(b)}"].tobytes()
+            if full[: len(ref)] != ref:
+                bad.append(("budget", i, int(b)))
+    assert not bad, bad
+
+
+def test_spiht_prefix_decode_bitwise(ctx, golden_spiht):
+    bad = []
+    for i, (r, c, seed, levels) in enumerate(golden_spiht["meta"]):
+        deep = golden_spiht[f"deep{i}"].tobytes()
+        full = golden_spiht[f"full{i}"].tobytes()
+        for cut, nl in golden_spiht[f"nlast{i}"]:
+            cut, nl = int(cut), int(nl)
+            if cut < 0:
+                dec, n_last = ctx.spiht_decode(full, int(r), int(c))
+                ref = golden_spiht[f"decfull{i}"]
+            else:
+                dec, n_last = ctx.spiht_decode(deep, int(r), int(c), cut)
+                ref = golden_spiht[f"dec{i}_{cut}"]
+            if not _same(dec, ref) or (-999 if n_last is None else n_last) != nl:
+                bad.append((i, cut, n_last, nl, int((dec != ref).sum())))
+    assert not bad, bad
+
+
+def _run_case(ebcc, case, arr):
+    """Returns None on parity, else a description of the first difference."""
+    kw = dict(rel_error=case["eps"], q=case["q"], chunk_shape=case.get("chunk_shape"))
+    if "error" in case:
+        try:
+            ebcc.compress(arr, **kw)
+        except ebcc.EbccError as exc:
+            return None if type(exc).__name__ == case["error"] else f"raised {exc!r}"
+        return f"expected {case['error']}"
+    try:
+        buf = ebcc.compress(arr, **kw)
+    except ebcc.EbccError as exc:
+        return f"raised {exc!r}"
+    if hashlib.sha256(buf).hexdigest() != case["container_sha"]:
+        from paper_2510_22265_b200.container import read_file
+        chunks, _, _ = read_file(buf)
+        return ("container", [int(c.mode) for c in chunks], [c.base_len for c in chunks],
+                [c.residual_len for c in chunks], case["modes"], case["base_lens"],
+                case["resid_lens"])
+    out = ebcc.decompress(buf)
+    if gi.sha(out) != case["decoded_sha"]:
+        return "decoded"
+    return None
+
+
+def test_small_chunk_containers(ebcc, golden_chunks):
+    bad = []
+    for case in golden_chunks["chunks"]:
+        r = _run_case(ebcc, case, gi.chunk_input(case))
+        if r is not None:
+            bad.append((case["kind"], case["rows"], case["cols"], case["eps"], case["q"], r))
+    assert not bad, f"{len(bad)} mismatches: {bad[:8]}"
+
+
+def test_probe_counts_match_reference(golden_chunks):
+    """P_base / P_trunc per chunk equal the reference's probe traces."""
+    from paper_2510_22265_b200 import fields  # noqa: F401
+    from paper_2510_22265_b200.chunk import EbccParams
+    from paper_2510_22265_b200.pipeline import compress_batch
+    bad = []
+    for case in golden_chunks["chunks"]:
+        if "error" in case or case["kind"] == "const":
+            continue
+        a = gi.chunk_input(case)
+        recs, _, _, st = compress_batch(a[None], EbccParams(case["eps"], case["q"]))
+        if st != 0:
+            continue
+        nb, nt = int(recs[0]["n_base_probes"]), int(recs[0]["n_trunc_probes"])
+        if nb != len(case["base_trace"]) or nt != len(case["trunc_trace"]):
+            bad.append((case["rows"], case["cols"], nb, len(case["base_trace"]), nt,
+                        len(case["trunc_trace"])))
+    assert not bad, bad
+
+
+def test_grids(ebcc, golden_chunks):
+    bad = []
+    for case in golden_chunks["grids"]:
+        arr = gi.grid_input(case["name"])
+        assert gi.sha(arr) == case["input_sha"]
+        r = _run_case(ebcc, case, arr)
+        if r is not None:
+            bad.append((case["name"], r))
+    assert not bad, bad
+
+
+def test_batched_equals_single(ebcc):
+    """One batch of many chunks gives the same bytes as one call per chunk."""
+    from paper_2510_22265_b200 import fields
+    stack = np.stack([fields.small_field(k, 40, 56, s) for s, k in
+                      enumerate(["smooth", "spiky", "precip", "noise"] * 3)])
+    whole = ebcc.compress(stack, 0.01)
+    parts = [ebcc.compress(stack[i], 0.01) for i in range(len(stack))]
+    from paper_2510_22265_b200.container import read_file
+    chunks, _, _ = read_file(whole)
+    for i, blob in enumerate(parts):
+        c1, _, _ = read_file(blob)
+        assert c1[0].payload == chunks[i].payload
+
+
+def test_large_golden(ebcc, golden_large):
+    bad = []
+    for case in golden_large:
+        arr = gi.large_input(case["name"])
+        assert gi.sha(arr) == case["input_sha"]
+        r = _run_case(ebcc, case, arr)
+        if r is not None:
+            bad.append((case["name"], r))
+    assert not bad, bad
+
+
+def test_random_fields_vs_oracle(ebcc, oracle):
+    """Fresh random shapes/kinds/targets (not in the goldens): GPU container
+    bytes equal the oracle's."""
+    from paper_2510_22265_b200 import fields
+    rng = np.random.default_rng(77)
+    bad = []
+    for i in range(40):
+        r = int(rng.integers(3, 140))
+        c = int(rng.integers(3, 140))
+        kind = ["smooth", "spiky", "precip", "noise"][i % 4]
+        eps = float(10 ** rng.uniform(-4, -0.5))
+        q = float([1 - 1e-5, 1.0, 0.999, 0.9][i % 4])
+        a = fields.small_field(kind, r, c, 9000 + i)
+        try:
+            want = oracle.compress(a, eps, q)
+        except Exception as exc:
+            want = type(exc).__name__
+        try:
+            got = ebcc.compress(a, eps, q)
+        except ebcc.EbccError as exc:
+            got = type(exc).__name__
+        if got != want:
+            bad.append((kind, r, c, eps, q))
+    assert not bad, bad
