@@ -1,0 +1,376 @@
+#!/usr/bin/env python3
+"""Benchmark: float32 GB/s compressed+decompressed at a 1% max-error bound.
+
+Workload (BASELINE.json configs[1], the metric's config that fits one GPU):
+37 vertical levels x 721x1440 float32 k^-3 GRF fields (seeded synthetic
+stand-ins for ERA5; per-level mean 200-300, std 2-20), eps_rel = 1%,
+q = 1-1e-5.  One step = compress the 37 fields + decompress them again
+(round trip).  value = 4*N*fields / (T_compress + T_decompress), whole job.
+
+Multi-GPU (torchrun, one process per GPU): weak scaling — every rank
+compresses its own 37-level stack (seeds offset by rank); the only
+collective is the final size all-gather used for container offsets.
+
+Arms:
+  default           this repo's CUDA path (libebcc_gpu.so through the C ABI)
+  --impl reference  the reference algorithm on host cores: the CPU oracle
+                    (oracle/, a C restatement of the reference pinned to its
+                    golden vectors; the Python reference cannot travel to the
+                    GPU box), one chunk per core via a process pool.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+ROWS, COLS = 721, 1440
+LEVELS = 37
+EPS = 0.01
+Q = 1.0 - 1e-5
+
+
+def workload(rank: int = 0, levels: int = LEVELS) -> np.ndarray:
+    from paper_2510_22265_b200 import fields
+    out = np.empty((levels, ROWS, COLS), dtype=np.float32)
+    for lev in range(levels):
+        frac = lev / max(1, LEVELS - 1)
+        out[lev] = fields.temperature_like(ROWS, COLS, seed=1000 + lev + 100 * rank,
+                                           mean=200.0 + 100.0 * frac, std=2.0 + 18.0 * frac)
+    return out
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if r[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2510_22265_b200 as ebcc
+    from paper_2510_22265_b200 import _lib
+    from paper_2510_22265_b200.chunk import EbccParams
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    # a dedicated (non-default) stream: the library runs on it and the CUDA
+    # events bracketing each step are recorded on it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ctx = _lib.context(local_rank)
+    ctx.set_stream(stream.cuda_stream)
+    # the public API path (e2e) uses the same per-thread context
+    os.environ["EBCC_DEVICE"] = str(local_rank)
+
+    host = workload(rank)
+    nf, n = host.shape[0], ROWS * COLS
+    pinned = torch.empty(host.shape, dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[...] = host
+    x = pinned.to(dev)
+    payload = torch.empty(nf * n * 8, dtype=torch.uint8, device=dev)
+    out = torch.empty((nf, ROWS, COLS), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    params = EbccParams(epsilon_rel=EPS, q=Q)
+    F_IN, F_OUT = _lib.INPUT_ON_DEVICE, _lib.OUTPUT_ON_DEVICE
+
+    def device_step():
+        recs, offs, total, st = ctx.compress(x.data_ptr(), nf, ROWS, COLS, params.epsilon_rel,
+                                             params.q, params.r0, params.search_tol,
+                                             flags=F_IN | F_OUT, payload=payload.data_ptr(),
+                                             payload_cap=payload.numel())
+        ctx.raise_for(st, "ebcc_compress")
+        cst = ctx.stats()
+        ctx.decompress(payload.data_ptr(), offs, recs, ROWS, COLS, 5, out.data_ptr(),
+                       flags=F_IN | F_OUT)
+        dst = ctx.stats()
+        return recs, total, cst, dst
+
+    for _ in range(args.warmup):
+        device_step()
+    torch.cuda.synchronize()
+
+    # parity of the timed output (bound honoured at every point)
+    recs, total, _, _ = device_step()
+    back = out.cpu().numpy()
+    err = np.abs(back.astype(np.float64) - host.astype(np.float64)).max(axis=(1, 2))
+    rng_ = host.reshape(nf, -1).max(axis=1).astype(np.float64) - host.reshape(nf, -1).min(axis=1)
+    bound_ok = bool(np.all(err <= EPS * rng_))
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    t_c = t_d = 0.0
+    launches = 0
+    probe_ms = probe_steps = 0.0
+    enc_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        recs, offs, total, st = ctx.compress(x.data_ptr(), nf, ROWS, COLS, params.epsilon_rel,
+                                             params.q, params.r0, params.search_tol,
+                                             flags=F_IN | F_OUT, payload=payload.data_ptr(),
+                                             payload_cap=payload.numel())
+        ctx.raise_for(st, "ebcc_compress")
+        cst = ctx.stats()
+        e1.record(stream)
+        ctx.decompress(payload.data_ptr(), offs, recs, ROWS, COLS, 5, out.data_ptr(),
+                       flags=F_IN | F_OUT)
+        dst = ctx.stats()
+        e2.record(stream)
+        torch.cuda.synchronize()
+        t_c += e0.elapsed_time(e1) / 1e3
+        t_d += e1.elapsed_time(e2) / 1e3
+        launches += cst["kernel_launches"] + dst["kernel_launches"]
+        probe_ms += cst["ms_probe"]
+        probe_steps += cst["probe_launches"]
+        enc_ms += cst["ms_encode"]
+    clocks = sampler.stop()
+
+    # size/offset all-gather: the one collective of the sharded path
+    sizes = torch.tensor([int(total)], dtype=torch.int64, device=dev)
+    if world > 1:
+        gathered = [torch.zeros_like(sizes) for _ in range(world)]
+        torch.distributed.all_gather(gathered, sizes)
+        tt = torch.tensor([t_c, t_d], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_c, t_d = float(tt[0]), float(tt[1])
+        total_payload = int(sum(int(g.item()) for g in gathered))
+    else:
+        total_payload = int(total)
+
+    # ---- e2e: the public API with host buffers, H2D + D2H inside ----
+    e2e_t = 0.0
+    e2e_steps = max(1, min(args.steps, 3))
+    blob = None
+    for _ in range(e2e_steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        blob = ebcc.compress(pinned.numpy(), rel_error=EPS, q=Q)
+        rec_host = ebcc.decompress(blob)
+        torch.cuda.synchronize()
+        e2e_t += time.perf_counter() - t0
+    assert rec_host.shape == (1, nf, ROWS, COLS)
+
+    steps = args.steps
+    bytes_in = 4.0 * n * nf
+    value = bytes_in * world * steps / (t_c + t_d) / 1e9
+    c_gbs = bytes_in * world * steps / t_c / 1e9
+    d_gbs = bytes_in * world * steps / t_d / 1e9
+    e2e_val = bytes_in * world * e2e_steps / e2e_t / 1e9 if world == 1 else \
+        bytes_in * e2e_steps / e2e_t / 1e9 * world
+    ratio = bytes_in * world / (total_payload + 42 + 25 * nf * world)
+    p_base = int(recs["n_base_probes"].sum())
+    p_trunc = int(recs["n_trunc_probes"].sum())
+
+    # roofline of the dominant stage: one batched feedback probe (closed-form
+    # decode -> 5-level IDWT -> fused reduction over all 37 fields).
+    # Algorithmic bytes per probe step = 4 B * N * fields (SURVEY.md §8(d):
+    # each evaluation must re-read the N original float32 values).
+    peaks = {}
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    probe_avg_s = (probe_ms / 1e3) / max(1.0, probe_steps)
+    achieved = (4.0 * n * nf) / probe_avg_s / 1e9 if probe_steps else 0.0
+    comp_alg = (4.0 * n * nf + total_payload / world + 4.0 * n * (p_base + p_trunc))
+    comp_alg_gbs = comp_alg * steps / t_c / 1e9
+
+    line = {
+        "metric": "float32 GB/s compressed+decompressed at 1% max-error bound; compression ratio",
+        "value": round(value, 4),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": args.warmup,
+        "ms_per_step": round((t_c + t_d) / steps * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded k^-3 GRFs standing in for ERA5)",
+        "config": {"workload": "configs[1]: 37 levels x 721x1440 float32, eps_rel=1%",
+                   "levels": nf, "rows": ROWS, "cols": COLS, "eps_rel": EPS, "q": Q,
+                   "parallelism": f"fields sharded, dp{world}",
+                   "l2": "256 MiB buffer written between timed steps (flush)",
+                   "inputs_resident": "device (value); host pinned (e2e)"},
+        "compression_ratio": round(ratio, 4),
+        "compress_gbs": round(c_gbs, 4),
+        "decompress_gbs": round(d_gbs, 4),
+        "bound_honoured": bound_ok,
+        "probes": {"P_base": p_base, "P_trunc": p_trunc, "probe_steps_per_compress":
+                   probe_steps / steps, "ms_probe_per_compress": probe_ms / steps,
+                   "ms_encode_per_compress": enc_ms / steps},
+        "e2e": {"value": round(e2e_val, 4), "unit": "GB/s",
+                "h2d_bytes_per_step": int(bytes_in + len(blob)),
+                "d2h_bytes_per_step": int(len(blob) + bytes_in)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": None,
+                     "kernel": "feedback probe step (decode+IDWT+fused reduction, 37 fields)",
+                     "compress_algorithmic_gbs": round(comp_alg_gbs, 2),
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(host, sample_fields=args.cpu_fields)
+    return line
+
+
+# ---------------------------------------------------------------------------
+def _oracle_roundtrip(arr):
+    from oracle import oracle
+    t0 = time.perf_counter()
+    blob = oracle.compress(arr, EPS, Q)
+    oracle.decompress(blob)
+    return time.perf_counter() - t0, len(blob)
+
+
+def cpu_baseline(host: np.ndarray, sample_fields: int = 0) -> dict:
+    """The reference algorithm (CPU oracle port) on this box's host cores:
+    one 721x1440 level per process, all cores at once, one round trip each."""
+    import multiprocessing as mp
+    from oracle import oracle
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    k = sample_fields or min(cores, host.shape[0])
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(min(cores, k)) as pool:
+        res = pool.map(_oracle_roundtrip, [host[i] for i in range(k)])
+    wall = time.perf_counter() - t0
+    return {"value": round(4.0 * ROWS * COLS * k / wall / 1e9, 6), "unit": "GB/s",
+            "cores": min(cores, k), "kind": "port",
+            "sample": f"{k} of the 37 levels, one compress+decompress round trip each, "
+                      f"{min(cores, k)} processes in parallel ({wall:.1f} s wall)"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port on all host cores, same metric."""
+    if rank != 0:
+        return None
+    import multiprocessing as mp
+    from oracle import oracle
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    host = workload(0, levels=min(LEVELS, cores))
+    k = host.shape[0]
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(k) as pool:
+        for step in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_oracle_roundtrip, [host[i] for i in range(k)])
+            if step >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = 4.0 * ROWS * COLS * k * len(times) / tot / 1e9
+    return {
+        "impl": "reference",
+        "metric": "float32 GB/s compressed+decompressed at 1% max-error bound; compression ratio",
+        "value": round(value, 6), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(tot / len(times) * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded k^-3 GRFs standing in for ERA5)",
+        "config": {"workload": "configs[1]: 37 levels x 721x1440 float32, eps_rel=1%",
+                   "levels_per_step": k, "rows": ROWS, "cols": COLS, "eps_rel": EPS, "q": Q},
+        "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": k, "kind": "port",
+                         "sample": f"{k} levels per step (one per core), compress+decompress"},
+        "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-fields", type=int, default=0)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl")
+    line = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -19,6 +19,8 @@
 // the order is observably identical, and running both base-memo searches
 // first lets the residual encode reuse the base coefficient metadata arrays.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -214,6 +216,7 @@ struct Workspace {
   int16_t *ec = nullptr, *ed = nullptr, *el = nullptr;
   uint32_t *mant = nullptr, *sign_pos = nullptr, *lsp_rank = nullptr;
   uint8_t* pinfo = nullptr;
+  uint4* packed = nullptr;
   uint32_t *lip = nullptr, *lis0 = nullptr, *lis1 = nullptr, *w0 = nullptr, *w1 = nullptr,
            *lsp = nullptr;
   uint32_t *bits_base = nullptr, *bits_res = nullptr;
@@ -225,15 +228,21 @@ struct Workspace {
   ProbeResult* res = nullptr;
   uint64_t* limit = nullptr;
   uint8_t* active = nullptr;
+  unsigned int* mm = nullptr;
+  // pinned host mirrors of the per-step control arrays
+  ProbeParam* h_prm = nullptr;
+  ProbeResult* h_res = nullptr;
   TreeTables tt{};
   bool has_tt = false;
 
   void release() {
-    void* ptrs[] = {x32, norm, A, B, base_dec, ec, ed, el, mant, sign_pos, lsp_rank, pinfo,
+    void* ptrs[] = {x32, norm, A, B, base_dec, ec, ed, el, mant, sign_pos, lsp_rank, pinfo, packed,
                     lip, lis0, lis1, w0, w1, lsp, bits_base, bits_res, pl_base, pl_res,
-                    mo_base, mo_res, fs, prm, res, limit, active};
+                    mo_base, mo_res, fs, prm, res, limit, active, mm};
     for (void* p : ptrs)
       if (p) cudaFree(p);
+    if (h_prm) cudaFreeHost(h_prm);
+    if (h_res) cudaFreeHost(h_res);
     if (has_tt) free_tree_tables(tt);
     *this = Workspace{};
   }
@@ -259,6 +268,8 @@ struct ebcc_ctx {
   int64_t payload_cap = 0, payload_total = 0;
   PackPart* d_parts = nullptr;
   int parts_cap = 0;
+  UnpackPart* d_unpack = nullptr;
+  int unpack_cap = 0;
   uint8_t* d_stage = nullptr;
   int64_t stage_cap = 0;
   float* d_out = nullptr;
@@ -290,6 +301,7 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   w.sign_pos = dalloc<uint32_t>(N);
   w.lsp_rank = dalloc<uint32_t>(N);
   w.pinfo = dalloc<uint8_t>(N);
+  w.packed = dalloc<uint4>(N);
   w.lip = dalloc<uint32_t>(N);
   w.lis0 = dalloc<uint32_t>(N);
   w.lis1 = dalloc<uint32_t>(N);
@@ -309,6 +321,9 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   w.res = dalloc<ProbeResult>(cap);
   w.limit = dalloc<uint64_t>(cap);
   w.active = dalloc<uint8_t>(cap);
+  w.mm = dalloc<unsigned int>(2 * cap);
+  CK(cudaMallocHost(&w.h_prm, sizeof(ProbeParam) * cap));
+  CK(cudaMallocHost(&w.h_res, sizeof(ProbeResult) * cap));
   build_tree_tables(g, w.tt, c->stream);
   w.has_tt = true;
 }
@@ -331,7 +346,7 @@ MachineBufs machine_bufs(Workspace& w, int nfields, bool residual) {
 
 Meta meta_of(Workspace& w, bool residual) {
   Meta m{};
-  m.mant = w.mant; m.sign_pos = w.sign_pos; m.lsp_rank = w.lsp_rank; m.pinfo = w.pinfo;
+  m.packed = w.packed;
   m.planes = residual ? w.pl_res : w.pl_base;
   m.mo = residual ? w.mo_res : w.mo_base;
   m.stride = w.g.n;
@@ -340,6 +355,10 @@ Meta meta_of(Workspace& w, bool residual) {
 
 // encode the pyramid currently in w.A (all fields): exponents, machine,
 // refinement.  Returns per-field machine summaries and plane records.
+struct PhaseClock;
+void pc_mark(PhaseClock* pc, const char* name);
+PhaseClock* g_pc = nullptr;
+
 void encode_pyramids(ebcc_ctx* c, int nfields, bool residual, int planes,
                      const std::vector<uint8_t>& active, std::vector<MachineOut>& mo,
                      std::vector<PlaneRec>& pl) {
@@ -353,6 +372,7 @@ void encode_pyramids(ebcc_ctx* c, int nfields, bool residual, int planes,
   coef_prepare(w.A, w.g.n, mb, w.g, st);
   subtree_exponents(mb, w.g, w.tt, st);
   c->stats.kernel_launches += 2 + w.g.levels;
+  pc_mark(g_pc, "exponents");
   // fields whose pyramid is all zero (n_max sentinel) skip the machine
   CK(cudaMemcpyAsync(mo.data(), mb.out, sizeof(MachineOut) * nfields, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -360,8 +380,11 @@ void encode_pyramids(ebcc_ctx* c, int nfields, bool residual, int planes,
   for (int f = 0; f < nfields; f++) act[f] = active[f] && mo[f].n_max != kExpNone;
   CK(cudaMemcpyAsync(w.active, act.data(), nfields, cudaMemcpyHostToDevice, st));
   run_machine(false, mb, w.g, w.tt, planes, st);
+  pc_mark(g_pc, "machine");
   write_refinement(mb, planes, st);
-  c->stats.kernel_launches += 2;
+  pack_meta(mb, w.packed, st);
+  pc_mark(g_pc, "refine");
+  c->stats.kernel_launches += 3;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(mo.data(), mb.out, sizeof(MachineOut) * nfields, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(pl.data(), mb.planes, sizeof(PlaneRec) * kMaxPlaneRecs * nfields,
@@ -400,6 +423,36 @@ void put_header(uint8_t* h, int n_max, int levels, int rows, int cols) {
   memcpy(h + 8, &cc, 4);
 }
 
+// EBCC_PROFILE=1: host wall-clock per phase (stream synced at each mark)
+struct PhaseClock {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0, last;
+  std::string log;
+  explicit PhaseClock(cudaStream_t s) : st(s) {
+    const char* e = getenv("EBCC_PROFILE");
+    on = e && *e == '1';
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    auto now = std::chrono::steady_clock::now();
+    char buf[128];
+    snprintf(buf, sizeof buf, " %s=%.2fms", name,
+             std::chrono::duration<double, std::milli>(now - last).count());
+    log += buf;
+    last = now;
+  }
+  ~PhaseClock() {
+    if (on && !log.empty()) fprintf(stderr, "[ebcc profile]%s\n", log.c_str());
+  }
+};
+
+void pc_mark(PhaseClock* pc, const char* name) {
+  if (pc) pc->mark(name);
+}
+
 struct EventTimer {
   ebcc_ctx* c;
   cudaEvent_t a, b;
@@ -429,9 +482,13 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   cudaStream_t st = c->stream;
   const int64_t N = g.n;
 
+  PhaseClock pc(st);
+  g_pc = pc.on ? &pc : nullptr;
+  double replay_ms = 0;
   // ---- ingest + normalise (core.normalize) ----
-  ingest_normalize(w.x32, N, nfields, w.norm, w.fs, eps_rel, st);
-  c->stats.kernel_launches += 3;
+  ingest_normalize(w.x32, N, nfields, w.norm, w.fs, w.mm, eps_rel, st);
+  pc.mark("ingest");
+  c->stats.kernel_launches += 4;
   std::vector<FieldScal> fs(nfields);
   CK(cudaMemcpyAsync(fs.data(), w.fs, sizeof(FieldScal) * nfields, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -454,8 +511,10 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     CK(cudaMemcpyAsync(w.A, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
     forward_dwt(w.A, w.B, N, nfields, g, st);
     c->stats.kernel_launches += 2 * g.levels;
+    pc.mark("fwd_dwt");
     encode_pyramids(c, nfields, false, kBasePlanes, active, mo, pl);
   }
+  pc.mark("base_tail");
   for (int f = 0; f < nfields; f++) cs[f].T_base = active[f] ? mo[f].total_bits : 0;
   std::vector<int> base_nmax(nfields);
   for (int f = 0; f < nfields; f++) base_nmax[f] = mo[f].n_max;
@@ -469,6 +528,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   for (int phase = 0; phase < 2; phase++) {
     for (;;) {
       bool any = false;
+      auto h0 = std::chrono::steady_clock::now();
       for (int f = 0; f < nfields; f++) {
         ChunkSearch& s = cs[f];
         prm[f] = ProbeParam{};
@@ -486,16 +546,19 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
           any = true;
         }
       }
+      replay_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
       if (!any) break;
       EventTimer t(c, &c->stats.ms_probe);
-      CK(cudaMemcpyAsync(w.prm, prm.data(), sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
+      memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
+      CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
       CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
       probe_base(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.x32, w.fs, w.res, st);
-      c->stats.kernel_launches += 1 + 2 * g.levels;
+      c->stats.kernel_launches += g.levels;
       c->stats.probe_launches++;
       CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(res.data(), w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      memcpy(res.data(), w.h_res, sizeof(ProbeResult) * nfields);
       for (int f = 0; f < nfields; f++) {
         if (!prm[f].active) continue;
         ChunkSearch& s = cs[f];
@@ -517,6 +580,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     }
     if (phase == 0)
       for (int f = 0; f < nfields; f++) base_entries[f] = cs[f].memo.size();
+    pc.mark(phase == 0 ? "base_search" : "pure_search");
   }
 
   // ---- residue = norm - base decode at the chosen budget; residual encode ----
@@ -535,12 +599,13 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     CK(cudaMemcpyAsync(w.prm, prm.data(), sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
     // resid overwrites norm in place (norm is not needed after the base searches)
     base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
-    c->stats.kernel_launches += 1 + 2 * g.levels;
+    c->stats.kernel_launches += g.levels;
     CK(cudaMemcpyAsync(w.A, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
     forward_dwt(w.A, w.B, N, nfields, g, st);
     c->stats.kernel_launches += 2 * g.levels;
     encode_pyramids(c, nfields, true, kDeepPlanes, active, rmo, rpl);
   }
+  pc.mark("residual_encode");
   Meta mres = meta_of(w, true);
   // stream totals of the 24- and 32-plane variants
   std::vector<uint64_t> T24(nfields, 0), T32(nfields, 0);
@@ -594,14 +659,16 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     }
     if (!any) break;
     EventTimer t(c, &c->stats.ms_probe);
-    CK(cudaMemcpyAsync(w.prm, prm.data(), sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
+    memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
+    CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
     probe_trunc(mres, w.prm, w.A, w.B, g, nfields, w.base_dec, w.x32, w.fs, w.res, st);
-    c->stats.kernel_launches += 1 + 2 * g.levels;
+    c->stats.kernel_launches += g.levels;
     c->stats.probe_launches++;
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(res.data(), w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    memcpy(res.data(), w.h_res, sizeof(ProbeResult) * nfields);
     for (int f = 0; f < nfields; f++) {
       if (!prm[f].active) continue;
       ChunkSearch& s = cs[f];
@@ -616,6 +683,13 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     }
   }
 
+  pc.mark("trunc_search");
+  g_pc = nullptr;
+  if (pc.on) {
+    char b[64];
+    snprintf(b, sizeof b, " (host replay %.2fms)", replay_ms);
+    pc.log += b;
+  }
   // ---- candidate choice (pipeline.py:315-329) + payload parts ----
   int status = EBCC_OK;
   for (int f = 0; f < nfields; f++) {
@@ -712,6 +786,7 @@ void ebcc_destroy(ebcc_ctx* c) {
   c->ws.release();
   if (c->d_payload) cudaFree(c->d_payload);
   if (c->d_parts) cudaFree(c->d_parts);
+  if (c->d_unpack) cudaFree(c->d_unpack);
   if (c->d_stage) cudaFree(c->d_stage);
   if (c->d_out) cudaFree(c->d_out);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -959,13 +1034,15 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
                            (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
                                                           : cudaMemcpyHostToDevice,
                            st));
-        UnpackPart* dup = nullptr;
-        dup = dalloc<UnpackPart>(up.size());
-        CK(cudaMemcpyAsync(dup, up.data(), sizeof(UnpackPart) * up.size(), cudaMemcpyHostToDevice, st));
-        unpack_parts(dup, (int)up.size(), c->d_stage, st);
+        if ((int)up.size() > c->unpack_cap) {
+          if (c->d_unpack) cudaFree(c->d_unpack);
+          c->unpack_cap = (int)up.size() * 2;
+          c->d_unpack = dalloc<UnpackPart>(c->unpack_cap);
+        }
+        CK(cudaMemcpyAsync(c->d_unpack, up.data(), sizeof(UnpackPart) * up.size(),
+                           cudaMemcpyHostToDevice, st));
+        unpack_parts(c->d_unpack, (int)up.size(), c->d_stage, st);
         c->stats.kernel_launches++;
-        CK(cudaStreamSynchronize(st));
-        cudaFree(dup);
       }
       std::vector<ProbeParam> prm(nb);
       float* dst = out + f0 * g.n;
@@ -997,7 +1074,8 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         decode_init(mb, st);
         run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
         gather_refinement(mb, st);
-        c->stats.kernel_launches += 3;
+        pack_meta(mb, w.packed, st);
+        c->stats.kernel_launches += 4;
         for (int i = 0; i < nb; i++) {
           prm[i] = ProbeParam{};
           prm[i].B = ~0ull;
@@ -1012,7 +1090,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         } else {
           decode_field_add_denorm(m, w.prm, w.A, w.B, g, nb, w.base_dec, w.fs, out_dev, st);
         }
-        c->stats.kernel_launches += 1 + 2 * g.levels;
+        c->stats.kernel_launches += g.levels;
         CK(cudaGetLastError());
       }
       CK(cudaMemcpyAsync(w.active, pure.data(), nb, cudaMemcpyHostToDevice, st));
@@ -1137,6 +1215,7 @@ int ebcc_spiht_decode(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t pre
     decode_init(mb, st);
     run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
     gather_refinement(mb, st);
+    pack_meta(mb, w.packed, st);
     ProbeParam p{};
     p.B = ~0ull; p.planes = -1; p.active = 1;
     CK(cudaMemcpyAsync(w.prm, &p, sizeof(p), cudaMemcpyHostToDevice, st));

@@ -10,6 +10,7 @@
 // The result is an exact float64 built from the top `kept` mantissa bits.
 // A probe = that decode + the inverse DWT + a reduction fused into the last
 // row pass; no intermediate field is written at level 0.
+#include "idwt_fused.cuh"
 #include "lift.cuh"
 #include "probe.cuh"
 
@@ -24,6 +25,11 @@ __device__ __forceinline__ unsigned int f32_key(float v) {
 __device__ __forceinline__ float key_f32(unsigned int k) {
   unsigned int u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
   return __uint_as_float(u);
+}
+
+__global__ void mm_init_kernel(unsigned int* mm, int nfields) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nfields) { mm[2 * f] = 0xffffffffu; mm[2 * f + 1] = 0u; }
 }
 
 __global__ void minmax_kernel(const float* __restrict__ x, int64_t n, unsigned int* mm) {
@@ -78,39 +84,30 @@ __global__ void decode_coeffs_kernel(Meta m, const ProbeParam* __restrict__ prm,
   const int f = blockIdx.y;
   const ProbeParam P = prm[f];
   if (!P.active) return;
-  __shared__ uint32_t rs[kMaxPlaneRecs];
-  const PlaneRec* pr = m.planes + (int64_t)f * kMaxPlaneRecs;
+  __shared__ uint64_t T[kMaxPlaneRecs];
   const int n_max = m.mo[f].n_max;
   int planes = P.planes, n_last = P.n_last;
-  if (planes < 0) {  // decoder path: planes entered and n_last come from the machine
+  if (planes < 0) {
     planes = m.mo[f].planes_run;
     n_last = planes > 0 ? n_max - (planes - 1) : n_max;
   }
-  for (int p = threadIdx.x; p < kMaxPlaneRecs; p += blockDim.x)
-    rs[p] = p < planes ? pr[p].refine_start : 0xffffffffu;
+  fused::build_thresholds(T, m.planes + (int64_t)f * kMaxPlaneRecs, planes, P.B);
   __syncthreads();
   const int64_t fo = (int64_t)f * m.stride;
   const double off = P.midpoint ? scalbn(0.5, n_last) : 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t sp = m.sign_pos[fo + i];
-    double v = 0.0;
-    if (sp != kNone && (uint64_t)sp < P.B) {
-      uint8_t pi = m.pinfo[fo + i];
-      int ps = pi & 0x3f;
-      uint64_t rank = m.lsp_rank[fo + i];
-      int lim = planes - 1 < ps + 31 ? planes - 1 : ps + 31;
-      int pm = ps;
-      while (pm < lim && (uint64_t)rs[pm + 1] + rank < P.B) pm++;
-      int kept = pm - ps + 1;
-      uint32_t K = m.mant[fo + i] >> (32 - kept);
-      v = scalbn((double)K, n_max - pm);
-      bool neg = pi & 0x80;
-      if (neg) v = -v;
-      if (P.midpoint) v = __dadd_rn(v, neg ? -off : off);
-    }
-    out[(int64_t)f * n + i] = v;
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[(int64_t)f * n + i] = fused::decode_raw(m.packed[fo + i], P.B, planes, n_max,
+                                                P.midpoint != 0, off, T);
+}
+
+__global__ void pack_meta_kernel(MachineBufs mb, uint4* packed) {
+  const int f = blockIdx.y;
+  const int64_t fo = (int64_t)f * mb.stride;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < mb.stride;
+       i += (int64_t)gridDim.x * blockDim.x)
+    packed[fo + i] = make_uint4(mb.sign_pos[fo + i], mb.lsp_rank[fo + i], mb.mant[fo + i],
+                                mb.pinfo[fo + i]);
 }
 
 // ---- epilogues for the last (level-0 row) pass -----------------------------
@@ -146,9 +143,11 @@ struct BaseProbeEpi {
     return true;
   }
   __device__ void store(double*, int f, int64_t off, double dec) {
-    double nv = norm[(int64_t)f * n + off];
+    float o = orig[(int64_t)f * n + off];
+    // normalised value recomputed exactly like core.normalize (core.py:179)
+    double nv = __ddiv_rn(__dsub_rn((double)o, s.vmin), s.range);
     cnt += fabs(__dsub_rn(dec, nv)) <= s.eps_rel;
-    double e = denorm_err(s, dec, orig[(int64_t)f * n + off]);
+    double e = denorm_err(s, dec, o);
     mx = e > mx ? e : mx;
   }
   __device__ void finish(int f) { warp_flush(&res[f], cnt, mx, true); }
@@ -205,22 +204,6 @@ struct AddDenormEpi {
   }
   __device__ void finish(int) {}
 };
-
-// levels L-1..1 fully, then level 0 columns; leaves the level-0 row pass to
-// the caller's epilogue.  a holds coefficients on entry.
-void inverse_all_but_last(double* a, double* b, const Geo& g, int nfields, cudaStream_t st) {
-  for (int k = g.levels - 1; k >= 1; k--) {
-    inverse_level_cols(a, b, g.n, nfields, g, k, st);
-    inverse_level_rows(b, a, g.n, nfields, g, k, st);
-  }
-  inverse_level_cols(a, b, g.n, nfields, g, 0, st);
-}
-
-template <class Epi>
-void last_rows(const double* b, double* a, const Geo& g, int nfields, cudaStream_t st,
-               const Epi& epi) {
-  lift::launch_pass_epi<true, Epi>(b, a, g.n, nfields, g.cols, g.rows, g.cols, false, st, epi);
-}
 
 int grid_for(int64_t n, int cap = 2048) {
   int64_t b = (n + 255) / 256;
@@ -281,17 +264,15 @@ __global__ void unpack_kernel(const UnpackPart* parts, const uint8_t* in) {
 }  // namespace
 
 void ingest_normalize(const float* x, int64_t n, int nfields, double* norm, FieldScal* fs,
-                      double eps_rel, cudaStream_t st) {
-  unsigned int* mm = nullptr;
-  cudaMallocAsync(&mm, sizeof(unsigned int) * 2 * nfields, st);
-  // lo starts at 0xffffffff, hi at 0
-  cudaMemsetAsync(mm, 0, sizeof(unsigned int) * 2 * nfields, st);
-  // set lo slots to all ones
-  for (int f = 0; f < nfields; f++) cudaMemsetAsync(mm + 2 * f, 0xff, sizeof(unsigned int), st);
+                      unsigned int* mm, double eps_rel, cudaStream_t st) {
+  mm_init_kernel<<<(nfields + 127) / 128, 128, 0, st>>>(mm, nfields);
   minmax_kernel<<<dim3(grid_for(n, 512), nfields), 256, 0, st>>>(x, n, mm);
   scalars_kernel<<<(nfields + 127) / 128, 128, 0, st>>>(mm, nfields, eps_rel, fs);
   normalize_kernel<<<dim3(grid_for(n, 1024), nfields), 256, 0, st>>>(x, n, fs, norm);
-  cudaFreeAsync(mm, st);
+}
+
+void pack_meta(const MachineBufs& mb, uint4* packed, cudaStream_t st) {
+  pack_meta_kernel<<<dim3(grid_for(mb.stride, 1024), mb.nfields), 256, 0, st>>>(mb, packed);
 }
 
 void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, int nfields,
@@ -302,45 +283,35 @@ void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, i
 void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                 int nfields, const double* norm, const float* orig, const FieldScal* fs,
                 ProbeResult* res, cudaStream_t st) {
-  decode_coeffs(m, prm, a, g.n, nfields, st);
-  inverse_all_but_last(a, b, g, nfields, st);
   BaseProbeEpi e{norm, orig, fs, prm, res, g.n, 0, 0.0, FieldScal{}};
-  last_rows(b, a, g, nfields, st, e);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e);
 }
 
 void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                  int nfields, const double* base_dec, const float* orig, const FieldScal* fs,
                  ProbeResult* res, cudaStream_t st) {
-  decode_coeffs(m, prm, a, g.n, nfields, st);
-  inverse_all_but_last(a, b, g, nfields, st);
   TruncProbeEpi e{base_dec, orig, fs, prm, res, g.n, 0.0, FieldScal{}};
-  last_rows(b, a, g, nfields, st, e);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e);
 }
 
 void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                      int nfields, const double* norm, double* base_dec, double* resid,
                      cudaStream_t st) {
-  decode_coeffs(m, prm, a, g.n, nfields, st);
-  inverse_all_but_last(a, b, g, nfields, st);
   ResidueEpi e{norm, base_dec, resid, prm, g.n};
-  last_rows(b, a, g, nfields, st, e);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e);
 }
 
 void decode_field(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                   int nfields, double* out, cudaStream_t st) {
-  decode_coeffs(m, prm, a, g.n, nfields, st);
-  inverse_all_but_last(a, b, g, nfields, st);
   StoreFieldEpi e{out, prm, g.n};
-  last_rows(b, a, g, nfields, st, e);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e);
 }
 
 void decode_field_add_denorm(const Meta& m, const ProbeParam* prm, double* a, double* b,
                              const Geo& g, int nfields, const double* base, const FieldScal* fs,
                              float* out32, cudaStream_t st) {
-  decode_coeffs(m, prm, a, g.n, nfields, st);
-  inverse_all_but_last(a, b, g, nfields, st);
   AddDenormEpi e{base, fs, prm, out32, g.n, FieldScal{}};
-  last_rows(b, a, g, nfields, st, e);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e);
 }
 
 void denorm_only(const double* base, const FieldScal* fs, const uint8_t* active, int64_t n,

@@ -30,19 +30,22 @@ struct ProbeResult {
   unsigned long long maxerr;  // bits of max |f32(denorm(rec)) - orig| (non-negative double)
 };
 
-struct Meta {  // per-coefficient closed-form metadata (one field = `stride` entries)
-  const uint32_t* mant;
-  const uint32_t* sign_pos;
-  const uint32_t* lsp_rank;
-  const uint8_t* pinfo;
+// Per-coefficient closed-form metadata packed for the probes: one 16-byte
+// load per coefficient = {sign bit offset, LSP rank, top-32 significand bits,
+// pinfo (plane index | sign << 7)}.
+struct Meta {  // one field = `stride` entries
+  const uint4* packed;
   const PlaneRec* planes;
   const MachineOut* mo;
   int64_t stride;
 };
 
+// build Meta::packed from the machine's per-coefficient arrays
+void pack_meta(const MachineBufs& mb, uint4* packed, cudaStream_t st);
+
 // f32 input -> per-field vmin/vmax/constant flag and float64 normalised field
 void ingest_normalize(const float* x, int64_t n, int nfields, double* norm, FieldScal* fs,
-                      double eps_rel, cudaStream_t st);
+                      unsigned int* mm, double eps_rel, cudaStream_t st);
 
 // closed-form prefix decode into coefficient buffer `a`
 void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, int nfields,
