@@ -112,6 +112,11 @@ int ebcc_spiht_encode(ebcc_ctx *ctx, const double *coeffs, int32_t rows, int32_t
 int ebcc_spiht_decode(ebcc_ctx *ctx, const uint8_t *data, int64_t len, int64_t prefix_len,
                       int32_t rows, int32_t cols, double *coeffs_out, int32_t *n_last);
 
+/* Self-test of the FMA-corrected exact divisions used by the kernels
+ * (x / SCALE_LOW, x / SCALE_HIGH, x / range) against IEEE __ddiv_rn on n
+ * random operands; *mismatches must be 0. */
+int ebcc_selftest_div(ebcc_ctx *ctx, int64_t n, uint64_t seed, int64_t *mismatches);
+
 /* Instrumentation for bench.py: kernels launched and device milliseconds
  * (CUDA events on the library stream) of the last call, split by stage. */
 typedef struct {

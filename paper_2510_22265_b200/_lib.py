@@ -26,7 +26,8 @@ OUTPUT_ON_DEVICE = 2
 # the exported symbols include/ebcc_gpu.h declares (checked by the CPU tests)
 EXPORTS = ("ebcc_abi_version", "ebcc_create", "ebcc_destroy", "ebcc_set_stream",
            "ebcc_last_error", "ebcc_compress", "ebcc_fetch_payload", "ebcc_decompress",
-           "ebcc_get_stats", "ebcc_dwt", "ebcc_spiht_encode", "ebcc_spiht_decode")
+           "ebcc_get_stats", "ebcc_dwt", "ebcc_spiht_encode", "ebcc_spiht_decode",
+           "ebcc_selftest_div")
 
 
 class ChunkRec(ctypes.Structure):
@@ -82,6 +83,7 @@ def load(path: str = LIB_PATH):
         L.ebcc_dwt.argtypes = [P, P, P, i64, i32, i32, i32, i32]
         L.ebcc_spiht_encode.argtypes = [P, P, i32, i32, i32, i32, P, i64, ctypes.POINTER(i64)]
         L.ebcc_spiht_decode.argtypes = [P, P, i64, i64, i32, i32, P, ctypes.POINTER(i32)]
+        L.ebcc_selftest_div.argtypes = [P, i64, ctypes.c_uint64, ctypes.POINTER(i64)]
         _lib = L
         return L
 
@@ -212,6 +214,13 @@ class Context:
                                         cols, out.ctypes.data, ctypes.byref(nl))
         self.raise_for(st, "ebcc_spiht_decode")
         return out, (None if nl.value == -999 else nl.value)
+
+
+    def selftest_div(self, n: int, seed: int = 1) -> int:
+        bad = ctypes.c_int64(0)
+        st = self.lib.ebcc_selftest_div(self.handle, int(n), int(seed), ctypes.byref(bad))
+        self.raise_for(st, "ebcc_selftest_div")
+        return int(bad.value)
 
 
 _contexts: dict = {}

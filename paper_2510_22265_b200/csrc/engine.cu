@@ -980,6 +980,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         const ebcc_chunk_rec& r = recs[f0 + i];
         fsv[i] = FieldScal{};
         fsv[i].vmin = r.vmin; fsv[i].vmax = r.vmax; fsv[i].range = r.vmax - r.vmin;
+        fsv[i].range_inv = fsv[i].range != 0.0 ? 1.0 / fsv[i].range : 0.0;
         bmo[i] = MachineOut{}; rmo[i] = MachineOut{};
         bmo[i].n_max = kExpNone; rmo[i].n_max = kExpNone;
         if (r.mode == EBCC_MODE_CONSTANT) { cst[i] = 1; continue; }
@@ -1226,6 +1227,26 @@ int ebcc_spiht_decode(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t pre
     CK(cudaStreamSynchronize(st));
     if (nm == kZeroSentinel) *n_last = -999;
     else *n_last = mo[0].planes_run > 0 ? nm - (mo[0].planes_run - 1) : nm;
+    return EBCC_OK;
+  } catch (CudaFail& e) {
+    cudaGetLastError();
+    return fail(c, EBCC_E_CUDA, std::string(e.what) + ": " + cudaGetErrorString(e.e));
+  }
+}
+
+int ebcc_selftest_div(ebcc_ctx* c, int64_t n, uint64_t seed, int64_t* mismatches) {
+  if (!c || !mismatches || n < 1) return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  try {
+    CK(cudaSetDevice(c->device));
+    unsigned long long* d = dalloc<unsigned long long>(1);
+    CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->stream));
+    selftest_div(n, seed, d, c->stream);
+    CK(cudaGetLastError());
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(d);
+    *mismatches = (int64_t)h;
     return EBCC_OK;
   } catch (CudaFail& e) {
     cudaGetLastError();

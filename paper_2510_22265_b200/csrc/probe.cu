@@ -61,6 +61,7 @@ __global__ void scalars_kernel(const unsigned int* mm, int nfields, double eps_r
   double range = __dsub_rn(vmax, vmin);
   FieldScal s;
   s.vmin = vmin; s.vmax = vmax; s.range = range;
+  s.range_inv = __drcp_rn(range);
   s.eps_rel = eps_rel;
   s.eps_abs = __dmul_rn(eps_rel, range);
   s.constant = range < 1e-30;
@@ -145,7 +146,7 @@ struct BaseProbeEpi {
   __device__ void store(double*, int f, int64_t off, double dec) {
     float o = orig[(int64_t)f * n + off];
     // normalised value recomputed exactly like core.normalize (core.py:179)
-    double nv = __ddiv_rn(__dsub_rn((double)o, s.vmin), s.range);
+    double nv = fused::div_exact(__dsub_rn((double)o, s.vmin), s.range, s.range_inv);
     cnt += fabs(__dsub_rn(dec, nv)) <= s.eps_rel;
     double e = denorm_err(s, dec, o);
     mx = e > mx ? e : mx;
@@ -269,6 +270,47 @@ void ingest_normalize(const float* x, int64_t n, int nfields, double* norm, Fiel
   minmax_kernel<<<dim3(grid_for(n, 512), nfields), 256, 0, st>>>(x, n, mm);
   scalars_kernel<<<(nfields + 127) / 128, 128, 0, st>>>(mm, nfields, eps_rel, fs);
   normalize_kernel<<<dim3(grid_for(n, 1024), nfields), 256, 0, st>>>(x, n, fs, norm);
+}
+
+namespace {
+// splitmix64
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double rand_double(uint64_t r, int emin, int emax) {
+  // random sign, exponent in [emin, emax], random 52-bit significand
+  int e = emin + (int)((r >> 52) % (uint64_t)(emax - emin + 1));
+  uint64_t bits = ((uint64_t)(e + 1023) << 52) | (r & ((1ull << 52) - 1));
+  if ((r >> 63) & 1) bits |= 1ull << 63;
+  return __longlong_as_double((long long)bits);
+}
+__global__ void selftest_div_kernel(int64_t n, uint64_t seed, unsigned long long* bad) {
+  unsigned long long local = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t r1 = mix64(seed ^ (uint64_t)i), r2 = mix64(r1), r3 = mix64(r2);
+    double x = rand_double(r1, -60, 60);
+    if ((r3 & 15) == 0) x = (double)(int64_t)(r3 >> 40);  // integers, incl. 0
+    // the two scale constants (inverse DWT)
+    local += __double_as_longlong(fused::div_scale(x, EBCC_SCALE_LOW, EBCC_INV_SL)) !=
+             __double_as_longlong(__ddiv_rn(x, EBCC_SCALE_LOW));
+    local += __double_as_longlong(fused::div_scale(x, EBCC_SCALE_HIGH, EBCC_INV_SH)) !=
+             __double_as_longlong(__ddiv_rn(x, EBCC_SCALE_HIGH));
+    // runtime divisors (normalisation by the value range)
+    double b = fabs(rand_double(r2, -40, 40));
+    local += __double_as_longlong(fused::div_exact(x, b, __drcp_rn(b))) !=
+             __double_as_longlong(__ddiv_rn(x, b));
+  }
+  for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(bad, local);
+}
+}  // namespace
+
+void selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t st) {
+  selftest_div_kernel<<<148 * 8, 256, 0, st>>>(n, seed, bad);
 }
 
 void pack_meta(const MachineBufs& mb, uint4* packed, cudaStream_t st) {

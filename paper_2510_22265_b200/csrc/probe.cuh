@@ -10,6 +10,7 @@ namespace ebcc {
 // per-field scalars shared by all probes
 struct FieldScal {
   double vmin, vmax, range;  // range = vmax - vmin (float64, like the reference)
+  double range_inv;          // RN(1/range), for the FMA-corrected exact division
   double eps_rel, eps_abs;
   int32_t constant;
   int32_t pad;
@@ -39,6 +40,9 @@ struct Meta {  // one field = `stride` entries
   const MachineOut* mo;
   int64_t stride;
 };
+
+// GPU self-test: FMA-corrected exact divisions vs __ddiv_rn on n random cases
+void selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t st);
 
 // build Meta::packed from the machine's per-coefficient arrays
 void pack_meta(const MachineBufs& mb, uint4* packed, cudaStream_t st);

@@ -201,3 +201,9 @@ def test_random_fields_vs_oracle(ebcc, oracle):
         if got != want:
             bad.append((kind, r, c, eps, q))
     assert not bad, bad
+
+
+def test_fma_corrected_division_is_exact(ctx):
+    """The kernels replace x/SCALE and x/range by an FMA-corrected reciprocal
+    multiply; it must equal IEEE division bit for bit (2^28 cases x 3)."""
+    assert ctx.selftest_div(1 << 28, seed=20251020) == 0
