@@ -85,7 +85,7 @@ __global__ void decode_coeffs_kernel(Meta m, const ProbeParam* __restrict__ prm,
   const int f = blockIdx.y;
   const ProbeParam P = prm[f];
   if (!P.active) return;
-  __shared__ uint64_t T[kMaxPlaneRecs];
+  __shared__ uint32_t T[kMaxPlaneRecs];
   const int n_max = m.mo[f].n_max;
   int planes = P.planes, n_last = P.n_last;
   if (planes < 0) {
@@ -137,6 +137,7 @@ struct BaseProbeEpi {
   const double* norm; const float* orig; const FieldScal* fs; const ProbeParam* prm;
   ProbeResult* res; int64_t n;
   unsigned long long cnt; double mx; FieldScal s;
+  __device__ void prefetch(int f, int64_t off) const { fused::prefetch_l2(orig + (int64_t)f * n + off); }
   __device__ bool begin(int f) {
     cnt = 0; mx = 0.0;
     if (!prm[f].active) return false;
@@ -158,6 +159,10 @@ struct TruncProbeEpi {
   const double* base; const float* orig; const FieldScal* fs; const ProbeParam* prm;
   ProbeResult* res; int64_t n;
   double mx; FieldScal s;
+  __device__ void prefetch(int f, int64_t off) const {
+    fused::prefetch_l2(orig + (int64_t)f * n + off);
+    fused::prefetch_l2(base + (int64_t)f * n + off);
+  }
   __device__ bool begin(int f) {
     mx = 0.0;
     if (!prm[f].active) return false;
@@ -174,6 +179,7 @@ struct TruncProbeEpi {
 
 struct ResidueEpi {
   const double* norm; double* base_dec; double* resid; const ProbeParam* prm; int64_t n;
+  __device__ void prefetch(int f, int64_t off) const { fused::prefetch_l2(norm + (int64_t)f * n + off); }
   __device__ bool begin(int f) { return prm[f].active != 0; }
   __device__ void store(double*, int f, int64_t off, double dec) {
     int64_t o = (int64_t)f * n + off;
@@ -185,6 +191,7 @@ struct ResidueEpi {
 
 struct StoreFieldEpi {
   double* out; const ProbeParam* prm; int64_t n;
+  __device__ void prefetch(int, int64_t) const {}
   __device__ bool begin(int f) { return prm[f].active != 0; }
   __device__ void store(double*, int f, int64_t off, double v) { out[(int64_t)f * n + off] = v; }
   __device__ void finish(int) {}
@@ -193,6 +200,7 @@ struct StoreFieldEpi {
 struct AddDenormEpi {
   const double* base; const FieldScal* fs; const ProbeParam* prm; float* out32; int64_t n;
   FieldScal s;
+  __device__ void prefetch(int f, int64_t off) const { fused::prefetch_l2(base + (int64_t)f * n + off); }
   __device__ bool begin(int f) {
     if (!prm[f].active) return false;
     s = fs[f];
