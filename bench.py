@@ -157,6 +157,7 @@ def run_ours(args, rank, world, local_rank):
     launches = 0
     probe_ms = probe_steps = 0.0
     enc_ms = 0.0
+    l0_ms = l0_n = 0.0
     for _ in range(args.steps):
         flush.zero_()
         if world > 1:
@@ -182,6 +183,8 @@ def run_ours(args, rank, world, local_rank):
         probe_ms += cst["ms_probe"]
         probe_steps += cst["probe_launches"]
         enc_ms += cst["ms_encode"]
+        l0_ms += cst["ms_probe_kernel"]
+        l0_n += cst["probe_kernel_count"]
     clocks = sampler.stop()
 
     # size/offset all-gather: the one collective of the sharded path
@@ -221,10 +224,12 @@ def run_ours(args, rank, world, local_rank):
     p_base = int(recs["n_base_probes"].sum())
     p_trunc = int(recs["n_trunc_probes"].sum())
 
-    # roofline of the dominant stage: one batched feedback probe (closed-form
-    # decode -> 5-level IDWT -> fused reduction over all 37 fields).
-    # Algorithmic bytes per probe step = 4 B * N * fields (SURVEY.md §8(d):
-    # each evaluation must re-read the N original float32 values).
+    # roofline of the dominant kernel: the level-0 fused IDWT probe kernel
+    # (closed-form decode + last synthesis level + fused reduction), one
+    # launch per feedback probe over all 37 fields, timed live with CUDA
+    # events around each launch.  Algorithmic bytes per launch = 4 B * N *
+    # fields (an evaluation must re-read the N original
+    # float32 values at least once).
     peaks = {}
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
@@ -232,8 +237,17 @@ def run_ours(args, rank, world, local_rank):
     except OSError:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    probe_avg_s = (probe_ms / 1e3) / max(1.0, probe_steps)
-    achieved = (4.0 * n * nf) / probe_avg_s / 1e9 if probe_steps else 0.0
+    traffic = None
+    try:
+        import glob
+        tf = sorted(glob.glob(os.path.join(REPO, "profiles", "r*_level0_traffic.json")))[-1]
+        with open(tf) as fh:
+            tj = json.load(fh)
+        traffic = int(tj["dram__bytes_read.sum"] + tj["dram__bytes_write.sum"])
+    except (IndexError, OSError, KeyError, ValueError):
+        pass
+    l0_avg_s = (l0_ms / 1e3) / max(1.0, l0_n)
+    achieved = (4.0 * n * nf) / l0_avg_s / 1e9 if l0_n else 0.0
     comp_alg = (4.0 * n * nf + total_payload / world + 4.0 * n * (p_base + p_trunc))
     comp_alg_gbs = comp_alg * steps / t_c / 1e9
 
@@ -267,8 +281,12 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(len(blob) + bytes_in)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": None,
-                     "kernel": "feedback probe step (decode+IDWT+fused reduction, 37 fields)",
+                     "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
+                     "kernel": "fused::level_kernel level 0 (decode + synthesis + reduction), "
+                               "one launch per probe over 37 fields",
+                     "kernel_avg_us": round(l0_avg_s * 1e6, 2),
+                     "algorithmic_bytes_per_launch": int(4 * n * nf),
+                     "traffic_source": "profiles/r*_level0_traffic.json (ncu --set full, one launch)",
                      "compress_algorithmic_gbs": round(comp_alg_gbs, 2),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         "clocks": clocks,

@@ -30,6 +30,7 @@
 
 #include "../../include/ebcc_gpu.h"
 #include "dwt.cuh"
+#include "idwt_fused.cuh"
 #include "probe.cuh"
 #include "spiht.cuh"
 
@@ -275,7 +276,7 @@ struct ebcc_ctx {
   float* d_out = nullptr;
   int64_t out_cap = 0;
   ebcc_stats stats{};
-  cudaEvent_t ev[8] = {};
+  fused::Level0Timer l0;
 };
 
 namespace {
@@ -473,6 +474,14 @@ struct EventTimer {
   }
 };
 
+void accumulate_level0(ebcc_ctx* c) {
+  float ms = 0;
+  if (cudaEventElapsedTime(&ms, c->l0.a, c->l0.b) == cudaSuccess) {
+    c->stats.ms_probe_kernel += ms;
+    c->stats.probe_kernel_count++;
+  }
+}
+
 // one compress batch of nfields (<= workspace capacity); x already in w.x32
 int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0, double tol,
                    ebcc_chunk_rec* recs, int64_t out_base_off, std::vector<PackPart>& parts,
@@ -552,12 +561,15 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
       CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
       CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
+      fused::g_level0_timer = &c->l0;
       probe_base(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.x32, w.fs, w.res, st);
+      fused::g_level0_timer = nullptr;
       c->stats.kernel_launches += g.levels;
       c->stats.probe_launches++;
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      accumulate_level0(c);
       memcpy(res.data(), w.h_res, sizeof(ProbeResult) * nfields);
       for (int f = 0; f < nfields; f++) {
         if (!prm[f].active) continue;
@@ -662,12 +674,15 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
     CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
+    fused::g_level0_timer = &c->l0;
     probe_trunc(mres, w.prm, w.A, w.B, g, nfields, w.base_dec, w.x32, w.fs, w.res, st);
+    fused::g_level0_timer = nullptr;
     c->stats.kernel_launches += g.levels;
     c->stats.probe_launches++;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    accumulate_level0(c);
     memcpy(res.data(), w.h_res, sizeof(ProbeResult) * nfields);
     for (int f = 0; f < nfields; f++) {
       if (!prm[f].active) continue;
@@ -775,6 +790,8 @@ int ebcc_create(int32_t device, ebcc_ctx** out) {
   c->device = device;
   e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) { delete c; return EBCC_E_CUDA; }
+  cudaEventCreate(&c->l0.a);
+  cudaEventCreate(&c->l0.b);
   c->own_stream = true;
   *out = c;
   return EBCC_OK;
@@ -790,6 +807,8 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->d_stage) cudaFree(c->d_stage);
   if (c->d_out) cudaFree(c->d_out);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->l0.a) cudaEventDestroy(c->l0.a);
+  if (c->l0.b) cudaEventDestroy(c->l0.b);
   delete c;
 }
 

@@ -16,6 +16,10 @@
 
 namespace ebcc {
 
+namespace fused {
+thread_local Level0Timer* g_level0_timer = nullptr;
+}
+
 namespace {
 
 __device__ __forceinline__ unsigned int f32_key(float v) {
