@@ -141,15 +141,15 @@ struct BaseProbeEpi {
   const double* norm; const float* orig; const FieldScal* fs; const ProbeParam* prm;
   ProbeResult* res; int64_t n;
   unsigned long long cnt; double mx; FieldScal s;
-  __device__ void prefetch(int f, int64_t off) const { fused::prefetch_l2(orig + (int64_t)f * n + off); }
+  using Pre = float;
+  __device__ Pre pre(int f, int64_t off) const { return orig[(int64_t)f * n + off]; }
   __device__ bool begin(int f) {
     cnt = 0; mx = 0.0;
     if (!prm[f].active) return false;
     s = fs[f];
     return true;
   }
-  __device__ void store(double*, int f, int64_t off, double dec) {
-    float o = orig[(int64_t)f * n + off];
+  __device__ void put(double*, int f, int64_t off, double dec, float o) {
     // normalised value recomputed exactly like core.normalize (core.py:179)
     double nv = fused::div_exact(__dsub_rn((double)o, s.vmin), s.range, s.range_inv);
     cnt += fabs(__dsub_rn(dec, nv)) <= s.eps_rel;
@@ -159,13 +159,18 @@ struct BaseProbeEpi {
   __device__ void finish(int f) { warp_flush(&res[f], cnt, mx, true); }
 };
 
+struct TruncPre {
+  double base;
+  float orig;
+};
+
 struct TruncProbeEpi {
   const double* base; const float* orig; const FieldScal* fs; const ProbeParam* prm;
   ProbeResult* res; int64_t n;
   double mx; FieldScal s;
-  __device__ void prefetch(int f, int64_t off) const {
-    fused::prefetch_l2(orig + (int64_t)f * n + off);
-    fused::prefetch_l2(base + (int64_t)f * n + off);
+  using Pre = TruncPre;
+  __device__ Pre pre(int f, int64_t off) const {
+    return {base[(int64_t)f * n + off], orig[(int64_t)f * n + off]};
   }
   __device__ bool begin(int f) {
     mx = 0.0;
@@ -173,9 +178,9 @@ struct TruncProbeEpi {
     s = fs[f];
     return true;
   }
-  __device__ void store(double*, int f, int64_t off, double v) {
-    double rec = __dadd_rn(base[(int64_t)f * n + off], v);  // base_field + dequantized
-    double e = denorm_err(s, rec, orig[(int64_t)f * n + off]);
+  __device__ void put(double*, int f, int64_t off, double v, const Pre& p) {
+    double rec = __dadd_rn(p.base, v);  // base_field + dequantized
+    double e = denorm_err(s, rec, p.orig);
     mx = e > mx ? e : mx;
   }
   __device__ void finish(int f) { warp_flush(&res[f], 0, mx, false); }
@@ -183,36 +188,41 @@ struct TruncProbeEpi {
 
 struct ResidueEpi {
   const double* norm; double* base_dec; double* resid; const ProbeParam* prm; int64_t n;
-  __device__ void prefetch(int f, int64_t off) const { fused::prefetch_l2(norm + (int64_t)f * n + off); }
+  using Pre = double;
+  __device__ Pre pre(int f, int64_t off) const { return norm[(int64_t)f * n + off]; }
   __device__ bool begin(int f) { return prm[f].active != 0; }
-  __device__ void store(double*, int f, int64_t off, double dec) {
+  __device__ void put(double*, int f, int64_t off, double dec, double nv) {
     int64_t o = (int64_t)f * n + off;
     base_dec[o] = dec;
-    resid[o] = __dsub_rn(norm[o], dec);  // nc.values - base_enc.decoded
+    resid[o] = __dsub_rn(nv, dec);  // nc.values - base_enc.decoded
   }
   __device__ void finish(int) {}
 };
 
 struct StoreFieldEpi {
   double* out; const ProbeParam* prm; int64_t n;
-  __device__ void prefetch(int, int64_t) const {}
+  using Pre = fused::NoPre;
+  __device__ Pre pre(int, int64_t) const { return {}; }
   __device__ bool begin(int f) { return prm[f].active != 0; }
-  __device__ void store(double*, int f, int64_t off, double v) { out[(int64_t)f * n + off] = v; }
+  __device__ void put(double*, int f, int64_t off, double v, const Pre&) {
+    out[(int64_t)f * n + off] = v;
+  }
   __device__ void finish(int) {}
 };
 
 struct AddDenormEpi {
   const double* base; const FieldScal* fs; const ProbeParam* prm; float* out32; int64_t n;
   FieldScal s;
-  __device__ void prefetch(int f, int64_t off) const { fused::prefetch_l2(base + (int64_t)f * n + off); }
+  using Pre = double;
+  __device__ Pre pre(int f, int64_t off) const { return base[(int64_t)f * n + off]; }
   __device__ bool begin(int f) {
     if (!prm[f].active) return false;
     s = fs[f];
     return true;
   }
-  __device__ void store(double*, int f, int64_t off, double v) {
+  __device__ void put(double*, int f, int64_t off, double v, double b) {
     int64_t o = (int64_t)f * n + off;
-    double fld = __dadd_rn(base[o], v);
+    double fld = __dadd_rn(b, v);
     out32[o] = __double2float_rn(__dadd_rn(s.vmin, __dmul_rn(fld, s.range)));
   }
   __device__ void finish(int) {}
