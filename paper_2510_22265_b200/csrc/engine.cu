@@ -218,8 +218,9 @@ struct Workspace {
   uint32_t *mant = nullptr, *sign_pos = nullptr, *lsp_rank = nullptr;
   uint8_t* pinfo = nullptr;
   uint4* packed = nullptr;
-  uint32_t *lip = nullptr, *lis0 = nullptr, *lis1 = nullptr, *w0 = nullptr, *w1 = nullptr,
-           *lsp = nullptr;
+  uint64_t *lip = nullptr, *lis0 = nullptr, *lis1 = nullptr, *w0 = nullptr, *w1 = nullptr;
+  uint32_t* lsp = nullptr;
+  uint64_t* ninfo = nullptr;
   uint32_t *bits_base = nullptr, *bits_res = nullptr;
   int64_t words_base = 0, words_res = 0;
   PlaneRec *pl_base = nullptr, *pl_res = nullptr;
@@ -237,7 +238,7 @@ struct Workspace {
   bool has_tt = false;
 
   void release() {
-    void* ptrs[] = {x32, norm, A, B, base_dec, ec, ed, el, mant, sign_pos, lsp_rank, pinfo, packed,
+    void* ptrs[] = {x32, norm, A, B, base_dec, ec, ed, el, mant, sign_pos, lsp_rank, pinfo, packed, ninfo,
                     lip, lis0, lis1, w0, w1, lsp, bits_base, bits_res, pl_base, pl_res,
                     mo_base, mo_res, fs, prm, res, limit, active, mm};
     for (void* p : ptrs)
@@ -303,12 +304,13 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   w.lsp_rank = dalloc<uint32_t>(N);
   w.pinfo = dalloc<uint8_t>(N);
   w.packed = dalloc<uint4>(N);
-  w.lip = dalloc<uint32_t>(N);
-  w.lis0 = dalloc<uint32_t>(N);
-  w.lis1 = dalloc<uint32_t>(N);
-  w.w0 = dalloc<uint32_t>(N);
-  w.w1 = dalloc<uint32_t>(N);
+  w.lip = dalloc<uint64_t>(N);
+  w.lis0 = dalloc<uint64_t>(N);
+  w.lis1 = dalloc<uint64_t>(N);
+  w.w0 = dalloc<uint64_t>(N);
+  w.w1 = dalloc<uint64_t>(N);
   w.lsp = dalloc<uint32_t>(N);
+  w.ninfo = dalloc<uint64_t>(N);
   w.words_base = words_for(g.n, kBasePlanes);
   w.words_res = words_for(g.n, kMaxDecodePlanes > kDeepPlanes ? kDeepPlanes : kDeepPlanes);
   w.bits_base = dalloc<uint32_t>(w.words_base * cap);
@@ -337,6 +339,8 @@ MachineBufs machine_bufs(Workspace& w, int nfields, bool residual) {
   mb.ec = w.ec; mb.ed = w.ed; mb.el = w.el;
   mb.mant = w.mant; mb.sign_pos = w.sign_pos; mb.lsp_rank = w.lsp_rank; mb.pinfo = w.pinfo;
   mb.lip = w.lip; mb.lis0 = w.lis0; mb.lis1 = w.lis1; mb.w0 = w.w0; mb.w1 = w.w1; mb.lsp = w.lsp;
+  mb.ninfo = w.ninfo;
+  mb.ginfo = w.tt.ginfo;
   mb.bits = residual ? w.bits_res : w.bits_base;
   mb.planes = residual ? w.pl_res : w.pl_base;
   mb.out = residual ? w.mo_res : w.mo_base;
@@ -851,7 +855,7 @@ int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
     // batch capacity from free memory (~100 B per point per field in flight)
     size_t freeb = 0, totalb = 0;
     CK(cudaMemGetInfo(&freeb, &totalb));
-    int64_t per_field = g.n * 104 + 4096;
+    int64_t per_field = g.n * 160 + 4096;
     int64_t cap = (int64_t)((freeb * 0.6) / per_field);
     if (cap < 1) cap = 1;
     if (cap > nfields) cap = nfields;
@@ -972,7 +976,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
     cudaEventRecord(t0, st);
     size_t freeb = 0, totalb = 0;
     CK(cudaMemGetInfo(&freeb, &totalb));
-    int64_t per_field = g.n * 104 + 4096;
+    int64_t per_field = g.n * 160 + 4096;
     int64_t cap = (int64_t)((freeb * 0.6) / per_field);
     if (cap < 1) cap = 1;
     if (cap > nfields) cap = nfields;

@@ -16,6 +16,7 @@
 // The same machine runs as encoder (significance from exponents) or decoder
 // (significance read from the stream at the offset the scan assigns), which is
 // how the reference keeps encoder and decoder in lockstep.
+#include <algorithm>
 #include <vector>
 
 #include "spiht.cuh"
@@ -34,7 +35,10 @@ constexpr uint32_t TYPE_B = 0x80000000u;
 
 // ---------------------------------------------------------------------------
 // tree tables
-__global__ void tree_flags_kernel(Geo g, uint8_t* flags) {
+__device__ __forceinline__ uint64_t bitsat(uint64_t v, int at) { return v << at; }
+
+// geometry node info: children count, has-grandchildren, band level/orientation
+__global__ void tree_info_kernel(Geo g, uint64_t* ginfo) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= g.n) return;
   int r = (int)(idx / g.cols), c = (int)(idx - (int64_t)r * g.cols);
@@ -46,8 +50,53 @@ __global__ void tree_flags_kernel(Geo g, uint8_t* flags) {
     int rr = (int)(ch[s] / g.cols), c2 = (int)(ch[s] - (uint32_t)rr * g.cols);
     gc |= tree_children(g, rr, c2, cc) > 0;
   }
-  flags[idx] = (uint8_t)(nc | (gc << 3));
+  int level = 0, orient = 0;
+  const int L = g.levels;
+  if (!(r < g.lr[L] && c < g.lc[L])) {
+    for (int kk = L; kk >= 1; kk--)
+      if (r < g.lr[kk - 1] && c < g.lc[kk - 1]) { level = kk; break; }
+    orient = (r < g.lr[level]) ? 0 : ((c < g.lc[level]) ? 1 : 2);
+  }
+  ginfo[idx] = (uint64_t)(uint32_t)idx | bitsat((uint64_t)nc, ninfo::NCH) |
+               bitsat((uint64_t)gc, ninfo::HASGC) | bitsat((uint64_t)level, ninfo::LEVEL) |
+               bitsat((uint64_t)orient, ninfo::ORIENT) | bitsat(63, ninfo::RELC) |
+               bitsat(63, ninfo::RELD) | bitsat(63, ninfo::RELL);
 }
+
+// children of an entry (spiht.py:108-163) from its level/orientation bits
+__device__ __forceinline__ int entry_children(const Geo& g, uint64_t e, uint32_t* ch) {
+  const uint32_t node = (uint32_t)e;
+  const int r = (int)(node / (uint32_t)g.cols), c = (int)(node - (uint32_t)r * (uint32_t)g.cols);
+  const int lev = (int)((e >> ninfo::LEVEL) & 7);
+  int m = 0;
+  if (lev == 0) {
+#pragma unroll
+    for (int o = 0; o < 3; o++) {
+      Rect R = detail_rect(g, g.levels, o);
+      if (R.h > 0 && R.w > 0 && r < R.h && c < R.w)
+        ch[m++] = (uint32_t)((R.r0 + r) * g.cols + (R.c0 + c));
+    }
+    return m;
+  }
+  if (lev < 2) return 0;
+  const int o = (int)((e >> ninfo::ORIENT) & 3);
+  Rect P = detail_rect(g, lev, o), C = detail_rect(g, lev - 1, o);
+  const int i = r - P.r0, j = c - P.c0;
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++) {
+      int ci = 2 * i + a, cj = 2 * j + b;
+      if (ci < C.h && cj < C.w) ch[m++] = (uint32_t)((C.r0 + ci) * g.cols + (C.c0 + cj));
+    }
+  return m;
+}
+
+__device__ __forceinline__ int e_rel(uint64_t e, int at) { return (int)((e >> at) & 63); }
+__device__ __forceinline__ int e_nch(uint64_t e) { return (int)((e >> ninfo::NCH) & 7); }
+__device__ __forceinline__ int e_hasgc(uint64_t e) { return (int)((e >> ninfo::HASGC) & 1); }
+__device__ __forceinline__ bool e_isb(uint64_t e) { return (e >> ninfo::TYPEB) & 1; }
+__device__ __forceinline__ int e_neg(uint64_t e) { return (int)((e >> ninfo::NEG) & 1); }
 
 // host replica of the children count (for the initial LIS)
 int host_nchild(const Geo& g, int r, int c) {
@@ -130,6 +179,28 @@ __global__ void subtree_kernel(Geo g, int level, int16_t* ec, int16_t* ed, int16
   }
 }
 
+__device__ __forceinline__ uint64_t rel_of(int n_max, int e) {
+  int r = n_max - e;
+  return (uint64_t)(r < 0 ? 0 : (r > 63 ? 63 : r));
+}
+
+// per-field node info = geometry info + relative exponents + sign
+__global__ void node_info_kernel(const uint64_t* __restrict__ ginfo, MachineBufs mb, int64_t n) {
+  const int f = blockIdx.y;
+  const int n_max = mb.out[f].n_max;
+  const int64_t fo = (int64_t)f * mb.stride;
+  const uint64_t clear = ~(bitsat(63, ninfo::RELC) | bitsat(63, ninfo::RELD) | bitsat(63, ninfo::RELL));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t e = ginfo[i] & clear;
+    e |= bitsat(rel_of(n_max, mb.ec[fo + i]), ninfo::RELC);
+    e |= bitsat(rel_of(n_max, mb.ed[fo + i]), ninfo::RELD);
+    e |= bitsat(rel_of(n_max, mb.el[fo + i]), ninfo::RELL);
+    e |= bitsat((uint64_t)(mb.pinfo[fo + i] >> 7), ninfo::NEG);
+    mb.ninfo[fo + i] = e;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // block scan of packed 4 x 16-bit counters (per-tile totals stay < 65536)
 struct ScanSmem {
@@ -183,12 +254,16 @@ __device__ __forceinline__ void stage_flush(Stage& s, uint64_t seg_start, uint64
   uint64_t w0 = seg_start >> 5, w1 = (seg_start + len - 1) >> 5;
   for (uint64_t i = threadIdx.x; i <= w1 - w0; i += MT) {
     uint32_t v = s.w[i];
-    if (v) atomicOr(gw + w0 + i, v);
+    if (!v) continue;
+    // interior words belong to this segment alone: plain store
+    if (i == 0 || i == w1 - w0) atomicOr(gw + w0 + i, v);
+    else gw[w0 + i] = v;
   }
 }
 
 // ---------------------------------------------------------------------------
-// the machine
+// the machine.  Encoder: significance from the entries' relative exponents;
+// decoder: significance read from the stream at the scan-assigned offset.
 template <bool DECODE>
 __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, TreeTables tt,
                                                         int planes) {
@@ -199,17 +274,15 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   __shared__ uint64_t red_sm[NW];
 
   const int64_t fo = (int64_t)f * mb.stride;
-  const int16_t* ec = mb.ec + fo;
-  const int16_t* ed = mb.ed + fo;
-  const int16_t* el = mb.el + fo;
   uint32_t* sign_pos = mb.sign_pos + fo;
   uint32_t* lsp_rank = mb.lsp_rank + fo;
   uint8_t* pinfo = mb.pinfo + fo;
-  uint32_t* lip = mb.lip + fo;
-  uint32_t* lis_old = mb.lis0 + fo;
-  uint32_t* lis_new = mb.lis1 + fo;
-  uint32_t* wav_a = mb.w0 + fo;
-  uint32_t* wav_b = mb.w1 + fo;
+  const uint64_t* info = DECODE ? mb.ginfo : mb.ninfo + fo;
+  uint64_t* lip = mb.lip + fo;
+  uint64_t* lis_old = mb.lis0 + fo;
+  uint64_t* lis_new = mb.lis1 + fo;
+  uint64_t* wav_a = mb.w0 + fo;
+  uint64_t* wav_b = mb.w1 + fo;
   uint32_t* lsp = mb.lsp + fo;
   uint32_t* bits = mb.bits + (int64_t)f * mb.bit_stride;
   PlaneRec* prec = mb.planes + (int64_t)f * kMaxPlaneRecs;
@@ -217,10 +290,11 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   const uint64_t limit = DECODE ? mb.limit[f] : ~0ull;
   const uint64_t bit_cap = (uint64_t)mb.bit_stride * 32;
   const uint64_t cap = (uint64_t)mb.stride;
+  const uint64_t TYPEB = 1ull << ninfo::TYPEB;
 
   // initial lists (spiht.py:300-303)
-  for (int64_t i = threadIdx.x; i < tt.nroots; i += MT) lip[i] = tt.roots[i];
-  for (int64_t i = threadIdx.x; i < tt.nlis_roots; i += MT) lis_old[i] = tt.lis_roots[i];
+  for (int64_t i = threadIdx.x; i < tt.nroots; i += MT) lip[i] = info[tt.roots[i]];
+  for (int64_t i = threadIdx.x; i < tt.nlis_roots; i += MT) lis_old[i] = info[tt.lis_roots[i]];
   uint64_t nlip = tt.nroots, nlis = tt.nlis_roots, nlsp = 0, pos = 0;
   int overflow = 0;
   int p = 0;
@@ -228,15 +302,14 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
 
   for (; p < planes; p++) {
     if (DECODE && pos >= limit) break;  // `while not src.depleted`
-    const int n = n_max - p;
     const uint64_t refine_len = nlsp;
     if (threadIdx.x == 0) prec[p].start = (uint32_t)pos;
 
-    // ---------------- LIP pass -------------------------------------------
+    // ---------------- LIP pass: a streaming stable partition -------------
     {
       uint64_t K = 0;  // newly significant so far
       for (uint64_t base = 0; base < nlip; base += TILE) {
-        uint32_t node[MI];
+        uint64_t ent[MI];
         int sig[MI];
         int cnt_sig = 0;
         const uint64_t i0 = base + (uint64_t)threadIdx.x * MI;
@@ -244,10 +317,10 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
         for (int k = 0; k < MI; k++) {
           uint64_t i = i0 + k;
           sig[k] = 0;
-          node[k] = 0;
+          ent[k] = 0;
           if (i < nlip) {
-            node[k] = lip[i];
-            sig[k] = DECODE ? read_bit(bits, pos + i, limit) : (ec[node[k]] >= n);
+            ent[k] = lip[i];
+            sig[k] = DECODE ? read_bit(bits, pos + i, limit) : (e_rel(ent[k], ninfo::RELC) <= p);
             cnt_sig += sig[k];
           }
         }
@@ -264,7 +337,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
           for (int k = 0; k < MI; k++) {
             if (!sig[k]) continue;
             stage_set(st_a, sig_seg, pos + i0 + k);
-            if (pinfo[node[k]] & 0x80) stage_set(st_b, sgn_seg, sgn_seg + r);
+            if (e_neg(ent[k])) stage_set(st_b, sgn_seg, sgn_seg + r);
             r++;
           }
           __syncthreads();
@@ -273,7 +346,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
         }
         // newly significant -> LSP, metadata; survivors compacted in place
         uint32_t r = (uint32_t)ex;
-        uint64_t keep_before = (i0 - base) - ex;  // kept entries before mine in this tile
+        uint64_t keep_before = (i0 - base) - ex;
         __syncthreads();  // all reads of lip[] in this tile done before compaction writes
 #pragma unroll
         for (int k = 0; k < MI; k++) {
@@ -282,7 +355,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
           if (sig[k]) {
             uint64_t rank = nlsp + K + r;
             uint64_t sp = pos + nlip + K + r;
-            uint32_t c = node[k];
+            uint32_t c = (uint32_t)ent[k];
             lsp[rank] = c;
             lsp_rank[c] = (uint32_t)rank;
             if (DECODE) {
@@ -294,11 +367,11 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
               }
             } else {
               sign_pos[c] = (uint32_t)sp;
-              pinfo[c] = (uint8_t)((pinfo[c] & 0x80) | p);
+              pinfo[c] = (uint8_t)((e_neg(ent[k]) << 7) | p);
             }
             r++;
           } else {
-            lip[base - K + keep_before] = node[k];
+            lip[base - K + keep_before] = ent[k];
             keep_before++;
           }
         }
@@ -313,8 +386,8 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
     // ---------------- LIS waves ------------------------------------------
     {
       uint64_t nkeep = 0;
-      const uint32_t* src = lis_old;
-      uint32_t* dst = wav_a;
+      const uint64_t* src = lis_old;
+      uint64_t* dst = wav_a;
       uint64_t cnt = nlis;
       while (cnt) {
         // prepass: total children bits of significant type-A entries
@@ -326,19 +399,18 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
           for (int k = 0; k < MI; k++) {
             uint64_t i = i0 + k;
             if (i >= cnt) break;
-            uint32_t e = src[i];
-            if (e & TYPE_B) continue;
-            uint32_t nd_ = e;
-            int s = DECODE ? read_bit(bits, pos + i, limit) : (ed[nd_] >= n);
-            if (s) local += tt.flags[nd_] & 7;
+            uint64_t e = src[i];
+            if (e_isb(e)) continue;
+            int s = DECODE ? read_bit(bits, pos + i, limit) : (e_rel(e, ninfo::RELD) <= p);
+            if (s) local += e_nch(e);
           }
           for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
           if ((threadIdx.x & 31) == 0) red_sm[threadIdx.x >> 5] = local;
           __syncthreads();
-          if (threadIdx.x == 0) {
-            uint64_t s = 0;
-            for (int w = 0; w < NW; w++) s += red_sm[w];
-            red_sm[0] = s;
+          if (threadIdx.x < 32) {
+            uint64_t s = threadIdx.x < NW ? red_sm[threadIdx.x] : 0;
+            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (threadIdx.x == 0) red_sm[0] = s;
           }
           __syncthreads();
           TC += red_sm[0];
@@ -348,7 +420,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
         const uint64_t sg_seg0 = pos + cnt + TC;  // their sign bits
         uint64_t ch_off = 0, sig_off = 0, nxt_off = 0;
         for (uint64_t base = 0; base < cnt; base += TILE) {
-          uint32_t ent[MI];
+          uint64_t ent[MI];
           int sig[MI], nch[MI], nxt[MI];
           uint32_t keep = 0, nchs = 0, nxts = 0;
           const uint64_t i0 = base + (uint64_t)threadIdx.x * MI;
@@ -357,32 +429,42 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
             uint64_t i = i0 + k;
             sig[k] = 0; nch[k] = 0; nxt[k] = 0; ent[k] = 0;
             if (i >= cnt) continue;
-            uint32_t e = src[i];
+            uint64_t e = src[i];
             ent[k] = e;
-            uint32_t nd_ = e & ~TYPE_B;
-            bool isb = e & TYPE_B;
-            sig[k] = DECODE ? read_bit(bits, pos + i, limit) : ((isb ? el[nd_] : ed[nd_]) >= n);
+            bool isb = e_isb(e);
+            sig[k] = DECODE ? read_bit(bits, pos + i, limit)
+                            : (e_rel(e, isb ? ninfo::RELL : ninfo::RELD) <= p);
             if (!sig[k]) { keep++; continue; }
-            uint8_t fl = tt.flags[nd_];
             if (!isb) {
-              nch[k] = fl & 7;
-              nxt[k] = (fl >> 3) & 1;
+              nch[k] = e_nch(e);
+              nxt[k] = e_hasgc(e);
             } else {
-              uint32_t ch[4];
-              int r = (int)(nd_ / g.cols), c = (int)(nd_ - (uint32_t)r * g.cols);
-              int m = tree_children(g, r, c, ch);
-              int q = 0;
-              for (int s = 0; s < m; s++) q += (tt.flags[ch[s]] & 7) != 0;
-              nxt[k] = q;
+              nxt[k] = -1;  // resolved below from the children's info
             }
             nchs += nch[k];
-            nxts += nxt[k];
           }
+          // children of significant entries (A: coded; B: next-wave sets)
+          uint32_t chn[MI][4];
+          uint64_t cin[MI][4];
+#pragma unroll
+          for (int k = 0; k < MI; k++) {
+            if (!sig[k] || (!nch[k] && nxt[k] >= 0)) continue;
+            int m = entry_children(g, ent[k], chn[k]);
+            for (int s = 0; s < m; s++) cin[k][s] = info[chn[k][s]];
+            if (nxt[k] < 0) {
+              int q = 0;
+              for (int s = 0; s < m; s++) q += e_nch(cin[k][s]) != 0;
+              nxt[k] = q;
+              nch[k] = 0;
+              chn[k][0] = (uint32_t)m;  // remember the child count for the next-wave copy
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < MI; k++) nxts += nxt[k] > 0 ? nxt[k] : 0;
           uint64_t tot1;
           uint64_t ex1 = block_exclusive_scan((uint64_t)keep | ((uint64_t)nchs << 16) |
                                                   ((uint64_t)nxts << 32), tot1, ssm);
           // children significance
-          uint32_t chn[MI][4];
           uint8_t chs[MI];  // bitmask of significant children
           uint32_t nsig = 0;
           {
@@ -390,12 +472,8 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
 #pragma unroll
             for (int k = 0; k < MI; k++) {
               chs[k] = 0;
-              if (!nch[k]) continue;
-              uint32_t nd_ = ent[k];
-              int r = (int)(nd_ / g.cols), c = (int)(nd_ - (uint32_t)r * g.cols);
-              tree_children(g, r, c, chn[k]);
               for (int s = 0; s < nch[k]; s++) {
-                int cs = DECODE ? read_bit(bits, cpos, limit) : (ec[chn[k][s]] >= n);
+                int cs = DECODE ? read_bit(bits, cpos, limit) : (e_rel(cin[k][s], ninfo::RELC) <= p);
                 chs[k] |= (uint8_t)(cs << s);
                 nsig += cs;
                 cpos++;
@@ -420,7 +498,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
               for (int s = 0; s < nch[k]; s++) {
                 if ((chs[k] >> s) & 1) {
                   stage_set(st_b, seg_b, cpos);
-                  if (pinfo[chn[k][s]] & 0x80) stage_set(st_c, seg_c, spos);
+                  if (e_neg(cin[k][s])) stage_set(st_c, seg_c, spos);
                   spos++;
                 }
                 cpos++;
@@ -441,8 +519,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
             for (int k = 0; k < MI; k++) {
               uint64_t i = i0 + k;
               if (i >= cnt) break;
-              uint32_t e = ent[k];
-              uint32_t nd_ = e & ~TYPE_B;
+              uint64_t e = ent[k];
               if (!sig[k]) {
                 if (kp < cap) lis_new[kp] = e; else overflow = 1;
                 kp++;
@@ -464,26 +541,24 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
                     }
                   } else {
                     sign_pos[c] = (uint32_t)sp;
-                    pinfo[c] = (uint8_t)((pinfo[c] & 0x80) | p);
+                    pinfo[c] = (uint8_t)((e_neg(cin[k][s]) << 7) | p);
                   }
                   sg++;
                 } else {
                   uint64_t li = nlip + ins;
-                  if (li < cap) lip[li] = c; else overflow = 1;
+                  if (li < cap) lip[li] = cin[k][s]; else overflow = 1;
                   ins++;
                 }
               }
-              if (nxt[k]) {
-                if (!(e & TYPE_B)) {
-                  if (nx < cap) dst[nx] = nd_ | TYPE_B; else overflow = 1;
+              if (nxt[k] > 0) {
+                if (!e_isb(e)) {
+                  if (nx < cap) dst[nx] = e | TYPEB; else overflow = 1;
                   nx++;
                 } else {
-                  uint32_t ch[4];
-                  int r = (int)(nd_ / g.cols), c = (int)(nd_ - (uint32_t)r * g.cols);
-                  int m = tree_children(g, r, c, ch);
+                  int m = (int)chn[k][0];
                   for (int s = 0; s < m; s++)
-                    if (tt.flags[ch[s]] & 7) {
-                      if (nx < cap) dst[nx] = ch[s]; else overflow = 1;
+                    if (e_nch(cin[k][s])) {
+                      if (nx < cap) dst[nx] = cin[k][s]; else overflow = 1;
                       nx++;
                     }
                 }
@@ -505,7 +580,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
         __syncthreads();
       }
       nlis = nkeep;
-      uint32_t* t = lis_old; lis_old = lis_new; lis_new = t;
+      uint64_t* t = lis_old; lis_old = lis_new; lis_new = t;
     }
 
     // ---------------- refinement (positions only) ------------------------
@@ -528,7 +603,6 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   }
 }
 
-// ---------------------------------------------------------------------------
 // encoder refinement: warp per 32 consecutive LSP ranks, ballot per plane.
 // Refinement bit of plane p for rank i sits at refine_start[p] + i, for every
 // plane p after the coefficient's significance plane (i < refine_len[p]).
@@ -613,8 +687,8 @@ __global__ void decode_init_kernel(MachineBufs mb) {
 
 // ---------------------------------------------------------------------------
 void build_tree_tables(const Geo& g, TreeTables& t, cudaStream_t st) {
-  cudaMalloc(&t.flags, g.n);
-  tree_flags_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, st>>>(g, t.flags);
+  cudaMalloc(&t.ginfo, sizeof(uint64_t) * g.n);
+  tree_info_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, st>>>(g, t.ginfo);
   // roots: LL row-major, then orphans per level L-1..1 and orientation (spiht.py:164-178)
   std::vector<uint32_t> roots, lis;
   int llr = g.lr[g.levels], llc = g.lc[g.levels];
@@ -643,7 +717,7 @@ void build_tree_tables(const Geo& g, TreeTables& t, cudaStream_t st) {
 }
 
 void free_tree_tables(TreeTables& t) {
-  cudaFree(t.flags); cudaFree(t.roots); cudaFree(t.lis_roots);
+  cudaFree(t.ginfo); cudaFree(t.roots); cudaFree(t.lis_roots);
   t = TreeTables{};
 }
 
@@ -656,7 +730,7 @@ void coef_prepare(const double* coef, int64_t field_stride, MachineBufs& mb, con
                                             mb.sign_pos, mb.pinfo, mb.stride, mb.out);
 }
 
-void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables&, cudaStream_t st) {
+void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables& tt, cudaStream_t st) {
   for (int k = 2; k <= g.levels; k++) {
     int64_t cnt = (int64_t)g.lr[k - 1] * g.lc[k - 1];
     int blocks = (int)((cnt + 255) / 256);
@@ -668,6 +742,8 @@ void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables&, cudaStr
   int blocks = (int)((cnt + 255) / 256);
   subtree_kernel<<<dim3(blocks, mb.nfields), 256, 0, st>>>(g, 0, mb.ec, mb.ed, mb.el, mb.stride,
                                                            mb.nfields);
+  node_info_kernel<<<dim3((unsigned)std::min<int64_t>((g.n + 255) / 256, 2048), mb.nfields), 256, 0,
+                     st>>>(tt.ginfo, mb, g.n);
 }
 
 void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& tt, int planes,

@@ -24,6 +24,22 @@ struct MachineOut {
   uint32_t pad[3];
 };
 
+// List entries are 64-bit "node info" words carrying everything the machine
+// needs about a node, so list passes stream instead of gathering:
+//   bits  0..31 node (flat index)
+//   bits 32..37 relc = clamp(n_max - floor(log2|c|), 0, 63)   (63: never)
+//   bits 38..43 reld  (same, for the max over all descendants)
+//   bits 44..49 rell  (same, for the max over grandchildren and below)
+//   bit  50     coefficient is negative
+//   bits 51..53 number of children; bit 54 has grandchildren
+//   bit  55     LIS entry of type B
+//   bits 56..58 band level (0 = LL, 1..5 detail); bits 59..60 orientation
+// "significant at plane index p" is simply rel <= p.
+namespace ninfo {
+constexpr int RELC = 32, RELD = 38, RELL = 44, NEG = 50, NCH = 51, HASGC = 54, TYPEB = 55,
+              LEVEL = 56, ORIENT = 59;
+}
+
 // Batched buffers, all fields `stride` elements apart (bits: bit_stride words).
 struct MachineBufs {
   int nfields;
@@ -32,8 +48,10 @@ struct MachineBufs {
   // per coefficient
   int16_t* ec; int16_t* ed; int16_t* el;
   uint32_t* mant; uint32_t* sign_pos; uint32_t* lsp_rank; uint8_t* pinfo;
+  uint64_t* ninfo;           // per-field node info (encode)
+  const uint64_t* ginfo;     // geometry-only node info (decode; shared by all fields)
   // lists (capacity `stride` each)
-  uint32_t* lip; uint32_t* lis0; uint32_t* lis1; uint32_t* w0; uint32_t* w1; uint32_t* lsp;
+  uint64_t* lip; uint64_t* lis0; uint64_t* lis1; uint64_t* w0; uint64_t* w1; uint32_t* lsp;
   // stream bits
   uint32_t* bits;
   PlaneRec* planes;          // [nfields][kMaxPlaneRecs]
@@ -44,7 +62,7 @@ struct MachineBufs {
 
 // geometry-wide tables (shared by every field of a batch)
 struct TreeTables {
-  uint8_t* flags;        // nchild | has_grandchild << 3
+  uint64_t* ginfo;       // geometry node info (nchild, has_gc, level, orientation)
   uint32_t* roots;       // LIP initial order
   uint32_t* lis_roots;   // roots with children (initial LIS, type A)
   int64_t nroots, nlis_roots;
@@ -56,7 +74,7 @@ void free_tree_tables(TreeTables& t);
 // coefficient exponents / mantissas / signs + per-field n_max
 void coef_prepare(const double* coef, int64_t field_stride, MachineBufs& mb, const Geo& g,
                   cudaStream_t st);
-// e_d / e_l bottom-up
+// e_d / e_l bottom-up, then the per-field node info words
 void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables& tt, cudaStream_t st);
 // the list machine (one CTA per field)
 void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& tt, int planes,
