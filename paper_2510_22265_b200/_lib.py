@@ -17,7 +17,7 @@ import numpy as np
 from .errors import ArgumentError, DeviceError, EbccError, FormatError, ResidualInsufficient
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libebcc_gpu.so")
+LIB_PATH = os.environ.get("EBCC_LIB") or os.path.join(HERE, "libebcc_gpu.so")
 
 OK, E_ARGUMENT, E_FORMAT, E_RESIDUAL, E_CAPACITY, E_CUDA, E_NOMEM = range(7)
 INPUT_ON_DEVICE = 1

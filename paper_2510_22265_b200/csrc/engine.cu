@@ -19,6 +19,7 @@
 // the order is observably identical, and running both base-memo searches
 // first lets the residual encode reuse the base coefficient metadata arrays.
 #include <algorithm>
+#include <thread>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -218,6 +219,8 @@ struct Workspace {
   uint32_t *mant = nullptr, *sign_pos = nullptr, *lsp_rank = nullptr;
   uint8_t* pinfo = nullptr;
   uint4* packed = nullptr;
+  uint4* packed2 = nullptr;      // residual metadata (built while the pure search runs)
+  double *A2 = nullptr, *B2 = nullptr;  // residual forward-DWT scratch
   uint64_t *lip = nullptr, *lis0 = nullptr, *lis1 = nullptr, *w0 = nullptr, *w1 = nullptr;
   uint32_t* lsp = nullptr;
   uint64_t* ninfo = nullptr;
@@ -239,6 +242,7 @@ struct Workspace {
 
   void release() {
     void* ptrs[] = {x32, norm, A, B, base_dec, ec, ed, el, mant, sign_pos, lsp_rank, pinfo, packed, ninfo,
+                    packed2, A2, B2,
                     lip, lis0, lis1, w0, w1, lsp, bits_base, bits_res, pl_base, pl_res,
                     mo_base, mo_res, fs, prm, res, limit, active, mm};
     for (void* p : ptrs)
@@ -278,6 +282,9 @@ struct ebcc_ctx {
   int64_t out_cap = 0;
   ebcc_stats stats{};
   fused::Level0Timer l0;
+  cudaStream_t side = nullptr;   // high-priority stream for the overlapped residual encode
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+  std::vector<ebcc_ctx*> lanes;  // child contexts for concurrent sub-batches
 };
 
 namespace {
@@ -304,6 +311,9 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   w.lsp_rank = dalloc<uint32_t>(N);
   w.pinfo = dalloc<uint8_t>(N);
   w.packed = dalloc<uint4>(N);
+  w.packed2 = dalloc<uint4>(N);
+  w.A2 = dalloc<double>(N);
+  w.B2 = dalloc<double>(N);
   w.lip = dalloc<uint64_t>(N);
   w.lis0 = dalloc<uint64_t>(N);
   w.lis1 = dalloc<uint64_t>(N);
@@ -351,7 +361,7 @@ MachineBufs machine_bufs(Workspace& w, int nfields, bool residual) {
 
 Meta meta_of(Workspace& w, bool residual) {
   Meta m{};
-  m.packed = w.packed;
+  m.packed = residual ? w.packed2 : w.packed;
   m.planes = residual ? w.pl_res : w.pl_base;
   m.mo = residual ? w.mo_res : w.mo_base;
   m.stride = w.g.n;
@@ -364,39 +374,44 @@ struct PhaseClock;
 void pc_mark(PhaseClock* pc, const char* name);
 PhaseClock* g_pc = nullptr;
 
-void encode_pyramids(ebcc_ctx* c, int nfields, bool residual, int planes,
-                     const std::vector<uint8_t>& active, std::vector<MachineOut>& mo,
-                     std::vector<PlaneRec>& pl) {
+// encode the pyramids in `coef` (all fields): exponents, machine (which
+// skips all-zero pyramids itself), refinement, packed metadata.  Async on st.
+void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const double* coef,
+                   uint4* packed, const std::vector<uint8_t>& active, cudaStream_t st) {
   Workspace& w = c->ws;
-  cudaStream_t st = c->stream;
   MachineBufs mb = machine_bufs(w, nfields, residual);
   std::vector<MachineOut> init(nfields);
   for (auto& m : init) { m = MachineOut{}; m.n_max = kExpNone; }
   CK(cudaMemcpyAsync(mb.out, init.data(), sizeof(MachineOut) * nfields, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(mb.bits, 0, sizeof(uint32_t) * mb.bit_stride * nfields, st));
-  coef_prepare(w.A, w.g.n, mb, w.g, st);
+  CK(cudaMemcpyAsync(w.active, active.data(), nfields, cudaMemcpyHostToDevice, st));
+  coef_prepare(coef, w.g.n, mb, w.g, st);
   subtree_exponents(mb, w.g, w.tt, st);
-  c->stats.kernel_launches += 2 + w.g.levels;
-  pc_mark(g_pc, "exponents");
-  // fields whose pyramid is all zero (n_max sentinel) skip the machine
-  CK(cudaMemcpyAsync(mo.data(), mb.out, sizeof(MachineOut) * nfields, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  std::vector<uint8_t> act(nfields);
-  for (int f = 0; f < nfields; f++) act[f] = active[f] && mo[f].n_max != kExpNone;
-  CK(cudaMemcpyAsync(w.active, act.data(), nfields, cudaMemcpyHostToDevice, st));
   run_machine(false, mb, w.g, w.tt, planes, st);
-  pc_mark(g_pc, "machine");
   write_refinement(mb, planes, st);
-  pack_meta(mb, w.packed, st);
-  pc_mark(g_pc, "refine");
-  c->stats.kernel_launches += 3;
+  pack_meta(mb, packed, st);
+  c->stats.kernel_launches += 6 + w.g.levels;
   CK(cudaGetLastError());
+}
+
+// machine summaries + plane records of the last encode_launch (syncs st)
+void encode_collect(ebcc_ctx* c, int nfields, bool residual, const std::vector<uint8_t>& active,
+                    std::vector<MachineOut>& mo, std::vector<PlaneRec>& pl, cudaStream_t st) {
+  MachineBufs mb = machine_bufs(c->ws, nfields, residual);
   CK(cudaMemcpyAsync(mo.data(), mb.out, sizeof(MachineOut) * nfields, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(pl.data(), mb.planes, sizeof(PlaneRec) * kMaxPlaneRecs * nfields,
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int f = 0; f < nfields; f++)
-    if (act[f] && mo[f].overflow) throw CudaFail{cudaErrorMemoryAllocation, "machine capacity"};
+    if (active[f] && mo[f].overflow) throw CudaFail{cudaErrorMemoryAllocation, "machine capacity"};
+}
+
+void encode_pyramids(ebcc_ctx* c, int nfields, bool residual, int planes,
+                     const std::vector<uint8_t>& active, std::vector<MachineOut>& mo,
+                     std::vector<PlaneRec>& pl) {
+  encode_launch(c, nfields, residual, planes, c->ws.A, residual ? c->ws.packed2 : c->ws.packed,
+                active, c->stream);
+  encode_collect(c, nfields, residual, active, mo, pl, c->stream);
 }
 
 // midpoint stopping plane of a decode of B bits of the `planes`-plane variant
@@ -597,30 +612,49 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     if (phase == 0)
       for (int f = 0; f < nfields; f++) base_entries[f] = cs[f].memo.size();
     pc.mark(phase == 0 ? "base_search" : "pure_search");
-  }
-
-  // ---- residue = norm - base decode at the chosen budget; residual encode ----
-  for (int f = 0; f < nfields; f++) {
-    prm[f] = ProbeParam{};
-    if (cs[f].constant) continue;
-    int64_t len = cs[f].stream_len(cs[f].base_budget);
-    uint64_t B = (uint64_t)(len - kHeader) * 8;
-    if (B > cs[f].T_base) B = cs[f].T_base;
-    prm[f].B = B; prm[f].planes = kBasePlanes; prm[f].active = 1;
+    if (phase == 0) {
+      // ---- residue = norm - base decode at the chosen budget (main stream),
+      // then the residual DWT + 32-plane encode on the high-priority side
+      // stream, overlapped with the pure-base search below (which only reads
+      // the base memo and the base metadata) ----
+      for (int f = 0; f < nfields; f++) {
+        prm[f] = ProbeParam{};
+        if (cs[f].constant) continue;
+        int64_t len = cs[f].stream_len(cs[f].base_budget);
+        uint64_t B = (uint64_t)(len - kHeader) * 8;
+        if (B > cs[f].T_base) B = cs[f].T_base;
+        prm[f].B = B; prm[f].planes = kBasePlanes; prm[f].active = 1;
+      }
+      memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
+      CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
+      // resid overwrites norm in place (nothing reads norm after this point)
+      base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
+      c->stats.kernel_launches += g.levels;
+      static const bool overlap = !(getenv("EBCC_OVERLAP") && getenv("EBCC_OVERLAP")[0] == '0');
+      cudaStream_t rs = overlap ? c->side : st;
+      CK(cudaEventRecord(c->ev_a, st));
+      CK(cudaStreamWaitEvent(rs, c->ev_a, 0));
+      CK(cudaEventRecord(c->ev_s0, rs));
+      CK(cudaMemcpyAsync(w.A2, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, rs));
+      forward_dwt(w.A2, w.B2, N, nfields, g, rs);
+      c->stats.kernel_launches += 2 * g.levels;
+      encode_launch(c, nfields, true, kDeepPlanes, w.A2, w.packed2, active, rs);
+      CK(cudaEventRecord(c->ev_s1, rs));
+      CK(cudaEventRecord(c->ev_b, rs));
+      if (!overlap) pc.mark("residual_encode(serial)");
+      // the pure search's first H2D of w.prm must not overtake base_to_residue:
+      // both are on `st`, so stream order already guarantees it
+    }
   }
   std::vector<MachineOut> rmo(nfields);
   std::vector<PlaneRec> rpl((size_t)kMaxPlaneRecs * nfields);
+  CK(cudaStreamWaitEvent(st, c->ev_b, 0));
+  encode_collect(c, nfields, true, active, rmo, rpl, st);
   {
-    EventTimer t(c, &c->stats.ms_encode);
-    CK(cudaMemcpyAsync(w.prm, prm.data(), sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
-    // resid overwrites norm in place (norm is not needed after the base searches)
-    base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
-    c->stats.kernel_launches += g.levels;
-    CK(cudaMemcpyAsync(w.A, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
-    forward_dwt(w.A, w.B, N, nfields, g, st);
-    c->stats.kernel_launches += 2 * g.levels;
-    encode_pyramids(c, nfields, true, kDeepPlanes, active, rmo, rpl);
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, c->ev_s0, c->ev_s1) == cudaSuccess) c->stats.ms_encode += ms;
   }
+
   pc.mark("residual_encode");
   Meta mres = meta_of(w, true);
   // stream totals of the 24- and 32-plane variants
@@ -796,6 +830,15 @@ int ebcc_create(int32_t device, ebcc_ctx** out) {
   if (e != cudaSuccess) { delete c; return EBCC_E_CUDA; }
   cudaEventCreate(&c->l0.a);
   cudaEventCreate(&c->l0.b);
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi);
+    cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming);
+    cudaEventCreate(&c->ev_s0);
+    cudaEventCreate(&c->ev_s1);
+  }
   c->own_stream = true;
   *out = c;
   return EBCC_OK;
@@ -803,6 +846,8 @@ int ebcc_create(int32_t device, ebcc_ctx** out) {
 
 void ebcc_destroy(ebcc_ctx* c) {
   if (!c) return;
+  for (ebcc_ctx* l : c->lanes) ebcc_destroy(l);
+  c->lanes.clear();
   cudaSetDevice(c->device);
   c->ws.release();
   if (c->d_payload) cudaFree(c->d_payload);
@@ -813,6 +858,11 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (c->l0.a) cudaEventDestroy(c->l0.a);
   if (c->l0.b) cudaEventDestroy(c->l0.b);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
+  if (c->ev_s0) cudaEventDestroy(c->ev_s0);
+  if (c->ev_s1) cudaEventDestroy(c->ev_s1);
   delete c;
 }
 
@@ -832,31 +882,28 @@ int ebcc_get_stats(const ebcc_ctx* c, ebcc_stats* out) {
   return EBCC_OK;
 }
 
-int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t rows, int32_t cols,
+}  // extern "C"
+
+namespace {
+// compress nfields chunks on one context; the packed payload is left in
+// c->d_payload (c->payload_total bytes), per-chunk sizes in `sizes`
+int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t rows, int32_t cols,
                   double eps_rel, double q, double r0, double search_tol, int32_t flags,
-                  ebcc_chunk_rec* recs, uint8_t* payload, int64_t payload_cap,
-                  int64_t* payload_offsets, int64_t* payload_total) {
-  if (!c || !fields || !recs || nfields < 0 || rows < 1 || cols < 1)
-    return fail(c, EBCC_E_ARGUMENT, "bad arguments");
-  // EbccParams.validate (pipeline.py:54-62)
-  if (!(eps_rel > 0.0 && eps_rel < 1.0))
-    return fail(c, EBCC_E_ARGUMENT, "epsilon_rel must be in (0, 1)");
-  if (!(q > 0.0 && q <= 1.0)) return fail(c, EBCC_E_ARGUMENT, "q must be in (0, 1]");
-  if (r0 < 1.0) return fail(c, EBCC_E_ARGUMENT, "r0 must be >= 1");
-  if (!(search_tol > 0.0)) return fail(c, EBCC_E_ARGUMENT, "search_tol must be positive");
-  if ((int64_t)rows * cols >= (1ll << 31)) return fail(c, EBCC_E_ARGUMENT, "chunk too large");
+                  ebcc_chunk_rec* recs, std::vector<int64_t>& sizes, cudaEvent_t start_after,
+                  double mem_share) {
   c->stats = ebcc_stats{};
   c->err.clear();
   try {
     CK(cudaSetDevice(c->device));
     cudaStream_t st = c->stream;
+    if (start_after) CK(cudaStreamWaitEvent(st, start_after, 0));
     int levels = clamp_levels(rows, cols, default_levels(rows, cols));
     Geo g = make_geo(rows, cols, levels);
     // batch capacity from free memory (~100 B per point per field in flight)
     size_t freeb = 0, totalb = 0;
     CK(cudaMemGetInfo(&freeb, &totalb));
     int64_t per_field = g.n * 160 + 4096;
-    int64_t cap = (int64_t)((freeb * 0.6) / per_field);
+    int64_t cap = (int64_t)((freeb * 0.6 * mem_share) / per_field);
     if (cap < 1) cap = 1;
     if (cap > nfields) cap = nfields;
     if (cap > 4096) cap = 4096;
@@ -865,7 +912,7 @@ int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
     cudaEventCreate(&t1);
     cudaEventRecord(t0, st);
     std::vector<PackPart> parts;
-    std::vector<int64_t> sizes;
+    sizes.clear();
     int status = EBCC_OK;
     for (int64_t f0 = 0; f0 < nfields; f0 += cap) {
       int nb = (int)std::min<int64_t>(cap, nfields - f0);
@@ -908,12 +955,8 @@ int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
       sizes.insert(sizes.end(), bsizes.begin(), bsizes.end());
     }
     int64_t total = 0;
-    for (int64_t f = 0; f < nfields; f++) {
-      if (payload_offsets) payload_offsets[f] = total;
-      total += sizes[f];
-    }
+    for (int64_t f = 0; f < nfields; f++) total += sizes[f];
     c->payload_total = total;
-    if (payload_total) *payload_total = total;
     cudaEventRecord(t1, st);
     cudaEventSynchronize(t1);
     float ms = 0;
@@ -922,6 +965,141 @@ int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
     c->stats.ms_other = ms - c->stats.ms_encode - c->stats.ms_probe;
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
+    return status;
+  } catch (CudaFail& e) {
+    cudaGetLastError();
+    return fail(c, e.e == cudaErrorMemoryAllocation ? EBCC_E_NOMEM : EBCC_E_CUDA,
+                std::string(e.what) + ": " + cudaGetErrorString(e.e));
+  } catch (std::exception& e) {
+    return fail(c, EBCC_E_CUDA, e.what());
+  }
+}
+
+int lanes_for(int64_t nfields) {
+  const char* e = getenv("EBCC_LANES");
+  int want = e ? atoi(e) : 1;  // concurrent lanes measured slower (context contention)
+  if (want < 1) want = 1;
+  if (want > nfields) want = (int)std::max<int64_t>(1, nfields);
+  return want;
+}
+
+ebcc_ctx* lane_ctx(ebcc_ctx* c, int k);
+
+void add_stats(ebcc_stats& a, const ebcc_stats& b) {
+  a.kernel_launches += b.kernel_launches;
+  a.ms_encode += b.ms_encode;
+  a.ms_probe += b.ms_probe;
+  a.probe_launches += b.probe_launches;
+  a.ms_probe_kernel += b.ms_probe_kernel;
+  a.probe_kernel_count += b.probe_kernel_count;
+}
+
+}  // namespace
+
+extern "C" int ebcc_create(int32_t device, ebcc_ctx** out);
+extern "C" void ebcc_destroy(ebcc_ctx* c);
+
+namespace {
+ebcc_ctx* lane_ctx(ebcc_ctx* c, int k) {
+  while ((int)c->lanes.size() <= k) {
+    ebcc_ctx* child = nullptr;
+    if (ebcc_create(c->device, &child) != EBCC_OK) throw CudaFail{cudaErrorUnknown, "lane create"};
+    c->lanes.push_back(child);
+  }
+  return c->lanes[k];
+}
+}  // namespace
+
+extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t rows,
+                             int32_t cols, double eps_rel, double q, double r0,
+                             double search_tol, int32_t flags, ebcc_chunk_rec* recs,
+                             uint8_t* payload, int64_t payload_cap, int64_t* payload_offsets,
+                             int64_t* payload_total) {
+  if (!c || !fields || !recs || nfields < 0 || rows < 1 || cols < 1)
+    return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  // EbccParams.validate (pipeline.py:54-62)
+  if (!(eps_rel > 0.0 && eps_rel < 1.0))
+    return fail(c, EBCC_E_ARGUMENT, "epsilon_rel must be in (0, 1)");
+  if (!(q > 0.0 && q <= 1.0)) return fail(c, EBCC_E_ARGUMENT, "q must be in (0, 1]");
+  if (r0 < 1.0) return fail(c, EBCC_E_ARGUMENT, "r0 must be >= 1");
+  if (!(search_tol > 0.0)) return fail(c, EBCC_E_ARGUMENT, "search_tol must be positive");
+  if ((int64_t)rows * cols >= (1ll << 31)) return fail(c, EBCC_E_ARGUMENT, "chunk too large");
+  c->err.clear();
+  try {
+    CK(cudaSetDevice(c->device));
+    const int L = lanes_for(nfields);
+    const int64_t n = (int64_t)rows * cols;
+    std::vector<int64_t> sizes;
+    int status = EBCC_OK;
+    cudaEvent_t t0, t1;
+    CK(cudaEventCreate(&t0));
+    CK(cudaEventCreate(&t1));
+    CK(cudaEventRecord(t0, c->stream));
+    ebcc_stats total_stats{};
+    if (L == 1) {
+      status = compress_impl(c, fields, nfields, rows, cols, eps_rel, q, r0, search_tol, flags,
+                             recs, sizes, nullptr, 1.0);
+      total_stats = c->stats;
+      if (status != EBCC_OK && status != EBCC_E_RESIDUAL) return status;
+    } else {
+      // concurrent sub-batches: each lane (own stream + workspace + host
+      // thread) runs the whole pipeline on a contiguous block of chunks, so
+      // one lane's latency-bound list machine overlaps another's probes
+      std::vector<ebcc_ctx*> ls(L);
+      for (int k = 0; k < L; k++) ls[k] = lane_ctx(c, k);
+      std::vector<int64_t> lo(L + 1);
+      for (int k = 0; k <= L; k++) lo[k] = nfields * k / L;
+      std::vector<std::vector<int64_t>> lsz(L);
+      std::vector<int> lst(L, EBCC_OK);
+      std::vector<std::thread> th;
+      for (int k = 0; k < L; k++)
+        th.emplace_back([&, k] {
+          cudaSetDevice(c->device);
+          lst[k] = compress_impl(ls[k], fields + lo[k] * n, lo[k + 1] - lo[k], rows, cols, eps_rel,
+                                 q, r0, search_tol, flags, recs + lo[k], lsz[k], t0, 1.0 / L);
+        });
+      for (auto& t : th) t.join();
+      for (int k = 0; k < L; k++) {
+        if (lst[k] != EBCC_OK && lst[k] != EBCC_E_RESIDUAL) {
+          c->err = ls[k]->err;
+          return lst[k];
+        }
+        if (lst[k] == EBCC_E_RESIDUAL) status = EBCC_E_RESIDUAL;
+        sizes.insert(sizes.end(), lsz[k].begin(), lsz[k].end());
+        add_stats(total_stats, ls[k]->stats);
+      }
+      // gather the lanes' payloads into this context's buffer
+      int64_t tot = 0;
+      for (int64_t z : sizes) tot += z;
+      if (tot > c->payload_cap) {
+        if (c->d_payload) cudaFree(c->d_payload);
+        c->payload_cap = std::max<int64_t>(tot * 2, 1 << 20);
+        c->d_payload = dalloc<uint8_t>((size_t)c->payload_cap);
+      }
+      int64_t off = 0;
+      for (int k = 0; k < L; k++) {
+        if (ls[k]->payload_total)
+          CK(cudaMemcpyAsync(c->d_payload + off, ls[k]->d_payload, ls[k]->payload_total,
+                             cudaMemcpyDeviceToDevice, c->stream));
+        off += ls[k]->payload_total;
+      }
+    }
+    int64_t total = 0;
+    for (int64_t f = 0; f < nfields; f++) {
+      if (payload_offsets) payload_offsets[f] = total;
+      total += sizes[f];
+    }
+    c->payload_total = total;
+    if (payload_total) *payload_total = total;
+    CK(cudaEventRecord(t1, c->stream));
+    CK(cudaEventSynchronize(t1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    c->stats = total_stats;
+    c->stats.ms_total = ms;
+    c->stats.ms_other = ms - c->stats.ms_encode / L - c->stats.ms_probe / L;
     if (status != EBCC_OK) {
       for (int64_t f = 0; f < nfields; f++)
         if (recs[f].status == EBCC_E_RESIDUAL)
@@ -933,18 +1111,18 @@ int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
       CK(cudaMemcpyAsync(payload, c->d_payload, total,
                          (flags & EBCC_OUTPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
                                                          : cudaMemcpyDeviceToHost,
-                         st));
-      CK(cudaStreamSynchronize(st));
+                         c->stream));
+      CK(cudaStreamSynchronize(c->stream));
     }
     return EBCC_OK;
   } catch (CudaFail& e) {
     cudaGetLastError();
     return fail(c, e.e == cudaErrorMemoryAllocation ? EBCC_E_NOMEM : EBCC_E_CUDA,
                 std::string(e.what) + ": " + cudaGetErrorString(e.e));
-  } catch (std::exception& e) {
-    return fail(c, EBCC_E_CUDA, e.what());
   }
 }
+
+extern "C" {
 
 int ebcc_fetch_payload(ebcc_ctx* c, uint8_t* payload, int64_t cap, int32_t flags) {
   if (!c || !payload) return EBCC_E_ARGUMENT;
@@ -1098,7 +1276,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         decode_init(mb, st);
         run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
         gather_refinement(mb, st);
-        pack_meta(mb, w.packed, st);
+        pack_meta(mb, resl ? w.packed2 : w.packed, st);
         c->stats.kernel_launches += 4;
         for (int i = 0; i < nb; i++) {
           prm[i] = ProbeParam{};
@@ -1239,7 +1417,7 @@ int ebcc_spiht_decode(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t pre
     decode_init(mb, st);
     run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
     gather_refinement(mb, st);
-    pack_meta(mb, w.packed, st);
+    pack_meta(mb, w.packed2, st);
     ProbeParam p{};
     p.B = ~0ull; p.planes = -1; p.active = 1;
     CK(cudaMemcpyAsync(w.prm, &p, sizeof(p), cudaMemcpyHostToDevice, st));

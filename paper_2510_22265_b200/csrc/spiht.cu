@@ -269,6 +269,15 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
                                                         int planes) {
   const int f = blockIdx.x;
   if (mb.active && !mb.active[f]) return;
+  if (!DECODE && mb.out[f].n_max == kExpNone) {  // all-zero pyramid: header-only stream
+    if (threadIdx.x == 0) {
+      mb.out[f].planes_run = 0;
+      mb.out[f].total_bits = 0;
+      mb.out[f].overflow = 0;
+      mb.out[f].lsp_count = 0;
+    }
+    return;
+  }
   __shared__ ScanSmem ssm;
   __shared__ Stage st_a, st_b, st_c;
   __shared__ uint64_t red_sm[NW];
