@@ -100,6 +100,8 @@ struct ChunkSearch {
 
   bool constant = false, failed = false;
   int phase = 0;                       // 0 base, 1 pure, 2 trunc, 3 done
+  int64_t pending = -1;                // budget / offset of the probe in flight
+  int pending_planes = 0;
   int64_t base_budget = -1, pure_budget = -1;
   int64_t trunc_t = -1;
   int trunc_planes = 0;
@@ -284,6 +286,7 @@ struct ebcc_ctx {
   fused::Level0Timer l0;
   cudaStream_t side = nullptr;   // high-priority stream for the overlapped residual encode
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+  cudaEvent_t tm_a = nullptr, tm_b = nullptr;
   std::vector<ebcc_ctx*> lanes;  // child contexts for concurrent sub-batches
 };
 
@@ -475,23 +478,21 @@ void pc_mark(PhaseClock* pc, const char* name) {
 
 struct EventTimer {
   ebcc_ctx* c;
-  cudaEvent_t a, b;
   double* acc;
-  EventTimer(ebcc_ctx* c_, double* acc_) : c(c_), acc(acc_) {
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    cudaEventRecord(a, c->stream);
-  }
-  ~EventTimer() {
-    cudaEventRecord(b, c->stream);
-    cudaEventSynchronize(b);
-    float ms = 0;
-    cudaEventElapsedTime(&ms, a, b);
-    *acc += ms;
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-  }
+  EventTimer(ebcc_ctx* c_, double* acc_);
+  ~EventTimer();
 };
+
+EventTimer::EventTimer(ebcc_ctx* c_, double* acc_) : c(c_), acc(acc_) {
+  cudaEventRecord(c->tm_a, c->stream);
+}
+EventTimer::~EventTimer() {
+  cudaEventRecord(c->tm_b, c->stream);
+  cudaEventSynchronize(c->tm_b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c->tm_a, c->tm_b);
+  *acc += ms;
+}
 
 void accumulate_level0(ebcc_ctx* c) {
   float ms = 0;
@@ -565,6 +566,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
           if (phase == 0) s.base_budget = s.search_base();
           else s.pure_budget = s.search_pure(base_entries[f]);
         } catch (NeedBase& nb) {
+          s.pending = nb.budget;
           int64_t len = s.stream_len(nb.budget);
           uint64_t B = (uint64_t)(len - kHeader) * 8;
           if (B > s.T_base) B = s.T_base;
@@ -593,12 +595,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       for (int f = 0; f < nfields; f++) {
         if (!prm[f].active) continue;
         ChunkSearch& s = cs[f];
-        // recover the budget this probe answered (same replay throws the same)
-        int64_t b;
-        try {
-          if (phase == 0) s.search_base(); else s.search_pure(base_entries[f]);
-          continue;  // unreachable
-        } catch (NeedBase& nb) { b = nb.budget; }
+        const int64_t b = s.pending;  // the budget this probe answered
         Entry e;
         e.budget = b;
         e.len = s.stream_len(b);
@@ -692,6 +689,8 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
           pass[f]++;
           if (pass[f] > 1) break;
         } catch (NeedTrunc& nt) {
+          s.pending = nt.t;
+          s.pending_planes = nt.planes;
           int P = nt.planes == 0 ? kBasePlanes : kDeepPlanes;
           uint64_t T = nt.planes == 0 ? T24[f] : T32[f];
           uint64_t Bfull = (uint64_t)nt.t * 8;
@@ -725,14 +724,10 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     for (int f = 0; f < nfields; f++) {
       if (!prm[f].active) continue;
       ChunkSearch& s = cs[f];
-      try {
-        s.search_trunc(pass[f], total_bytes(f, pass[f]));
-      } catch (NeedTrunc& nt) {
-        double e;
-        uint64_t bitsv = res[f].maxerr;
-        memcpy(&e, &bitsv, 8);
-        s.trunc[nt.planes][nt.t] = e;
-      }
+      double e;
+      uint64_t bitsv = res[f].maxerr;
+      memcpy(&e, &bitsv, 8);
+      s.trunc[s.pending_planes][s.pending] = e;
     }
   }
 
@@ -838,6 +833,8 @@ int ebcc_create(int32_t device, ebcc_ctx** out) {
     cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming);
     cudaEventCreate(&c->ev_s0);
     cudaEventCreate(&c->ev_s1);
+    cudaEventCreate(&c->tm_a);
+    cudaEventCreate(&c->tm_b);
   }
   c->own_stream = true;
   *out = c;
@@ -863,6 +860,8 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->ev_b) cudaEventDestroy(c->ev_b);
   if (c->ev_s0) cudaEventDestroy(c->ev_s0);
   if (c->ev_s1) cudaEventDestroy(c->ev_s1);
+  if (c->tm_a) cudaEventDestroy(c->tm_a);
+  if (c->tm_b) cudaEventDestroy(c->tm_b);
   delete c;
 }
 
