@@ -17,9 +17,13 @@
 // (significance read from the stream at the offset the scan assigns), which is
 // how the reference keeps encoder and decoder in lockstep.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "spiht.cuh"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace ebcc {
 
@@ -236,6 +240,44 @@ __device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t& t
 
 __device__ __forceinline__ uint32_t lane16(uint64_t v, int k) { return (uint32_t)(v >> (16 * k)) & 0xffffu; }
 
+// Cluster-wide exclusive scan: the CTAs of a cluster process consecutive
+// sub-tiles of one list, so each thread's prefix is its block prefix plus the
+// totals of the lower-ranked CTAs, exchanged through distributed shared
+// memory with one cluster barrier (double-buffered slots).
+struct ClusterScanOut {
+  uint64_t ex;          // this thread's exclusive prefix over the cluster tile
+  uint64_t total;       // cluster-tile total
+  uint64_t cta_before;  // total of lower-ranked CTAs
+  uint64_t cta_total;   // this CTA's total
+};
+
+__device__ __forceinline__ ClusterScanOut cluster_scan(uint64_t v, ScanSmem& sm, uint64_t* slots,
+                                                       int& parity, const cg::cluster_group& cl) {
+  ClusterScanOut o;
+  uint64_t btot;
+  uint64_t ex = block_exclusive_scan(v, btot, sm);
+  const unsigned n = cl.num_blocks();
+  o.cta_total = btot;
+  if (n == 1) {
+    o.ex = ex; o.total = btot; o.cta_before = 0;
+    return o;
+  }
+  if (threadIdx.x == 0) slots[parity] = btot;
+  cl.sync();
+  const unsigned rank = cl.block_rank();
+  uint64_t before = 0, all = 0;
+  for (unsigned r = 0; r < n; r++) {
+    uint64_t t = *cl.map_shared_rank(&slots[parity], r);
+    if (r < rank) before += t;
+    all += t;
+  }
+  parity ^= 1;
+  o.ex = before + ex;
+  o.total = all;
+  o.cta_before = before;
+  return o;
+}
+
 // bit staging for one contiguous output segment [seg_start, seg_start + len)
 struct Stage {
   uint32_t w[STAGE_WORDS];
@@ -267,10 +309,13 @@ __device__ __forceinline__ void stage_flush(Stage& s, uint64_t seg_start, uint64
 template <bool DECODE>
 __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, TreeTables tt,
                                                         int planes) {
-  const int f = blockIdx.x;
-  if (mb.active && !mb.active[f]) return;
+  cg::cluster_group cl = cg::this_cluster();
+  const int csize = (int)cl.num_blocks();
+  const int crank = (int)cl.block_rank();
+  const int f = blockIdx.x / csize;
+  if (mb.active && !mb.active[f]) return;  // uniform across the cluster
   if (!DECODE && mb.out[f].n_max == kExpNone) {  // all-zero pyramid: header-only stream
-    if (threadIdx.x == 0) {
+    if (crank == 0 && threadIdx.x == 0) {
       mb.out[f].planes_run = 0;
       mb.out[f].total_bits = 0;
       mb.out[f].overflow = 0;
@@ -280,7 +325,13 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   }
   __shared__ ScanSmem ssm;
   __shared__ Stage st_a, st_b, st_c;
-  __shared__ uint64_t red_sm[NW];
+  __shared__ uint64_t slots[2];
+  int parity = 0;
+  auto cscan = [&](uint64_t v) { return cluster_scan(v, ssm, slots, parity, cl); };
+  auto csync = [&]() {
+    if (csize > 1) cl.sync();
+    else __syncthreads();
+  };
 
   const int64_t fo = (int64_t)f * mb.stride;
   uint32_t* sign_pos = mb.sign_pos + fo;
@@ -300,28 +351,33 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   const uint64_t bit_cap = (uint64_t)mb.bit_stride * 32;
   const uint64_t cap = (uint64_t)mb.stride;
   const uint64_t TYPEB = 1ull << ninfo::TYPEB;
+  const bool leader = crank == 0 && threadIdx.x == 0;
+  const uint64_t CT = (uint64_t)TILE * csize;      // entries per cluster tile
+  const uint64_t my0 = (uint64_t)crank * TILE;      // my sub-tile offset
 
-  // initial lists (spiht.py:300-303)
-  for (int64_t i = threadIdx.x; i < tt.nroots; i += MT) lip[i] = info[tt.roots[i]];
-  for (int64_t i = threadIdx.x; i < tt.nlis_roots; i += MT) lis_old[i] = info[tt.lis_roots[i]];
+  // initial lists (spiht.py:300-303); CTAs split the copy
+  for (int64_t i = (int64_t)crank * MT + threadIdx.x; i < tt.nroots; i += (int64_t)MT * csize)
+    lip[i] = info[tt.roots[i]];
+  for (int64_t i = (int64_t)crank * MT + threadIdx.x; i < tt.nlis_roots; i += (int64_t)MT * csize)
+    lis_old[i] = info[tt.lis_roots[i]];
   uint64_t nlip = tt.nroots, nlis = tt.nlis_roots, nlsp = 0, pos = 0;
   int overflow = 0;
   int p = 0;
-  __syncthreads();
+  csync();
 
   for (; p < planes; p++) {
     if (DECODE && pos >= limit) break;  // `while not src.depleted`
     const uint64_t refine_len = nlsp;
-    if (threadIdx.x == 0) prec[p].start = (uint32_t)pos;
+    if (leader) prec[p].start = (uint32_t)pos;
 
     // ---------------- LIP pass: a streaming stable partition -------------
     {
       uint64_t K = 0;  // newly significant so far
-      for (uint64_t base = 0; base < nlip; base += TILE) {
+      for (uint64_t base = 0; base < nlip; base += CT) {
         uint64_t ent[MI];
         int sig[MI];
         int cnt_sig = 0;
-        const uint64_t i0 = base + (uint64_t)threadIdx.x * MI;
+        const uint64_t i0 = base + my0 + (uint64_t)threadIdx.x * MI;
 #pragma unroll
         for (int k = 0; k < MI; k++) {
           uint64_t i = i0 + k;
@@ -333,30 +389,32 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
             cnt_sig += sig[k];
           }
         }
-        uint64_t tot;
-        uint64_t ex = block_exclusive_scan((uint64_t)cnt_sig, tot, ssm);
-        const uint64_t tile_len = (nlip - base) < TILE ? (nlip - base) : TILE;
+        const ClusterScanOut cs = cscan((uint64_t)cnt_sig);
+        const uint64_t ex = cs.ex, tot = cs.total;
+        const uint64_t sub0 = base + my0;
+        const uint64_t my_len = nlip > sub0 ? ((nlip - sub0) < TILE ? (nlip - sub0) : TILE) : 0;
         if (!DECODE) {
           stage_clear(st_a);
           stage_clear(st_b);
           __syncthreads();
-          uint64_t sig_seg = pos + base, sgn_seg = pos + nlip + K;
-          uint32_t r = (uint32_t)ex;
+          uint64_t sig_seg = pos + sub0, sgn_seg = pos + nlip + K + cs.cta_before;
+          uint64_t r = ex;
 #pragma unroll
           for (int k = 0; k < MI; k++) {
             if (!sig[k]) continue;
             stage_set(st_a, sig_seg, pos + i0 + k);
-            if (e_neg(ent[k])) stage_set(st_b, sgn_seg, sgn_seg + r);
+            if (e_neg(ent[k])) stage_set(st_b, sgn_seg, pos + nlip + K + r);
             r++;
           }
           __syncthreads();
-          stage_flush(st_a, sig_seg, tile_len, bits);
-          stage_flush(st_b, sgn_seg, tot, bits);
+          stage_flush(st_a, sig_seg, my_len, bits);
+          stage_flush(st_b, sgn_seg, cs.cta_total, bits);
         }
         // newly significant -> LSP, metadata; survivors compacted in place
-        uint32_t r = (uint32_t)ex;
+        // (every CTA of the cluster loaded its entries before the scan's barrier)
+        uint64_t r = ex;
         uint64_t keep_before = (i0 - base) - ex;
-        __syncthreads();  // all reads of lip[] in this tile done before compaction writes
+        __syncthreads();
 #pragma unroll
         for (int k = 0; k < MI; k++) {
           uint64_t i = i0 + k;
@@ -390,6 +448,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
       pos += nlip + K;
       nlsp += K;
       nlip -= K;
+      csync();  // compaction visible cluster-wide before the LIS appends / next pass
     }
 
     // ---------------- LIS waves ------------------------------------------
@@ -401,9 +460,9 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
       while (cnt) {
         // prepass: total children bits of significant type-A entries
         uint64_t TC = 0;
-        for (uint64_t base = 0; base < cnt; base += TILE) {
+        for (uint64_t base = 0; base < cnt; base += CT) {
           uint64_t local = 0;
-          const uint64_t i0 = base + (uint64_t)threadIdx.x * MI;
+          const uint64_t i0 = base + my0 + (uint64_t)threadIdx.x * MI;
 #pragma unroll
           for (int k = 0; k < MI; k++) {
             uint64_t i = i0 + k;
@@ -413,26 +472,16 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
             int s = DECODE ? read_bit(bits, pos + i, limit) : (e_rel(e, ninfo::RELD) <= p);
             if (s) local += e_nch(e);
           }
-          for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-          if ((threadIdx.x & 31) == 0) red_sm[threadIdx.x >> 5] = local;
-          __syncthreads();
-          if (threadIdx.x < 32) {
-            uint64_t s = threadIdx.x < NW ? red_sm[threadIdx.x] : 0;
-            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (threadIdx.x == 0) red_sm[0] = s;
-          }
-          __syncthreads();
-          TC += red_sm[0];
-          __syncthreads();
+          TC += cscan(local).total;
         }
         const uint64_t ch_seg0 = pos + cnt;       // children significance bits
         const uint64_t sg_seg0 = pos + cnt + TC;  // their sign bits
         uint64_t ch_off = 0, sig_off = 0, nxt_off = 0;
-        for (uint64_t base = 0; base < cnt; base += TILE) {
+        for (uint64_t base = 0; base < cnt; base += CT) {
           uint64_t ent[MI];
           int sig[MI], nch[MI], nxt[MI];
           uint32_t keep = 0, nchs = 0, nxts = 0;
-          const uint64_t i0 = base + (uint64_t)threadIdx.x * MI;
+          const uint64_t i0 = base + my0 + (uint64_t)threadIdx.x * MI;
 #pragma unroll
           for (int k = 0; k < MI; k++) {
             uint64_t i = i0 + k;
@@ -470,9 +519,9 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
           }
 #pragma unroll
           for (int k = 0; k < MI; k++) nxts += nxt[k] > 0 ? nxt[k] : 0;
-          uint64_t tot1;
-          uint64_t ex1 = block_exclusive_scan((uint64_t)keep | ((uint64_t)nchs << 16) |
-                                                  ((uint64_t)nxts << 32), tot1, ssm);
+          const ClusterScanOut s1 = cscan((uint64_t)keep | ((uint64_t)nchs << 16) |
+                                          ((uint64_t)nxts << 32));
+          const uint64_t ex1 = s1.ex, tot1 = s1.total;
           // children significance
           uint8_t chs[MI];  // bitmask of significant children
           uint32_t nsig = 0;
@@ -489,18 +538,20 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
               }
             }
           }
-          uint64_t tot2;
-          uint64_t ex2 = block_exclusive_scan((uint64_t)nsig, tot2, ssm);
-          const uint64_t tile_len = (cnt - base) < TILE ? (cnt - base) : TILE;
-          const uint64_t tile_ch = lane16(tot1, 1);
+          const ClusterScanOut s2 = cscan((uint64_t)nsig);
+          const uint64_t ex2 = s2.ex, tot2 = s2.total;
+          const uint64_t sub0 = base + my0;
+          const uint64_t my_len = cnt > sub0 ? ((cnt - sub0) < TILE ? (cnt - sub0) : TILE) : 0;
           if (!DECODE) {
             stage_clear(st_a);
             stage_clear(st_b);
             stage_clear(st_c);
             __syncthreads();
-            uint64_t seg_a = pos + base, seg_b = ch_seg0 + ch_off, seg_c = sg_seg0 + sig_off;
-            uint64_t cpos = seg_b + lane16(ex1, 1);
-            uint64_t spos = seg_c + ex2;
+            uint64_t seg_a = pos + sub0;
+            uint64_t seg_b = ch_seg0 + ch_off + lane16(s1.cta_before, 1);
+            uint64_t seg_c = sg_seg0 + sig_off + s2.cta_before;
+            uint64_t cpos = ch_seg0 + ch_off + lane16(ex1, 1);
+            uint64_t spos = sg_seg0 + sig_off + ex2;
 #pragma unroll
             for (int k = 0; k < MI; k++) {
               if (sig[k]) stage_set(st_a, seg_a, pos + i0 + k);
@@ -514,9 +565,9 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
               }
             }
             __syncthreads();
-            stage_flush(st_a, seg_a, tile_len, bits);
-            stage_flush(st_b, seg_b, tile_ch, bits);
-            stage_flush(st_c, seg_c, tot2, bits);
+            stage_flush(st_a, seg_a, my_len, bits);
+            stage_flush(st_b, seg_b, lane16(s1.cta_total, 1), bits);
+            stage_flush(st_c, seg_c, s2.cta_total, bits);
           }
           // list updates
           {
@@ -586,25 +637,26 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
         cnt = nxt_off;
         src = dst;
         dst = (dst == wav_a) ? wav_b : wav_a;
-        __syncthreads();
+        csync();  // the next wave reads entries every CTA wrote
       }
       nlis = nkeep;
       uint64_t* t = lis_old; lis_old = lis_new; lis_new = t;
     }
 
     // ---------------- refinement (positions only) ------------------------
-    if (threadIdx.x == 0) {
+    if (leader) {
       prec[p].refine_start = (uint32_t)pos;
       prec[p].refine_len = (uint32_t)refine_len;
     }
     pos += refine_len;
-    if (threadIdx.x == 0) prec[p].lists_end = (uint32_t)(nlip + nlis + nlsp);
+    if (leader) prec[p].lists_end = (uint32_t)(nlip + nlis + nlsp);
     if (!DECODE && pos > bit_cap) { overflow = 1; }
     if (pos > 0xffffffffull) overflow = 1;
     overflow = __syncthreads_or(overflow);
+    if (csize > 1) overflow = cscan((uint64_t)(overflow && threadIdx.x == 0)).total != 0;
     if (overflow) { p++; break; }
   }
-  if (threadIdx.x == 0) {
+  if (leader) {
     mb.out[f].planes_run = p;
     mb.out[f].total_bits = (uint32_t)(pos > 0xffffffffull ? 0xffffffffull : pos);
     mb.out[f].overflow = overflow;
@@ -755,10 +807,31 @@ void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables& tt, cuda
                      st>>>(tt.ginfo, mb, g.n);
 }
 
+int machine_cluster_size(int nfields) {
+  const char* e = getenv("EBCC_MACHINE_CLUSTER");
+  int c = e ? atoi(e) : 148 / (nfields > 0 ? nfields : 1);
+  // measured on B200 (37 fields): 2 CTAs/field beats 1 and 4 (cluster-barrier cost);
+  // 16-bit scan lanes hold at most a 4-CTA cluster tile
+  return c < 1 ? 1 : (c > 2 && !e ? 2 : (c > 4 ? 4 : c));
+}
+
 void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& tt, int planes,
                  cudaStream_t st) {
-  if (decode) machine_kernel<true><<<mb.nfields, MT, 0, st>>>(mb, g, tt, planes);
-  else machine_kernel<false><<<mb.nfields, MT, 0, st>>>(mb, g, tt, planes);
+  const int cs = machine_cluster_size(mb.nfields);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(mb.nfields * cs), 1, 1);
+  cfg.blockDim = dim3(MT, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (decode) cudaLaunchKernelEx(&cfg, machine_kernel<true>, mb, g, tt, planes);
+  else cudaLaunchKernelEx(&cfg, machine_kernel<false>, mb, g, tt, planes);
 }
 
 void write_refinement(MachineBufs& mb, int planes, cudaStream_t st) {
