@@ -36,6 +36,7 @@ extern "C" {
 #define EBCC_E_CAPACITY 4      /* payload buffer too small; see payload_total  */
 #define EBCC_E_CUDA 5          /* CUDA runtime failure -> EbccError              */
 #define EBCC_E_NOMEM 6         /* device allocation failed                     */
+#define EBCC_E_INGEST 7        /* IngestError: non-finite input (core.py:74-79) */
 
 /* flags */
 #define EBCC_INPUT_ON_DEVICE 1   /* `fields` / `payload` are device pointers  */
@@ -70,6 +71,9 @@ void ebcc_destroy(ebcc_ctx *ctx);
 /* Run on this cudaStream_t (default: the context's own stream). */
 int ebcc_set_stream(ebcc_ctx *ctx, void *cuda_stream);
 const char *ebcc_last_error(const ebcc_ctx *ctx);
+/* After EBCC_E_INGEST: flat index (into the `fields` array of the call) of the
+ * first non-finite value, in C order; -1 otherwise. */
+int64_t ebcc_last_error_index(const ebcc_ctx *ctx);
 
 /* Compress `nfields` row-major float32 chunks of rows x cols each, laid out
  * back to back (chunk i at fields + i*rows*cols).  Parameters are the

@@ -14,18 +14,19 @@ import threading
 
 import numpy as np
 
-from .errors import ArgumentError, DeviceError, EbccError, FormatError, ResidualInsufficient
+from .errors import (ArgumentError, DeviceError, EbccError, FormatError, IngestError,
+                     ResidualInsufficient)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("EBCC_LIB") or os.path.join(HERE, "libebcc_gpu.so")
 
-OK, E_ARGUMENT, E_FORMAT, E_RESIDUAL, E_CAPACITY, E_CUDA, E_NOMEM = range(7)
+OK, E_ARGUMENT, E_FORMAT, E_RESIDUAL, E_CAPACITY, E_CUDA, E_NOMEM, E_INGEST = range(8)
 INPUT_ON_DEVICE = 1
 OUTPUT_ON_DEVICE = 2
 
 # the exported symbols include/ebcc_gpu.h declares (checked by the CPU tests)
 EXPORTS = ("ebcc_abi_version", "ebcc_create", "ebcc_destroy", "ebcc_set_stream",
-           "ebcc_last_error", "ebcc_compress", "ebcc_fetch_payload", "ebcc_decompress",
+           "ebcc_last_error", "ebcc_last_error_index", "ebcc_compress", "ebcc_fetch_payload", "ebcc_decompress",
            "ebcc_get_stats", "ebcc_dwt", "ebcc_spiht_encode", "ebcc_spiht_decode",
            "ebcc_selftest_div")
 
@@ -76,6 +77,8 @@ def load(path: str = LIB_PATH):
         L.ebcc_set_stream.argtypes = [P, P]
         L.ebcc_last_error.argtypes = [P]
         L.ebcc_last_error.restype = ctypes.c_char_p
+        L.ebcc_last_error_index.argtypes = [P]
+        L.ebcc_last_error_index.restype = i64
         L.ebcc_compress.argtypes = [P, P, i64, i32, i32, f64, f64, f64, f64, i32, P, P, i64, P, P]
         L.ebcc_fetch_payload.argtypes = [P, P, i64, i32]
         L.ebcc_decompress.argtypes = [P, P, P, P, i64, i32, i32, i32, i32, P]
@@ -125,6 +128,8 @@ class Context:
             raise FormatError(msg)
         if status == E_RESIDUAL:
             raise ResidualInsufficient(msg)
+        if status == E_INGEST:
+            raise IngestError(msg, index=int(self.lib.ebcc_last_error_index(self.handle)))
         if status in (E_CUDA, E_NOMEM):
             raise DeviceError(msg)
         raise EbccError(msg)

@@ -47,10 +47,12 @@ struct CudaFail {
   const char* what;
 };
 
-#define CK(x)                                            \
-  do {                                                   \
-    cudaError_t e_ = (x);                                \
-    if (e_ != cudaSuccess) throw CudaFail{e_, #x};       \
+#define CK_STR2(x) #x
+#define CK_STR(x) CK_STR2(x)
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) throw CudaFail{e_, "engine.cu:" CK_STR(__LINE__) " " #x}; \
   } while (0)
 
 template <class T>
@@ -78,7 +80,38 @@ double py_floordiv(double vx, double wx) {
   return fl;
 }
 
+// host memcpy split over a thread team (first-touch page faults of a fresh
+// destination are spread over the team too)
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  unsigned hw = std::thread::hardware_concurrency();
+  int T = (int)std::min<unsigned>(hw ? hw : 4, 16);
+  if (bytes < (8u << 20) || T <= 1) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  size_t step = (bytes + T - 1) / T;
+  step = (step + 4095) & ~size_t(4095);
+  for (int t = 0; t < T; t++) {
+    size_t lo = (size_t)t * step;
+    if (lo >= bytes) break;
+    size_t n = std::min(step, bytes - lo);
+    th.emplace_back([=] { memcpy((char*)dst + lo, (const char*)src + lo, n); });
+  }
+  for (auto& x : th) x.join();
+}
+
+bool is_pageable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
 struct NeedBase { int64_t budget; };
+struct IngestFail {};
 struct NeedTrunc { int planes; int64_t t; };
 
 // ---------------------------------------------------------------------------
@@ -270,7 +303,11 @@ struct ebcc_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   std::string err;
+  int64_t err_index = -1;   // flat element index of the last EBCC_E_INGEST
   Workspace ws;
+  // pinned staging for pageable host buffers (copied by a thread team)
+  uint8_t* h_stage = nullptr;
+  int64_t h_stage_cap = 0;
   // last compress result
   uint8_t* d_payload = nullptr;
   int64_t payload_cap = 0, payload_total = 0;
@@ -337,7 +374,7 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   w.res = dalloc<ProbeResult>(cap);
   w.limit = dalloc<uint64_t>(cap);
   w.active = dalloc<uint8_t>(cap);
-  w.mm = dalloc<unsigned int>(2 * cap);
+  w.mm = dalloc<unsigned int>(4 * cap + 2);
   CK(cudaMallocHost(&w.h_prm, sizeof(ProbeParam) * cap));
   CK(cudaMallocHost(&w.h_res, sizeof(ProbeResult) * cap));
   build_tree_tables(g, w.tt, c->stream);
@@ -382,6 +419,7 @@ PhaseClock* g_pc = nullptr;
 void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const double* coef,
                    uint4* packed, const std::vector<uint8_t>& active, cudaStream_t st) {
   Workspace& w = c->ws;
+  CK(cudaGetLastError());  // surface anything deferred from before this encode
   MachineBufs mb = machine_bufs(w, nfields, residual);
   std::vector<MachineOut> init(nfields);
   for (auto& m : init) { m = MachineOut{}; m.n_max = kExpNone; }
@@ -389,9 +427,13 @@ void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const do
   CK(cudaMemsetAsync(mb.bits, 0, sizeof(uint32_t) * mb.bit_stride * nfields, st));
   CK(cudaMemcpyAsync(w.active, active.data(), nfields, cudaMemcpyHostToDevice, st));
   coef_prepare(coef, w.g.n, mb, w.g, st);
+  CK(cudaGetLastError());
   subtree_exponents(mb, w.g, w.tt, st);
+  CK(cudaGetLastError());
   run_machine(false, mb, w.g, w.tt, planes, st);
+  CK(cudaGetLastError());
   write_refinement(mb, planes, st);
+  CK(cudaGetLastError());
   pack_meta(mb, packed, st);
   c->stats.kernel_launches += 6 + w.g.levels;
   CK(cudaGetLastError());
@@ -494,6 +536,17 @@ EventTimer::~EventTimer() {
   *acc += ms;
 }
 
+uint8_t* host_stage(ebcc_ctx* c, int64_t bytes) {
+  if (bytes > c->h_stage_cap) {
+    if (c->h_stage) CK(cudaFreeHost(c->h_stage));
+    c->h_stage = nullptr;
+    c->h_stage_cap = 0;
+    CK(cudaMallocHost(&c->h_stage, (size_t)bytes));
+    c->h_stage_cap = bytes;
+  }
+  return c->h_stage;
+}
+
 void accumulate_level0(ebcc_ctx* c) {
   float ms = 0;
   if (cudaEventElapsedTime(&ms, c->l0.a, c->l0.b) == cudaSuccess) {
@@ -515,13 +568,20 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   g_pc = pc.on ? &pc : nullptr;
   double replay_ms = 0;
   // ---- ingest + normalise (core.normalize) ----
+  CK(cudaGetLastError());
   ingest_normalize(w.x32, N, nfields, w.norm, w.fs, w.mm, eps_rel, st);
+  CK(cudaGetLastError());
   pc.mark("ingest");
   c->stats.kernel_launches += 4;
   std::vector<FieldScal> fs(nfields);
   CK(cudaMemcpyAsync(fs.data(), w.fs, sizeof(FieldScal) * nfields, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
 
+  for (int f = 0; f < nfields; f++)
+    if (fs[f].first_bad >= 0) {
+      c->err_index = (int64_t)f * N + fs[f].first_bad;
+      throw IngestFail{};
+    }
   std::vector<ChunkSearch> cs(nfields);
   std::vector<uint8_t> active(nfields);
   for (int f = 0; f < nfields; f++) {
@@ -539,6 +599,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     EventTimer t(c, &c->stats.ms_encode);
     CK(cudaMemcpyAsync(w.A, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
     forward_dwt(w.A, w.B, N, nfields, g, st);
+    CK(cudaGetLastError());
     c->stats.kernel_launches += 2 * g.levels;
     pc.mark("fwd_dwt");
     encode_pyramids(c, nfields, false, kBasePlanes, active, mo, pl);
@@ -852,6 +913,7 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->d_unpack) cudaFree(c->d_unpack);
   if (c->d_stage) cudaFree(c->d_stage);
   if (c->d_out) cudaFree(c->d_out);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (c->l0.a) cudaEventDestroy(c->l0.a);
   if (c->l0.b) cudaEventDestroy(c->l0.b);
@@ -875,6 +937,8 @@ int ebcc_set_stream(ebcc_ctx* c, void* s) {
 
 const char* ebcc_last_error(const ebcc_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
+int64_t ebcc_last_error_index(const ebcc_ctx* c) { return c ? c->err_index : -1; }
+
 int ebcc_get_stats(const ebcc_ctx* c, ebcc_stats* out) {
   if (!c || !out) return EBCC_E_ARGUMENT;
   *out = c->stats;
@@ -894,6 +958,7 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
   c->err.clear();
   try {
     CK(cudaSetDevice(c->device));
+    CK(cudaGetLastError());
     cudaStream_t st = c->stream;
     if (start_after) CK(cudaStreamWaitEvent(st, start_after, 0));
     int levels = clamp_levels(rows, cols, default_levels(rows, cols));
@@ -916,7 +981,18 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
     for (int64_t f0 = 0; f0 < nfields; f0 += cap) {
       int nb = (int)std::min<int64_t>(cap, nfields - f0);
       ensure_workspace(c, g, nb);
-      CK(cudaMemcpyAsync(c->ws.x32, fields + f0 * g.n, sizeof(float) * g.n * nb,
+      CK(cudaGetLastError());
+      const float* src = fields + f0 * g.n;
+      const size_t in_bytes = sizeof(float) * g.n * nb;
+      if (!(flags & EBCC_INPUT_ON_DEVICE) && is_pageable(src)) {
+        CK(cudaGetLastError());
+        uint8_t* stg = host_stage(c, (int64_t)in_bytes);
+        CK(cudaGetLastError());
+        parallel_memcpy(stg, src, in_bytes);
+        src = reinterpret_cast<const float*>(stg);
+      }
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(c->ws.x32, src, in_bytes,
                          (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
                                                         : cudaMemcpyHostToDevice,
                          st));
@@ -924,7 +1000,13 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
       int64_t done = 0;
       for (int64_t z : sizes) done += z;
       std::vector<int64_t> bsizes;
-      int s = compress_batch(c, nb, eps_rel, q, r0, search_tol, recs + f0, done, bparts, bsizes);
+      int s;
+      try {
+        s = compress_batch(c, nb, eps_rel, q, r0, search_tol, recs + f0, done, bparts, bsizes);
+      } catch (IngestFail&) {
+        c->err_index += f0 * g.n;
+        return fail(c, EBCC_E_INGEST, "non-finite value in the input");
+      }
       if (s != EBCC_OK) status = s;
       // pack this batch now: the stream buffers are reused by the next batch
       int64_t bytes = done;
@@ -1024,6 +1106,7 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
   if (!(search_tol > 0.0)) return fail(c, EBCC_E_ARGUMENT, "search_tol must be positive");
   if ((int64_t)rows * cols >= (1ll << 31)) return fail(c, EBCC_E_ARGUMENT, "chunk too large");
   c->err.clear();
+  c->err_index = -1;
   try {
     CK(cudaSetDevice(c->device));
     const int L = lanes_for(nfields);
@@ -1061,6 +1144,7 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
       for (int k = 0; k < L; k++) {
         if (lst[k] != EBCC_OK && lst[k] != EBCC_E_RESIDUAL) {
           c->err = ls[k]->err;
+          c->err_index = ls[k]->err_index + lo[k] * n;
           return lst[k];
         }
         if (lst[k] == EBCC_E_RESIDUAL) status = EBCC_E_RESIDUAL;
@@ -1301,8 +1385,17 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
       fill_constant(w.fs, w.active, g.n, nb, out_dev, st);
       c->stats.kernel_launches += 2;
       CK(cudaGetLastError());
-      if (!(flags & EBCC_OUTPUT_ON_DEVICE))
-        CK(cudaMemcpyAsync(dst, out_dev, sizeof(float) * g.n * nb, cudaMemcpyDeviceToHost, st));
+      if (!(flags & EBCC_OUTPUT_ON_DEVICE)) {
+        const size_t ob = sizeof(float) * g.n * nb;
+        if (is_pageable(dst)) {
+          uint8_t* stg = host_stage(c, (int64_t)ob);
+          CK(cudaMemcpyAsync(stg, out_dev, ob, cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          parallel_memcpy(dst, stg, ob);
+        } else {
+          CK(cudaMemcpyAsync(dst, out_dev, ob, cudaMemcpyDeviceToHost, st));
+        }
+      }
       CK(cudaStreamSynchronize(st));
     }
     cudaEventRecord(t1, st);

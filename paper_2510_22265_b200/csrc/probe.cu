@@ -31,21 +31,26 @@ __device__ __forceinline__ float key_f32(unsigned int k) {
   return __uint_as_float(u);
 }
 
-__global__ void mm_init_kernel(unsigned int* mm, int nfields) {
+__global__ void mm_init_kernel(unsigned int* mm, unsigned long long* first_bad, int nfields) {
   int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f < nfields) { mm[2 * f] = 0xffffffffu; mm[2 * f + 1] = 0u; }
+  if (f < nfields) { mm[2 * f] = 0xffffffffu; mm[2 * f + 1] = 0u; first_bad[f] = ~0ull; }
 }
 
-__global__ void minmax_kernel(const float* __restrict__ x, int64_t n, unsigned int* mm) {
+__global__ void minmax_kernel(const float* __restrict__ x, int64_t n, unsigned int* mm,
+                              unsigned long long* first_bad) {
   const int f = blockIdx.y;
   const float* xf = x + (int64_t)f * n;
   unsigned int lo = 0xffffffffu, hi = 0u;
+  unsigned long long bad = ~0ull;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    unsigned int k = f32_key(xf[i]);
+    float v = xf[i];
+    if (!isfinite(v)) bad = bad < (unsigned long long)i ? bad : (unsigned long long)i;
+    unsigned int k = f32_key(v);
     lo = k < lo ? k : lo;
     hi = k > hi ? k : hi;
   }
+  if (bad != ~0ull) atomicMin(&first_bad[f], bad);  // core._check_finite, on device
   for (int o = 16; o; o >>= 1) {
     unsigned int a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
     lo = a < lo ? a : lo;
@@ -58,7 +63,8 @@ __global__ void minmax_kernel(const float* __restrict__ x, int64_t n, unsigned i
 }
 
 // core.normalize (core.py:161-180) + _ChunkCoder.eps_abs (pipeline.py:98)
-__global__ void scalars_kernel(const unsigned int* mm, int nfields, double eps_rel, FieldScal* fs) {
+__global__ void scalars_kernel(const unsigned int* mm, const unsigned long long* first_bad,
+                               int nfields, double eps_rel, FieldScal* fs) {
   int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nfields) return;
   double vmin = (double)key_f32(mm[2 * f]), vmax = (double)key_f32(mm[2 * f + 1]);
@@ -70,6 +76,7 @@ __global__ void scalars_kernel(const unsigned int* mm, int nfields, double eps_r
   s.eps_abs = __dmul_rn(eps_rel, range);
   s.constant = range < 1e-30;
   s.pad = 0;
+  s.first_bad = (long long)(first_bad[f] == ~0ull ? -1ll : (long long)first_bad[f]);
   fs[f] = s;
 }
 
@@ -288,9 +295,10 @@ __global__ void unpack_kernel(const UnpackPart* parts, const uint8_t* in) {
 
 void ingest_normalize(const float* x, int64_t n, int nfields, double* norm, FieldScal* fs,
                       unsigned int* mm, double eps_rel, cudaStream_t st) {
-  mm_init_kernel<<<(nfields + 127) / 128, 128, 0, st>>>(mm, nfields);
-  minmax_kernel<<<dim3(grid_for(n, 512), nfields), 256, 0, st>>>(x, n, mm);
-  scalars_kernel<<<(nfields + 127) / 128, 128, 0, st>>>(mm, nfields, eps_rel, fs);
+  unsigned long long* first_bad = reinterpret_cast<unsigned long long*>(mm + 2 * nfields);
+  mm_init_kernel<<<(nfields + 127) / 128, 128, 0, st>>>(mm, first_bad, nfields);
+  minmax_kernel<<<dim3(grid_for(n, 512), nfields), 256, 0, st>>>(x, n, mm, first_bad);
+  scalars_kernel<<<(nfields + 127) / 128, 128, 0, st>>>(mm, first_bad, nfields, eps_rel, fs);
   normalize_kernel<<<dim3(grid_for(n, 1024), nfields), 256, 0, st>>>(x, n, fs, norm);
 }
 

@@ -14,6 +14,7 @@ struct FieldScal {
   double eps_rel, eps_abs;
   int32_t constant;
   int32_t pad;
+  long long first_bad;       // first non-finite element of the chunk, -1 if none
 };
 
 // what one probe decodes
@@ -47,7 +48,8 @@ void selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_
 // build Meta::packed from the machine's per-coefficient arrays
 void pack_meta(const MachineBufs& mb, uint4* packed, cudaStream_t st);
 
-// f32 input -> per-field vmin/vmax/constant flag and float64 normalised field
+// f32 input -> per-field vmin/vmax/constant flag/first non-finite index and
+// the float64 normalised field.  `mm` holds 2*nfields u32 + nfields u64.
 void ingest_normalize(const float* x, int64_t n, int nfields, double* norm, FieldScal* fs,
                       unsigned int* mm, double eps_rel, cudaStream_t st);
 

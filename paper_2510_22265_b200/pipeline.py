@@ -25,7 +25,7 @@ from .chunk import CompressedChunk, EbccParams, Mode
 from .container import RECORD_DTYPE
 from .core import (Chunk, GridArray, block_shape_at, flatten_chunk, iter_blocks, tile_origins,
                    unflatten_chunk)
-from .errors import ArgumentError, EbccError, FormatError, ResidualInsufficient
+from .errors import ArgumentError, EbccError, FormatError, IngestError, ResidualInsufficient
 
 __all__ = ["Mode", "EbccParams", "CompressedChunk", "compress_chunk", "decompress_chunk",
            "compress_grid", "decompress_grid", "compress_batch", "decompress_batch",
@@ -237,21 +237,31 @@ def decompress_grid(chunks, dims, chunk_shape=None, ctx=None) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # container-level fast paths used by api.compress / api.decompress
 
-def grid_to_records(grid: GridArray, params: EbccParams, ctx=None):
+def grid_to_records(grid: GridArray, params: EbccParams, ctx=None, orig_shape=None):
     """Compress a grid straight to (records[RECORD_DTYPE], payload, offsets).
 
     Default chunking (one 2D slice per (t, p)) is fed to the device without a
-    host-side gather.  Error semantics equal compress_grid's.
+    host-side gather, and the non-finite scan happens on the device (reported
+    as IngestError with the index in ``orig_shape``, the caller's array
+    shape).  Error semantics and their order equal the reference's
+    (ingest before parameter validation, core.py:89-105 / pipeline.py:54).
     """
     t, p, h, w = grid.dims
+    shape = tuple(orig_shape) if orig_shape is not None else tuple(grid.dims)
     if tuple(grid.chunk_shape) == (1, 1, h, w):
         origins = tile_origins(grid.dims, grid.chunk_shape)
         try:
             params.validate()
         except ArgumentError as exc:
+            from .core import _require_finite
+            _require_finite(grid.data.reshape(shape))
             raise _chunk_error(origins[0], exc)
         stack = grid.data.reshape(t * p, h, w)
-        recs, offs, payload, st = compress_batch(stack, params, ctx)
+        try:
+            recs, offs, payload, st = compress_batch(stack, params, ctx)
+        except IngestError as exc:
+            at = tuple(int(i) for i in np.unravel_index(int(exc.index), shape))
+            raise IngestError(f"non-finite value at index {at}", index=at) from None
         if st == _lib.E_RESIDUAL:
             bad = int(np.flatnonzero(recs["status"] == _lib.E_RESIDUAL)[0])
             raise _chunk_error(origins[bad], ResidualInsufficient(
@@ -265,6 +275,8 @@ def grid_to_records(grid: GridArray, params: EbccParams, ctx=None):
         out["base_len"] = recs["base_len"]
         out["resid_len"] = recs["resid_len"]
         return out, payload, offs, recs
+    from .core import _require_finite
+    _require_finite(grid.data.reshape(shape))
     chunks = compress_grid(grid, params, ctx)
     out = np.zeros(len(chunks), dtype=RECORD_DTYPE)
     offs = np.zeros(len(chunks), dtype=np.int64)

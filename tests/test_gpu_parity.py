@@ -207,3 +207,21 @@ def test_fma_corrected_division_is_exact(ctx):
     """The kernels replace x/SCALE and x/range by an FMA-corrected reciprocal
     multiply; it must equal IEEE division bit for bit (2^28 cases x 3)."""
     assert ctx.selftest_div(1 << 28, seed=20251020) == 0
+
+
+def test_ingest_errors_from_device(ebcc):
+    """Non-finite input is reported by the device ingest kernel with the
+    reference's IngestError(index) (core.py:74-79), before param validation."""
+    a = np.random.default_rng(1).standard_normal((3, 40, 50)).astype(np.float32)
+    a[1, 7, 9] = np.nan
+    a[2, 0, 0] = np.inf
+    with pytest.raises(ebcc.IngestError) as ei:
+        ebcc.compress(a, 0.01)
+    assert ei.value.index == (1, 7, 9)
+    with pytest.raises(ebcc.IngestError):
+        ebcc.compress(a, 2.0)  # bad param too: ingest error wins, like the reference
+    b = np.ones((20, 30), np.float32)
+    b[-1, -1] = -np.inf
+    with pytest.raises(ebcc.IngestError) as ei:
+        ebcc.compress(b)
+    assert ei.value.index == (19, 29)
