@@ -188,11 +188,13 @@ def run_ours(args, rank, world, local_rank):
     clocks = sampler.stop()
 
     # size/offset all-gather: the one collective of the sharded path
-    sizes = torch.tensor([int(total)], dtype=torch.int64, device=dev)
+    cdev = dev if torch.distributed.is_initialized() and \
+        torch.distributed.get_backend() == "nccl" else torch.device("cpu")
+    sizes = torch.tensor([int(total)], dtype=torch.int64, device=cdev)
     if world > 1:
         gathered = [torch.zeros_like(sizes) for _ in range(world)]
         torch.distributed.all_gather(gathered, sizes)
-        tt = torch.tensor([t_c, t_d], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_c, t_d], dtype=torch.float64, device=cdev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_c, t_d = float(tt[0]), float(tt[1])
         total_payload = int(sum(int(g.item()) for g in gathered))
@@ -200,7 +202,7 @@ def run_ours(args, rank, world, local_rank):
         total_payload = int(total)
 
     # ---- e2e: the public API with host buffers, H2D + D2H inside ----
-    e2e_t = 0.0
+    e2e_t = e2e_c = 0.0
     e2e_steps = max(1, min(args.steps, 3))
     blob = None
     for _ in range(e2e_steps):
@@ -208,18 +210,23 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         blob = ebcc.compress(pinned.numpy(), rel_error=EPS, q=Q)
+        t1 = time.perf_counter()
         rec_host = ebcc.decompress(blob)
         torch.cuda.synchronize()
         e2e_t += time.perf_counter() - t0
+        e2e_c += t1 - t0
     assert rec_host.shape == (1, nf, ROWS, COLS)
+    if world > 1:
+        te = torch.tensor([e2e_t, e2e_c], dtype=torch.float64, device=cdev)
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        e2e_t, e2e_c = float(te[0]), float(te[1])
 
     steps = args.steps
     bytes_in = 4.0 * n * nf
     value = bytes_in * world * steps / (t_c + t_d) / 1e9
     c_gbs = bytes_in * world * steps / t_c / 1e9
     d_gbs = bytes_in * world * steps / t_d / 1e9
-    e2e_val = bytes_in * world * e2e_steps / e2e_t / 1e9 if world == 1 else \
-        bytes_in * e2e_steps / e2e_t / 1e9 * world
+    e2e_val = bytes_in * world * e2e_steps / e2e_t / 1e9  # max-over-ranks time
     ratio = bytes_in * world / (total_payload + 42 + 25 * nf * world)
     p_base = int(recs["n_base_probes"].sum())
     p_trunc = int(recs["n_trunc_probes"].sum())
@@ -278,7 +285,11 @@ def run_ours(args, rank, world, local_rank):
                    "ms_encode_per_compress": enc_ms / steps},
         "e2e": {"value": round(e2e_val, 4), "unit": "GB/s",
                 "h2d_bytes_per_step": int(bytes_in + len(blob)),
-                "d2h_bytes_per_step": int(len(blob) + bytes_in)},
+                "d2h_bytes_per_step": int(len(blob) + bytes_in),
+                "ms_compress": round(e2e_c / e2e_steps * 1e3, 2),
+                "ms_decompress": round((e2e_t - e2e_c) / e2e_steps * 1e3, 2),
+                "path": "paper_2510_22265_b200.compress(pinned host array) -> container bytes "
+                        "-> paper_2510_22265_b200.decompress -> host ndarray"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
@@ -379,8 +390,15 @@ def main():
         return
     if world > 1:
         import torch
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl")
+        if os.environ.get("EBCC_BENCH_SAME_DEVICE") == "1":
+            # test hook for 1-GPU boxes: every rank on cuda:0, collectives over
+            # gloo (the ranks' kernels never wait on one another)
+            local_rank = 0
+            torch.cuda.set_device(0)
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            torch.distributed.init_process_group("nccl")
     line = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(line), flush=True)
