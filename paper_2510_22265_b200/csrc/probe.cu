@@ -109,8 +109,8 @@ __global__ void decode_coeffs_kernel(Meta m, const ProbeParam* __restrict__ prm,
   const double off = P.midpoint ? scalbn(0.5, n_last) : 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    out[(int64_t)f * n + i] = fused::decode_raw(m.packed[fo + i], P.B, planes, n_max,
-                                                P.midpoint != 0, off, T);
+    out[(int64_t)f * n + i] = fused::decode_raw_scan(m.packed[fo + i], P.B, planes, n_max,
+                                                     P.midpoint != 0, off, T);
 }
 
 __global__ void pack_meta_kernel(MachineBufs mb, uint4* packed) {
@@ -161,7 +161,7 @@ struct BaseProbeEpi {
     double nv = fused::div_exact(__dsub_rn((double)o, s.vmin), s.range, s.range_inv);
     cnt += fabs(__dsub_rn(dec, nv)) <= s.eps_rel;
     double e = denorm_err(s, dec, o);
-    mx = e > mx ? e : mx;
+    mx = fmax(e, mx);
   }
   __device__ void finish(int f) { warp_flush(&res[f], cnt, mx, true); }
 };
@@ -188,7 +188,7 @@ struct TruncProbeEpi {
   __device__ void put(double*, int f, int64_t off, double v, const Pre& p) {
     double rec = __dadd_rn(p.base, v);  // base_field + dequantized
     double e = denorm_err(s, rec, p.orig);
-    mx = e > mx ? e : mx;
+    mx = fmax(e, mx);
   }
   __device__ void finish(int f) { warp_flush(&res[f], 0, mx, false); }
 };
@@ -356,34 +356,34 @@ void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, cons
                 int nfields, const double* norm, const float* orig, const FieldScal* fs,
                 ProbeResult* res, cudaStream_t st) {
   BaseProbeEpi e{norm, orig, fs, prm, res, g.n, 0, 0.0, FieldScal{}};
-  fused::inverse_fused(m, prm, a, b, g, nfields, st, e);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false);
 }
 
 void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                  int nfields, const double* base_dec, const float* orig, const FieldScal* fs,
                  ProbeResult* res, cudaStream_t st) {
   TruncProbeEpi e{base_dec, orig, fs, prm, res, g.n, 0.0, FieldScal{}};
-  fused::inverse_fused(m, prm, a, b, g, nfields, st, e);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, true);
 }
 
 void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                      int nfields, const double* norm, double* base_dec, double* resid,
                      cudaStream_t st) {
   ResidueEpi e{norm, base_dec, resid, prm, g.n};
-  fused::inverse_fused(m, prm, a, b, g, nfields, st, e);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false);
 }
 
 void decode_field(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                   int nfields, double* out, cudaStream_t st) {
   StoreFieldEpi e{out, prm, g.n};
-  fused::inverse_fused(m, prm, a, b, g, nfields, st, e);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false);
 }
 
 void decode_field_add_denorm(const Meta& m, const ProbeParam* prm, double* a, double* b,
                              const Geo& g, int nfields, const double* base, const FieldScal* fs,
                              float* out32, cudaStream_t st) {
   AddDenormEpi e{base, fs, prm, out32, g.n, FieldScal{}};
-  fused::inverse_fused(m, prm, a, b, g, nfields, st, e);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, true);
 }
 
 void denorm_only(const double* base, const FieldScal* fs, const uint8_t* active, int64_t n,
