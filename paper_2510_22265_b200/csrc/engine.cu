@@ -149,11 +149,24 @@ struct ChunkSearch {
     int64_t full = kHeader + (int64_t)((T_base + 7) / 8);
     return b < full ? b : full;
   }
+  // Replay miss handling: the first memo miss of a replay is the probe to
+  // run next.  Instead of unwinding (an exception per chunk per step), the
+  // replay continues on a dummy infeasible answer (q = 0, error = inf), which
+  // drives every loop of the searches to termination; its result is ignored.
+  bool missed = false;
+  int64_t miss_key = -1;
+  int miss_planes = 0;
+  Entry dummy{};
+
   // _ChunkCoder.at_budget with the replay timeline
   const Entry& at_budget(int64_t b) {
     b = clamp_budget(b);
     auto it = at.find(b);
-    if (it == at.end()) throw NeedBase{b};
+    if (it == at.end()) {
+      if (!missed) { missed = true; miss_key = b; }
+      dummy = Entry{b, 0, 0, INFINITY};
+      return dummy;
+    }
     size_t seq = (size_t)it->second;
     if (seq == vsize) vsize++;
     return memo[seq];
@@ -233,7 +246,10 @@ struct ChunkSearch {
   int64_t search_trunc(int pi, int64_t total) {
     auto err_at = [&](int64_t t) -> double {
       auto it = trunc[pi].find(t);
-      if (it == trunc[pi].end()) throw NeedTrunc{pi, t};
+      if (it == trunc[pi].end()) {
+        if (!missed) { missed = true; miss_key = t; miss_planes = pi; }
+        return INFINITY;
+      }
       n_trunc_calls++;
       return it->second;
     };
@@ -547,11 +563,45 @@ uint8_t* host_stage(ebcc_ctx* c, int64_t bytes) {
   return c->h_stage;
 }
 
-void accumulate_level0(ebcc_ctx* c) {
+// One feedback-probe step (H2D params, reset results, the level kernels, D2H
+// results) replayed as a CUDA graph: the first step of each kind runs
+// eagerly (it also sets kernel attributes), the second is captured, later
+// steps only launch the graph.
+struct StepGraph {
+  cudaGraphExec_t exec = nullptr;
+  int eager = 0;
+  ~StepGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+  template <class F>
+  void run(cudaStream_t st, F enqueue) {
+    static const bool off = getenv("EBCC_GRAPHS") && getenv("EBCC_GRAPHS")[0] == '0';
+    if (off || eager < 1) {
+      enqueue(true);
+      eager++;
+      return;
+    }
+    if (!exec) {
+      cudaGraph_t gr = nullptr;
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      enqueue(false);
+      CK(cudaStreamEndCapture(st, &gr));
+      CK(cudaGraphInstantiate(&exec, gr, 0));
+      cudaGraphDestroy(gr);
+    }
+    CK(cudaGraphLaunch(exec, st));
+  }
+};
+
+// level-0 kernel timing: only eager (uncaptured) steps record the events
+void accumulate_level0(ebcc_ctx* c, bool timed) {
+  if (!timed) return;
   float ms = 0;
   if (cudaEventElapsedTime(&ms, c->l0.a, c->l0.b) == cudaSuccess) {
     c->stats.ms_probe_kernel += ms;
     c->stats.probe_kernel_count++;
+  } else {
+    cudaGetLastError();
   }
 }
 
@@ -612,6 +662,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   std::vector<ProbeParam> prm(nfields);
   std::vector<ProbeResult> res(nfields);
   Meta mbase = meta_of(w, false);
+  StepGraph base_graph, trunc_graph;
 
   // ---- base-memo searches (phase 0: quantile search, phase 1: pure) ----
   std::vector<size_t> base_entries(nfields, 0);
@@ -623,12 +674,14 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
         ChunkSearch& s = cs[f];
         prm[f] = ProbeParam{};
         if (s.constant) continue;
-        try {
-          if (phase == 0) s.base_budget = s.search_base();
-          else s.pure_budget = s.search_pure(base_entries[f]);
-        } catch (NeedBase& nb) {
-          s.pending = nb.budget;
-          int64_t len = s.stream_len(nb.budget);
+        s.missed = false;
+        int64_t r = phase == 0 ? s.search_base() : s.search_pure(base_entries[f]);
+        if (!s.missed) {
+          if (phase == 0) s.base_budget = r;
+          else s.pure_budget = r;
+        } else {
+          s.pending = s.miss_key;
+          int64_t len = s.stream_len(s.miss_key);
           uint64_t B = (uint64_t)(len - kHeader) * 8;
           if (B > s.T_base) B = s.T_base;
           prm[f].B = B;
@@ -641,17 +694,23 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       if (!any) break;
       EventTimer t(c, &c->stats.ms_probe);
       memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
-      CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
-      CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
-      fused::g_level0_timer = &c->l0;
-      probe_base(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.x32, w.fs, w.res, st);
-      fused::g_level0_timer = nullptr;
+      bool timed = false;
+      base_graph.run(st, [&](bool eager) {
+        timed = eager;
+        CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice,
+                           st));
+        CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
+        fused::g_level0_timer = eager ? &c->l0 : nullptr;
+        probe_base(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.x32, w.fs, w.res, st);
+        fused::g_level0_timer = nullptr;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost,
+                           st));
+      });
       c->stats.kernel_launches += g.levels;
       c->stats.probe_launches++;
-      CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      accumulate_level0(c);
+      accumulate_level0(c, timed);
       memcpy(res.data(), w.h_res, sizeof(ProbeResult) * nfields);
       for (int f = 0; f < nfields; f++) {
         if (!prm[f].active) continue;
@@ -738,8 +797,9 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       prm[f] = ProbeParam{};
       if (s.constant || s.trunc_planes || pass[f] > 1) continue;
       for (;;) {
-        try {
-          int64_t t = s.search_trunc(pass[f], total_bytes(f, pass[f]));
+        s.missed = false;
+        int64_t t = s.search_trunc(pass[f], total_bytes(f, pass[f]));
+        if (!s.missed) {
           if (t >= 0) {
             s.trunc_t = t;
             s.trunc_planes = pass[f] == 0 ? kBasePlanes : kDeepPlanes;
@@ -749,7 +809,8 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
           trunc_calls[f] += s.n_trunc_calls;
           pass[f]++;
           if (pass[f] > 1) break;
-        } catch (NeedTrunc& nt) {
+        } else {
+          NeedTrunc nt{s.miss_planes, s.miss_key};
           s.pending = nt.t;
           s.pending_planes = nt.planes;
           int P = nt.planes == 0 ? kBasePlanes : kDeepPlanes;
@@ -770,17 +831,21 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     if (!any) break;
     EventTimer t(c, &c->stats.ms_probe);
     memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
-    CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
-    fused::g_level0_timer = &c->l0;
-    probe_trunc(mres, w.prm, w.A, w.B, g, nfields, w.base_dec, w.x32, w.fs, w.res, st);
-    fused::g_level0_timer = nullptr;
+    bool timed = false;
+      trunc_graph.run(st, [&](bool eager) {
+        timed = eager;
+      CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
+      fused::g_level0_timer = eager ? &c->l0 : nullptr;
+      probe_trunc(mres, w.prm, w.A, w.B, g, nfields, w.base_dec, w.x32, w.fs, w.res, st);
+      fused::g_level0_timer = nullptr;
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
+    });
     c->stats.kernel_launches += g.levels;
     c->stats.probe_launches++;
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    accumulate_level0(c);
+    accumulate_level0(c, timed);
     memcpy(res.data(), w.h_res, sizeof(ProbeResult) * nfields);
     for (int f = 0; f < nfields; f++) {
       if (!prm[f].active) continue;

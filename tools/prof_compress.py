@@ -25,6 +25,8 @@ for it in range(iters):
                                          1e-3, flags=F, payload=pay.data_ptr(),
                                          payload_cap=pay.numel())
     t1 = time.perf_counter()
+    if st:
+        print("compress status", st, ctx.error(), file=sys.stderr)
     print(f"compress wall {1e3*(t1 - t0):.1f} ms", ctx.stats(), file=sys.stderr)
     ctx.decompress(pay.data_ptr(), offs, recs, 721, 1440, 5, out.data_ptr(), flags=F)
     torch.cuda.synchronize()
