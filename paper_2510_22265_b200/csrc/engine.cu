@@ -433,7 +433,8 @@ PhaseClock* g_pc = nullptr;
 // encode the pyramids in `coef` (all fields): exponents, machine (which
 // skips all-zero pyramids itself), refinement, packed metadata.  Async on st.
 void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const double* coef,
-                   uint4* packed, const std::vector<uint8_t>& active, cudaStream_t st) {
+                   uint4* packed, const std::vector<uint8_t>& active, cudaStream_t st,
+                   int cluster = 0) {
   Workspace& w = c->ws;
   CK(cudaGetLastError());  // surface anything deferred from before this encode
   MachineBufs mb = machine_bufs(w, nfields, residual);
@@ -446,7 +447,7 @@ void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const do
   CK(cudaGetLastError());
   subtree_exponents(mb, w.g, w.tt, st);
   CK(cudaGetLastError());
-  run_machine(false, mb, w.g, w.tt, planes, st);
+  run_machine(false, mb, w.g, w.tt, planes, st, cluster);
   CK(cudaGetLastError());
   write_refinement(mb, planes, st);
   CK(cudaGetLastError());
@@ -755,7 +756,11 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       CK(cudaMemcpyAsync(w.A2, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, rs));
       forward_dwt(w.A2, w.B2, N, nfields, g, rs);
       c->stats.kernel_launches += 2 * g.levels;
-      encode_launch(c, nfields, true, kDeepPlanes, w.A2, w.packed2, active, rs);
+      // off the critical path while overlapped: one CTA per field leaves
+      // more SMs to the pure-search probes running beside it
+      static const int rc = getenv("EBCC_RESID_CLUSTER") ? atoi(getenv("EBCC_RESID_CLUSTER")) : 1;
+      encode_launch(c, nfields, true, kDeepPlanes, w.A2, w.packed2, active, rs,
+                    overlap ? rc : 0);
       CK(cudaEventRecord(c->ev_s1, rs));
       CK(cudaEventRecord(c->ev_b, rs));
       if (!overlap) pc.mark("residual_encode(serial)");

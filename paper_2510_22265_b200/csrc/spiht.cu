@@ -816,8 +816,8 @@ int machine_cluster_size(int nfields) {
 }
 
 void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& tt, int planes,
-                 cudaStream_t st) {
-  const int cs = machine_cluster_size(mb.nfields);
+                 cudaStream_t st, int cluster) {
+  const int cs = cluster > 0 ? cluster : machine_cluster_size(mb.nfields);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(mb.nfields * cs), 1, 1);
   cfg.blockDim = dim3(MT, 1, 1);

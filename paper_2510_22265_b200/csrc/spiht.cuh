@@ -77,8 +77,9 @@ void coef_prepare(const double* coef, int64_t field_stride, MachineBufs& mb, con
 // e_d / e_l bottom-up, then the per-field node info words
 void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables& tt, cudaStream_t st);
 // the list machine (one CTA per field)
+// cluster > 0 forces the CTAs per field (1..4); 0 picks by batch size
 void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& tt, int planes,
-                 cudaStream_t st);
+                 cudaStream_t st, int cluster = 0);
 // encoder refinement bits (fully parallel over LSP)
 void write_refinement(MachineBufs& mb, int planes, cudaStream_t st);
 // decoder: reset per-coefficient metadata before run_machine(decode=true)
