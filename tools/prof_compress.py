@@ -17,6 +17,10 @@ x = torch.from_numpy(host).cuda()
 pay = torch.empty(host.nbytes * 2, dtype=torch.uint8, device="cuda")
 out = torch.empty_like(x)
 ctx = _lib.context(0)
+if os.environ.get("TORCH_STREAM") == "1":
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
 F = _lib.INPUT_ON_DEVICE | _lib.OUTPUT_ON_DEVICE
 for it in range(iters):
     torch.cuda.synchronize()
