@@ -449,10 +449,12 @@ void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const do
   CK(cudaGetLastError());
   run_machine(false, mb, w.g, w.tt, planes, st, cluster);
   CK(cudaGetLastError());
+  emit_lip(mb, planes, st);
+  CK(cudaGetLastError());
   write_refinement(mb, planes, st);
   CK(cudaGetLastError());
   pack_meta(mb, packed, st);
-  c->stats.kernel_launches += 6 + w.g.levels;
+  c->stats.kernel_launches += 9 + w.g.levels;
   CK(cudaGetLastError());
 }
 

@@ -326,6 +326,13 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   __shared__ ScanSmem ssm;
   __shared__ Stage st_a, st_b, st_c;
   __shared__ uint64_t slots[2];
+  // encoder: the LIP passes are deferred to emit_lip; the machine only needs
+  // |LIP_p| and the count K_p of LIP entries turning significant at plane p.
+  // An entry appended while coding plane q with relc r is in the LIP for
+  // planes q+1..r: difference counts over planes, summed across the cluster.
+  __shared__ int s_diff[66];
+  __shared__ int s_knew[64];
+  __shared__ long long s_bc[2];
   int parity = 0;
   auto cscan = [&](uint64_t v) { return cluster_scan(v, ssm, slots, parity, cl); };
   auto csync = [&]() {
@@ -356,11 +363,25 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   const uint64_t my0 = (uint64_t)crank * TILE;      // my sub-tile offset
 
   // initial lists (spiht.py:300-303); CTAs split the copy
-  for (int64_t i = (int64_t)crank * MT + threadIdx.x; i < tt.nroots; i += (int64_t)MT * csize)
-    lip[i] = info[tt.roots[i]];
+  if (!DECODE) {
+    for (int i = threadIdx.x; i < 66; i += MT) s_diff[i] = 0;
+    for (int i = threadIdx.x; i < 64; i += MT) s_knew[i] = 0;
+    __syncthreads();
+    if (leader) s_diff[0] = (int)tt.nroots;
+  }
+  for (int64_t i = (int64_t)crank * MT + threadIdx.x; i < tt.nroots; i += (int64_t)MT * csize) {
+    const uint64_t e = info[tt.roots[i]];
+    lip[i] = e;
+    if (!DECODE) {
+      const int r = e_rel(e, ninfo::RELC);
+      atomicSub(&s_diff[r + 1], 1);
+      atomicAdd(&s_knew[r], 1);
+    }
+  }
   for (int64_t i = (int64_t)crank * MT + threadIdx.x; i < tt.nlis_roots; i += (int64_t)MT * csize)
     lis_old[i] = info[tt.lis_roots[i]];
   uint64_t nlip = tt.nroots, nlis = tt.nlis_roots, nlsp = 0, pos = 0;
+  uint64_t hlen = tt.nroots, lip_run = 0;  // encoder: LIP history length, |LIP_p|
   int overflow = 0;
   int p = 0;
   csync();
@@ -370,8 +391,27 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
     const uint64_t refine_len = nlsp;
     if (leader) prec[p].start = (uint32_t)pos;
 
+    if (!DECODE) {
+      // ------------- LIP pass (encoder): counts only -----------------------
+      if (threadIdx.x == 0) {
+        long long d = 0, kk = 0;
+        for (int r = 0; r < csize; r++) {
+          d += *cl.map_shared_rank(&s_diff[p], r);
+          kk += *cl.map_shared_rank(&s_knew[p], r);
+        }
+        s_bc[0] = d;
+        s_bc[1] = kk;
+      }
+      __syncthreads();
+      lip_run += (uint64_t)s_bc[0];
+      const uint64_t K = (uint64_t)s_bc[1];
+      if (leader) prec[p].lip_len = (uint32_t)lip_run;
+      pos += lip_run + K;
+      nlsp += K;
+      nlip -= K;
+    }
     // ---------------- LIP pass: a streaming stable partition -------------
-    {
+    if (DECODE) {
       uint64_t K = 0;  // newly significant so far
       for (uint64_t base = 0; base < nlip; base += CT) {
         uint64_t ent[MI];
@@ -605,8 +645,13 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
                   }
                   sg++;
                 } else {
-                  uint64_t li = nlip + ins;
+                  uint64_t li = (DECODE ? nlip : hlen) + ins;
                   if (li < cap) lip[li] = cin[k][s]; else overflow = 1;
+                  if (!DECODE) {
+                    const int r = e_rel(cin[k][s], ninfo::RELC);
+                    atomicSub(&s_diff[r + 1], 1);
+                    atomicAdd(&s_knew[r], 1);
+                  }
                   ins++;
                 }
               }
@@ -634,6 +679,10 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
         pos += cnt + TC + sig_off;
         nlsp += sig_off;
         nlip += TC - sig_off;
+        if (!DECODE) {
+          hlen += TC - sig_off;
+          if (leader) s_diff[p + 1] += (int)(TC - sig_off);
+        }
         cnt = nxt_off;
         src = dst;
         dst = (dst == wav_a) ? wav_b : wav_a;
@@ -661,6 +710,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
     mb.out[f].total_bits = (uint32_t)(pos > 0xffffffffull ? 0xffffffffull : pos);
     mb.out[f].overflow = overflow;
     mb.out[f].lsp_count = (uint32_t)nlsp;
+    mb.out[f].hist_len = (uint32_t)hlen;
   }
 }
 
@@ -730,6 +780,148 @@ __global__ void refine_gather_kernel(MachineBufs mb) {
     }
     mb.mant[fo + c] = m;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Deferred encoder LIP passes.  The LIP before plane p's pass is the LIP
+// history H (roots, then every insignificant child in append order) filtered
+// by relc >= p: entries leave the LIP at their significance plane and are
+// appended in plane order (an entry appended while coding plane q has
+// relc > q).  So entry i with relc r < planes_run has
+//   significance bit at  start[r] + #{j < i : relc_j >= r}
+//   sign bit at          start[r] + lip_len[r] + #{j < i : relc_j == r}
+//   LSP rank             refine_len[r] + #{j < i : relc_j == r}
+// (spiht.py's LIP pass, every plane at once): two rank-by-value counts over
+// 64 relc buckets, from tile histograms, per-warp histograms and a bit-sliced
+// in-warp compare.
+constexpr int ET = 1024;  // LIP-history entries per emit tile (one per thread)
+
+__device__ __forceinline__ bool emit_skip(const MachineBufs& mb, int f) {
+  return (mb.active && !mb.active[f]) || mb.out[f].overflow;
+}
+
+__device__ __forceinline__ uint32_t hist_len_of(const MachineBufs& mb, int f) {
+  const uint32_t h = mb.out[f].hist_len;
+  return (int64_t)h < mb.stride ? h : (uint32_t)mb.stride;
+}
+
+__global__ void __launch_bounds__(ET) lip_hist_kernel(MachineBufs mb, uint32_t* hist, int tiles) {
+  const int f = blockIdx.y;
+  if (emit_skip(mb, f)) return;
+  const uint32_t hlen = hist_len_of(mb, f);
+  const int64_t t0 = (int64_t)blockIdx.x * ET;
+  if (t0 >= hlen) return;
+  __shared__ uint32_t h[64];
+  if (threadIdx.x < 64) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t i = t0 + threadIdx.x;
+  const int b = i < hlen ? e_rel(mb.lip[(int64_t)f * mb.stride + i], ninfo::RELC) : 64;
+  const unsigned m = __match_any_sync(0xffffffffu, b);
+  if (b < 64 && (int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&h[b], (uint32_t)__popc(m));
+  __syncthreads();
+  if (threadIdx.x < 64) hist[((int64_t)f * tiles + blockIdx.x) * 64 + threadIdx.x] = h[threadIdx.x];
+}
+
+// exclusive scan of the tile histograms over tiles, per bucket (in place)
+__global__ void __launch_bounds__(1024) lip_scan_kernel(MachineBufs mb, uint32_t* hist, int tiles) {
+  const int f = blockIdx.x;
+  if (emit_skip(mb, f)) return;
+  const int ntiles = (int)((hist_len_of(mb, f) + ET - 1) / ET);
+  const int v = threadIdx.x & 63, sg = threadIdx.x >> 6;  // 16 segments of tiles
+  const int per = (ntiles + 15) / 16;
+  const int tb = sg * per, te = min(ntiles, tb + per);
+  uint32_t* hf = hist + (int64_t)f * tiles * 64;
+  uint32_t sum = 0;
+  for (int t = tb; t < te; t++) sum += hf[(int64_t)t * 64 + v];
+  __shared__ uint32_t seg[16][64];
+  seg[sg][v] = sum;
+  __syncthreads();
+  uint32_t acc = 0;
+  for (int q = 0; q < sg; q++) acc += seg[q][v];
+  for (int t = tb; t < te; t++) {
+    const uint32_t x = hf[(int64_t)t * 64 + v];
+    hf[(int64_t)t * 64 + v] = acc;
+    acc += x;
+  }
+}
+
+__global__ void __launch_bounds__(ET) lip_emit_kernel(MachineBufs mb, const uint32_t* hist,
+                                                      int tiles) {
+  const int f = blockIdx.y;
+  if (emit_skip(mb, f)) return;
+  const uint32_t hlen = hist_len_of(mb, f);
+  const int64_t t0 = (int64_t)blockIdx.x * ET;
+  if (t0 >= hlen) return;
+  const int pr = mb.out[f].planes_run;
+  const int64_t fo = (int64_t)f * mb.stride;
+  __shared__ uint32_t wh[32][64];
+  __shared__ uint32_t s_start[kMaxPlaneRecs], s_lip[kMaxPlaneRecs], s_ref[kMaxPlaneRecs];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int k = tid; k < 32 * 64; k += ET) (&wh[0][0])[k] = 0;
+  if (tid < kMaxPlaneRecs) {
+    const PlaneRec& R = mb.planes[(int64_t)f * kMaxPlaneRecs + tid];
+    s_start[tid] = R.start;
+    s_lip[tid] = R.lip_len;
+    s_ref[tid] = R.refine_len;
+  }
+  const int64_t i = t0 + tid;
+  const uint64_t e = i < hlen ? mb.lip[fo + i] : 0;
+  const int b = i < hlen ? e_rel(e, ninfo::RELC) : 64;
+  const unsigned m = __match_any_sync(0xffffffffu, b);
+  __syncthreads();
+  if (b < 64 && lane == __ffs(m) - 1) wh[warp][b] = (uint32_t)__popc(m);
+  __syncthreads();
+  if (tid < 64) {  // exclusive over warps, on top of the tiles before this one
+    uint32_t acc = hist[((int64_t)f * tiles + blockIdx.x) * 64 + tid];
+    for (int w = 0; w < 32; w++) {
+      const uint32_t x = wh[w][tid];
+      wh[w][tid] = acc;
+      acc += x;
+    }
+  }
+  __syncthreads();
+  // bucket counts before this warp, and their suffix sums (relc >= v)
+  const uint32_t clo = wh[warp][lane], chi = wh[warp][lane + 32];
+  uint32_t slo = clo, shi = chi;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t yl = __shfl_down_sync(0xffffffffu, slo, o);
+    const uint32_t yh = __shfl_down_sync(0xffffffffu, shi, o);
+    if (lane + o < 32) { slo += yl; shi += yh; }
+  }
+  slo += __shfl_sync(0xffffffffu, shi, 0);
+  const int src = b & 31;
+  const uint32_t s_l = __shfl_sync(0xffffffffu, slo, src), s_h = __shfl_sync(0xffffffffu, shi, src);
+  const uint32_t c_l = __shfl_sync(0xffffffffu, clo, src), c_h = __shfl_sync(0xffffffffu, chi, src);
+  // in-warp: lanes below me with relc == b / relc >= b (bit-sliced compare)
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned eqm = 0xffffffffu, gtm = 0u;
+#pragma unroll
+  for (int k = 6; k >= 0; k--) {
+    const unsigned B = __ballot_sync(0xffffffffu, (b >> k) & 1);
+    if ((b >> k) & 1) {
+      eqm &= B;
+    } else {
+      gtm |= eqm & B;
+      eqm &= ~B;
+    }
+  }
+  if (b >= pr) return;  // never significant within the planes run (or padding)
+  const uint64_t ge = (uint64_t)(b < 32 ? s_l : s_h) + (uint32_t)__popc((gtm | eqm) & lt);
+  const uint64_t eq = (uint64_t)(b < 32 ? c_l : c_h) + (uint32_t)__popc(m & lt);
+  const uint32_t c = (uint32_t)e;
+  const int neg = e_neg(e);
+  const uint64_t sig = (uint64_t)s_start[b] + ge;
+  const uint64_t sp = (uint64_t)s_start[b] + s_lip[b] + eq;
+  const uint32_t rank = s_ref[b] + (uint32_t)eq;
+  uint32_t* bits = mb.bits + (int64_t)f * mb.bit_stride;
+  const uint64_t bit_cap = (uint64_t)mb.bit_stride * 32;
+  if (sig < bit_cap) atomicOr(bits + (sig >> 5), bit_mask_in_word(sig));
+  if (neg && sp < bit_cap) atomicOr(bits + (sp >> 5), bit_mask_in_word(sp));
+  mb.lsp[fo + rank] = c;
+  mb.lsp_rank[fo + c] = rank;
+  mb.sign_pos[fo + c] = (uint32_t)sp;
+  mb.pinfo[fo + c] = (uint8_t)((neg << 7) | b);
 }
 
 // decoder init: nothing placed yet
@@ -832,6 +1024,16 @@ void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& t
   cfg.numAttrs = 1;
   if (decode) cudaLaunchKernelEx(&cfg, machine_kernel<true>, mb, g, tt, planes);
   else cudaLaunchKernelEx(&cfg, machine_kernel<false>, mb, g, tt, planes);
+}
+
+void emit_lip(MachineBufs& mb, int planes, cudaStream_t st) {
+  (void)planes;
+  const int tiles = (int)((mb.stride + ET - 1) / ET);
+  // the wave buffers are free once the machine is done: tile histograms
+  uint32_t* hist = reinterpret_cast<uint32_t*>(mb.w0);
+  lip_hist_kernel<<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist, tiles);
+  lip_scan_kernel<<<mb.nfields, 1024, 0, st>>>(mb, hist, tiles);
+  lip_emit_kernel<<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist, tiles);
 }
 
 void write_refinement(MachineBufs& mb, int planes, cudaStream_t st) {

@@ -10,6 +10,8 @@ struct PlaneRec {
   uint32_t refine_start;  // bit offset of plane p's refinement segment
   uint32_t refine_len;    // |LSP| at the start of plane p
   uint32_t lists_end;     // |LIP| + |LIS| + |LSP| after plane p
+  uint32_t lip_len;       // |LIP| at the start of plane p (encoder)
+  uint32_t pad[3];
 };
 
 constexpr int kMaxPlaneRecs = 64;
@@ -21,7 +23,8 @@ struct MachineOut {
   uint32_t total_bits;    // bit position after the last plane
   int32_t overflow;       // list or bit-buffer capacity exceeded
   uint32_t lsp_count;     // |LSP| at the end
-  uint32_t pad[3];
+  uint32_t hist_len;      // encoder: entries ever appended to the LIP
+  uint32_t pad[2];
 };
 
 // List entries are 64-bit "node info" words carrying everything the machine
@@ -80,6 +83,9 @@ void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables& tt, cuda
 // cluster > 0 forces the CTAs per field (1..4); 0 picks by batch size
 void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& tt, int planes,
                  cudaStream_t st, int cluster = 0);
+// encoder: the deferred LIP passes (fully parallel over the LIP history);
+// must run after run_machine(decode=false) and before write_refinement
+void emit_lip(MachineBufs& mb, int planes, cudaStream_t st);
 // encoder refinement bits (fully parallel over LSP)
 void write_refinement(MachineBufs& mb, int planes, cudaStream_t st);
 // decoder: reset per-coefficient metadata before run_machine(decode=true)
