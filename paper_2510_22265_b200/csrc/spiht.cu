@@ -714,9 +714,16 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   }
 }
 
-// encoder refinement: warp per 32 consecutive LSP ranks, ballot per plane.
-// Refinement bit of plane p for rank i sits at refine_start[p] + i, for every
-// plane p after the coefficient's significance plane (i < refine_len[p]).
+// encoder refinement, word aligned.  Refinement bit of plane p for rank i
+// sits at refine_start[p] + i for every plane after the coefficient's
+// significance plane (that plane being < p is exactly i < refine_len[p]).
+// A warp walks a contiguous run of 32-rank groups: each lane aligns its
+// mantissa so bit 31-p is its plane-p bit, a 32x32 bit transpose (5 shuffle
+// stages) hands lane p the plane-p ballot of the group, and output word w of
+// plane p's segment (ranks 32w - o .. 32w - o + 31, o = refine_start[p] & 31)
+// is a funnel shift of this group's and the previous group's masks.  Lane p
+// stores plane p's word; only a segment's two edge words (shared with its
+// neighbours) need an atomic.
 __global__ void refine_write_kernel(MachineBufs mb, int planes) {
   const int f = blockIdx.y;
   if (mb.active && !mb.active[f]) return;
@@ -726,31 +733,54 @@ __global__ void refine_write_kernel(MachineBufs mb, int planes) {
   if (pr < 2) return;
   uint32_t* bits = mb.bits + (int64_t)f * mb.bit_stride;
   const int lane = threadIdx.x & 31;
-  const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t maxlen = prec[pr - 1].refine_len;  // non-decreasing in p
-  for (int64_t w = warp_global; w * 32 < (int64_t)maxlen; w += nwarps) {
-    uint32_t i = (uint32_t)(w * 32 + lane);
-    uint32_t m = 0;
-    int ps = 64;
-    if (i < maxlen) {
-      uint32_t c = mb.lsp[fo + i];
-      m = mb.mant[fo + c];
-      ps = mb.pinfo[fo + c] & 0x3f;
-    }
-    for (int p = 1; p < pr; p++) {
-      uint32_t len = prec[p].refine_len;
-      if ((uint32_t)(w * 32) >= len) continue;  // warp-uniform
-      int b = (i < len && p > ps) ? (int)((m >> (31 - (p - ps))) & 1u) : 0;
-      uint64_t q0 = (uint64_t)prec[p].refine_start + (uint64_t)w * 32;
-      uint64_t q = q0 + lane;
-      uint32_t word0 = (uint32_t)(q0 >> 5);
-      uint32_t mine = b ? bit_mask_in_word(q) : 0u;
-      bool second = ((q >> 5) != word0);
-      uint32_t v0 = __reduce_or_sync(0xffffffffu, second ? 0u : mine);
-      uint32_t v1 = __reduce_or_sync(0xffffffffu, second ? mine : 0u);
-      if (lane == 0 && v0) atomicOr(bits + word0, v0);
-      if (lane == 1 && v1) atomicOr(bits + word0 + 1, v1);
+  const uint32_t nw = maxlen / 32 + 2;
+  const uint32_t run = (nw + nwarps - 1) / nwarps;
+  const uint32_t wb = warp_global * run, we = min(nw, wb + run);
+  if (wb >= we) return;
+  for (int p0 = 0; p0 < pr; p0 += 32) {  // lane q <-> plane p0 + q
+    const int pl = p0 + lane;
+    const bool pon = pl >= 1 && pl < pr;
+    const uint32_t rs = pon ? prec[pl].refine_start : 0u;
+    const uint32_t rl = pon ? prec[pl].refine_len : 0u;
+    const int o = (int)(rs & 31u);
+    const uint32_t last = rl ? (uint32_t)(((uint64_t)rs + rl - 1) >> 5) : 0xffffffffu;
+    auto group = [&](uint32_t g) -> uint32_t {
+      const uint32_t i = g * 32 + lane;
+      uint32_t a = 0;
+      if (i < maxlen) {
+        const uint32_t c = mb.lsp[fo + i];
+        const uint32_t m = mb.mant[fo + c];
+        const int d = p0 - (mb.pinfo[fo + c] & 0x3f);
+        // bit 31-q of a = plane (p0+q) bit = m bit 31-(p0+q-ps), for p0+q > ps
+        if (d <= 0) a = -d < 31 ? (m >> -d) & ((1u << (31 + d)) - 1u) : 0u;
+        else a = d < 32 ? m << d : 0u;
+      }
+      uint32_t x = __brev(a);  // bit q <-> plane p0 + q
+      // 32x32 transpose: lane q ends with bit l = lane l's bit q
+#pragma unroll
+      for (int j = 16; j >= 1; j >>= 1) {
+        const uint32_t lo = j == 16 ? 0x0000ffffu : j == 8 ? 0x00ff00ffu : j == 4 ? 0x0f0f0f0fu
+                          : j == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        x = (lane & j) ? ((x & ~lo) | ((y & ~lo) >> j)) : ((x & lo) | ((y & lo) << j));
+      }
+      return x;
+    };
+    uint32_t prev = wb > 0 ? group(wb - 1) : 0u;
+    for (uint32_t w = wb; w < we; w++) {
+      const uint32_t cur = group(w);
+      // lane-order mask of output word w: bit q <-> rank 32w - o + q
+      const uint32_t lm = o ? __funnelshift_l(prev, cur, o) : cur;
+      prev = cur;
+      if (pon && lm) {
+        const uint32_t v = __byte_perm(__brev(lm), 0, 0x0123);
+        const uint32_t wd = (rs >> 5) + w;
+        if (w == 0 || wd == last) atomicOr(bits + wd, v);
+        else bits[wd] = v;
+      }
     }
   }
 }
@@ -794,7 +824,10 @@ __global__ void refine_gather_kernel(MachineBufs mb) {
 // (spiht.py's LIP pass, every plane at once): two rank-by-value counts over
 // 64 relc buckets, from tile histograms, per-warp histograms and a bit-sliced
 // in-warp compare.
-constexpr int ET = 1024;  // LIP-history entries per emit tile (one per thread)
+constexpr int ET = 1024;        // emit threads per CTA
+constexpr int EPT = 4;          // entries per thread
+constexpr int ETILE = ET * EPT; // LIP-history entries per tile
+constexpr int EVW = ETILE / 32; // 32-entry groups ("virtual warps") per tile
 
 __device__ __forceinline__ bool emit_skip(const MachineBufs& mb, int f) {
   return (mb.active && !mb.active[f]) || mb.out[f].overflow;
@@ -805,19 +838,33 @@ __device__ __forceinline__ uint32_t hist_len_of(const MachineBufs& mb, int f) {
   return (int64_t)h < mb.stride ? h : (uint32_t)mb.stride;
 }
 
+// entry k of thread tid in a tile: sub-tile k, 32-entry group k*32 + warp
+__device__ __forceinline__ int64_t emit_index(int64_t t0, int k) {
+  return t0 + (int64_t)k * ET + threadIdx.x;
+}
+
 __global__ void __launch_bounds__(ET) lip_hist_kernel(MachineBufs mb, uint32_t* hist, int tiles) {
   const int f = blockIdx.y;
   if (emit_skip(mb, f)) return;
   const uint32_t hlen = hist_len_of(mb, f);
-  const int64_t t0 = (int64_t)blockIdx.x * ET;
+  const int64_t t0 = (int64_t)blockIdx.x * ETILE;
   if (t0 >= hlen) return;
   __shared__ uint32_t h[64];
   if (threadIdx.x < 64) h[threadIdx.x] = 0;
+  const uint64_t* lip = mb.lip + (int64_t)f * mb.stride;
+  int bk[EPT];
+#pragma unroll
+  for (int k = 0; k < EPT; k++) {
+    const int64_t i = emit_index(t0, k);
+    bk[k] = i < hlen ? e_rel(lip[i], ninfo::RELC) : 64;
+  }
   __syncthreads();
-  const int64_t i = t0 + threadIdx.x;
-  const int b = i < hlen ? e_rel(mb.lip[(int64_t)f * mb.stride + i], ninfo::RELC) : 64;
-  const unsigned m = __match_any_sync(0xffffffffu, b);
-  if (b < 64 && (int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&h[b], (uint32_t)__popc(m));
+#pragma unroll
+  for (int k = 0; k < EPT; k++) {
+    const unsigned m = __match_any_sync(0xffffffffu, bk[k]);
+    if (bk[k] < 64 && (int)(threadIdx.x & 31) == __ffs(m) - 1)
+      atomicAdd(&h[bk[k]], (uint32_t)__popc(m));
+  }
   __syncthreads();
   if (threadIdx.x < 64) hist[((int64_t)f * tiles + blockIdx.x) * 64 + threadIdx.x] = h[threadIdx.x];
 }
@@ -826,7 +873,7 @@ __global__ void __launch_bounds__(ET) lip_hist_kernel(MachineBufs mb, uint32_t* 
 __global__ void __launch_bounds__(1024) lip_scan_kernel(MachineBufs mb, uint32_t* hist, int tiles) {
   const int f = blockIdx.x;
   if (emit_skip(mb, f)) return;
-  const int ntiles = (int)((hist_len_of(mb, f) + ET - 1) / ET);
+  const int ntiles = (int)((hist_len_of(mb, f) + ETILE - 1) / ETILE);
   const int v = threadIdx.x & 63, sg = threadIdx.x >> 6;  // 16 segments of tiles
   const int per = (ntiles + 15) / 16;
   const int tb = sg * per, te = min(ntiles, tb + per);
@@ -850,78 +897,130 @@ __global__ void __launch_bounds__(ET) lip_emit_kernel(MachineBufs mb, const uint
   const int f = blockIdx.y;
   if (emit_skip(mb, f)) return;
   const uint32_t hlen = hist_len_of(mb, f);
-  const int64_t t0 = (int64_t)blockIdx.x * ET;
+  const int64_t t0 = (int64_t)blockIdx.x * ETILE;
   if (t0 >= hlen) return;
   const int pr = mb.out[f].planes_run;
   const int64_t fo = (int64_t)f * mb.stride;
-  __shared__ uint32_t wh[32][64];
+  __shared__ uint32_t wh[64][EVW + 1];  // [bucket][32-entry group], padded
   __shared__ uint32_t s_start[kMaxPlaneRecs], s_lip[kMaxPlaneRecs], s_ref[kMaxPlaneRecs];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int k = tid; k < 32 * 64; k += ET) (&wh[0][0])[k] = 0;
+  for (int k = tid; k < 64 * (EVW + 1); k += ET) (&wh[0][0])[k] = 0;
   if (tid < kMaxPlaneRecs) {
     const PlaneRec& R = mb.planes[(int64_t)f * kMaxPlaneRecs + tid];
     s_start[tid] = R.start;
     s_lip[tid] = R.lip_len;
     s_ref[tid] = R.refine_len;
   }
-  const int64_t i = t0 + tid;
-  const uint64_t e = i < hlen ? mb.lip[fo + i] : 0;
-  const int b = i < hlen ? e_rel(e, ninfo::RELC) : 64;
-  const unsigned m = __match_any_sync(0xffffffffu, b);
+  uint64_t ent[EPT];
+  int bk[EPT];
+  unsigned mk[EPT];
+#pragma unroll
+  for (int k = 0; k < EPT; k++) {
+    const int64_t i = emit_index(t0, k);
+    ent[k] = i < hlen ? mb.lip[fo + i] : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < EPT; k++) {
+    const int64_t i = emit_index(t0, k);
+    bk[k] = i < hlen ? e_rel(ent[k], ninfo::RELC) : 64;
+    mk[k] = __match_any_sync(0xffffffffu, bk[k]);
+  }
   __syncthreads();
-  if (b < 64 && lane == __ffs(m) - 1) wh[warp][b] = (uint32_t)__popc(m);
+#pragma unroll
+  for (int k = 0; k < EPT; k++)
+    if (bk[k] < 64 && lane == __ffs(mk[k]) - 1) wh[bk[k]][k * 32 + warp] = (uint32_t)__popc(mk[k]);
   __syncthreads();
-  if (tid < 64) {  // exclusive over warps, on top of the tiles before this one
-    uint32_t acc = hist[((int64_t)f * tiles + blockIdx.x) * 64 + tid];
-    for (int w = 0; w < 32; w++) {
-      const uint32_t x = wh[w][tid];
-      wh[w][tid] = acc;
-      acc += x;
+  {  // exclusive over the groups (lane l owns groups EPT*l ..), on top of earlier tiles
+    const uint32_t* tp = hist + ((int64_t)f * tiles + blockIdx.x) * 64;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int v = warp + 32 * h;
+      uint32_t x[EPT], loc = 0;
+#pragma unroll
+      for (int j = 0; j < EPT; j++) { x[j] = wh[v][EPT * lane + j]; loc += x[j]; }
+      uint32_t y = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += z;
+      }
+      uint32_t run = tp[v] + y - loc;
+#pragma unroll
+      for (int j = 0; j < EPT; j++) { wh[v][EPT * lane + j] = run; run += x[j]; }
     }
   }
   __syncthreads();
-  // bucket counts before this warp, and their suffix sums (relc >= v)
-  const uint32_t clo = wh[warp][lane], chi = wh[warp][lane + 32];
-  uint32_t slo = clo, shi = chi;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t yl = __shfl_down_sync(0xffffffffu, slo, o);
-    const uint32_t yh = __shfl_down_sync(0xffffffffu, shi, o);
-    if (lane + o < 32) { slo += yl; shi += yh; }
-  }
-  slo += __shfl_sync(0xffffffffu, shi, 0);
-  const int src = b & 31;
-  const uint32_t s_l = __shfl_sync(0xffffffffu, slo, src), s_h = __shfl_sync(0xffffffffu, shi, src);
-  const uint32_t c_l = __shfl_sync(0xffffffffu, clo, src), c_h = __shfl_sync(0xffffffffu, chi, src);
-  // in-warp: lanes below me with relc == b / relc >= b (bit-sliced compare)
-  const unsigned lt = (1u << lane) - 1u;
-  unsigned eqm = 0xffffffffu, gtm = 0u;
-#pragma unroll
-  for (int k = 6; k >= 0; k--) {
-    const unsigned B = __ballot_sync(0xffffffffu, (b >> k) & 1);
-    if ((b >> k) & 1) {
-      eqm &= B;
-    } else {
-      gtm |= eqm & B;
-      eqm &= ~B;
-    }
-  }
-  if (b >= pr) return;  // never significant within the planes run (or padding)
-  const uint64_t ge = (uint64_t)(b < 32 ? s_l : s_h) + (uint32_t)__popc((gtm | eqm) & lt);
-  const uint64_t eq = (uint64_t)(b < 32 ? c_l : c_h) + (uint32_t)__popc(m & lt);
-  const uint32_t c = (uint32_t)e;
-  const int neg = e_neg(e);
-  const uint64_t sig = (uint64_t)s_start[b] + ge;
-  const uint64_t sp = (uint64_t)s_start[b] + s_lip[b] + eq;
-  const uint32_t rank = s_ref[b] + (uint32_t)eq;
   uint32_t* bits = mb.bits + (int64_t)f * mb.bit_stride;
   const uint64_t bit_cap = (uint64_t)mb.bit_stride * 32;
-  if (sig < bit_cap) atomicOr(bits + (sig >> 5), bit_mask_in_word(sig));
-  if (neg && sp < bit_cap) atomicOr(bits + (sp >> 5), bit_mask_in_word(sp));
-  mb.lsp[fo + rank] = c;
-  mb.lsp_rank[fo + c] = rank;
-  mb.sign_pos[fo + c] = (uint32_t)sp;
-  mb.pinfo[fo + c] = (uint8_t)((neg << 7) | b);
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int k = 0; k < EPT; k++) {
+    const int b = bk[k];
+    if (__all_sync(0xffffffffu, b >= pr)) continue;
+    // bucket counts before this group, and their suffix sums (relc >= v)
+    const int gi = k * 32 + warp;
+    const uint32_t clo = wh[lane][gi], chi = wh[lane + 32][gi];
+    uint32_t slo = clo, shi = chi;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t yl = __shfl_down_sync(0xffffffffu, slo, o);
+      const uint32_t yh = __shfl_down_sync(0xffffffffu, shi, o);
+      if (lane + o < 32) { slo += yl; shi += yh; }
+    }
+    slo += __shfl_sync(0xffffffffu, shi, 0);
+    const int src = b & 31;
+    const uint32_t s_l = __shfl_sync(0xffffffffu, slo, src), s_h = __shfl_sync(0xffffffffu, shi, src);
+    const uint32_t c_l = __shfl_sync(0xffffffffu, clo, src), c_h = __shfl_sync(0xffffffffu, chi, src);
+    // in-group: lanes below me with relc == b / relc >= b (bit-sliced compare)
+    unsigned eqm = 0xffffffffu, gtm = 0u;
+#pragma unroll
+    for (int q = 6; q >= 0; q--) {
+      const unsigned B = __ballot_sync(0xffffffffu, (b >> q) & 1);
+      if ((b >> q) & 1) {
+        eqm &= B;
+      } else {
+        gtm |= eqm & B;
+        eqm &= ~B;
+      }
+    }
+    const bool on = b < pr;  // significant within the planes run (padding: b = 64)
+    const uint64_t ge = (uint64_t)(b < 32 ? s_l : s_h) + (uint32_t)__popc((gtm | eqm) & lt);
+    const uint64_t eq = (uint64_t)(b < 32 ? c_l : c_h) + (uint32_t)__popc(mk[k] & lt);
+    const int neg = e_neg(ent[k]);
+    const uint64_t sig = on ? (uint64_t)s_start[b] + ge : ~0ull;
+    const uint64_t sp = on ? (uint64_t)s_start[b] + s_lip[b] + eq : ~0ull;
+    // one atomic per distinct word per group
+    {
+      const uint32_t wd = on ? (uint32_t)(sig >> 5) : 0xffffffffu;
+      const unsigned g = __match_any_sync(0xffffffffu, wd);
+      const uint32_t v = __reduce_or_sync(g, on ? bit_mask_in_word(sig) : 0u);
+      if (on && lane == __ffs(g) - 1 && sig < bit_cap) atomicOr(bits + wd, v);
+    }
+    {
+      const bool sn = on && neg;
+      const uint32_t wd = sn ? (uint32_t)(sp >> 5) : 0xffffffffu;
+      const unsigned g = __match_any_sync(0xffffffffu, wd);
+      const uint32_t v = __reduce_or_sync(g, sn ? bit_mask_in_word(sp) : 0u);
+      if (sn && lane == __ffs(g) - 1 && sp < bit_cap) atomicOr(bits + wd, v);
+    }
+    if (on) {
+      const uint32_t c = (uint32_t)ent[k];
+      const uint32_t rank = s_ref[b] + (uint32_t)eq;
+      mb.lsp[fo + rank] = c;
+      mb.lsp_rank[fo + c] = rank;
+      mb.sign_pos[fo + c] = (uint32_t)sp;
+      mb.pinfo[fo + c] = (uint8_t)((neg << 7) | b);
+    }
+  }
+}
+
+void emit_lip_host(MachineBufs& mb, cudaStream_t st) {
+  const int tiles = (int)((mb.stride + ETILE - 1) / ETILE);
+  // the wave buffers are free once the machine is done: tile histograms
+  uint32_t* hist = reinterpret_cast<uint32_t*>(mb.w0);
+  lip_hist_kernel<<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist, tiles);
+  lip_scan_kernel<<<mb.nfields, 1024, 0, st>>>(mb, hist, tiles);
+  lip_emit_kernel<<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist, tiles);
 }
 
 // decoder init: nothing placed yet
@@ -1028,12 +1127,7 @@ void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& t
 
 void emit_lip(MachineBufs& mb, int planes, cudaStream_t st) {
   (void)planes;
-  const int tiles = (int)((mb.stride + ET - 1) / ET);
-  // the wave buffers are free once the machine is done: tile histograms
-  uint32_t* hist = reinterpret_cast<uint32_t*>(mb.w0);
-  lip_hist_kernel<<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist, tiles);
-  lip_scan_kernel<<<mb.nfields, 1024, 0, st>>>(mb, hist, tiles);
-  lip_emit_kernel<<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist, tiles);
+  emit_lip_host(mb, st);
 }
 
 void write_refinement(MachineBufs& mb, int planes, cudaStream_t st) {
