@@ -1,3 +1,4 @@
+#include <algorithm>
 // Field-level kernels of the EBCC path: the closed-form prefix decode and the
 // feedback probes built on the lifting passes.
 //
@@ -263,10 +264,11 @@ __global__ void fill_kernel(const FieldScal* fs, const uint8_t* active, int64_t 
 
 // one CTA per part; bytes are MSB-first stream bytes = little-endian words
 __global__ void pack_kernel(const PackPart* parts, uint8_t* out) {
-  const PackPart P = parts[blockIdx.x];
+  const PackPart P = parts[blockIdx.y];
   uint8_t* d = out + P.dst_off;
   const uint8_t* s = reinterpret_cast<const uint8_t*>(P.src);
-  for (uint64_t i = threadIdx.x; i < P.nbytes; i += blockDim.x) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.nbytes;
+       i += (uint64_t)gridDim.x * blockDim.x) {
     uint8_t v;
     if (i < (uint64_t)kHeader) {
       v = P.hdr[i];
@@ -284,10 +286,11 @@ __global__ void pack_kernel(const PackPart* parts, uint8_t* out) {
 }
 
 __global__ void unpack_kernel(const UnpackPart* parts, const uint8_t* in) {
-  const UnpackPart P = parts[blockIdx.x];
+  const UnpackPart P = parts[blockIdx.y];
   uint8_t* d = reinterpret_cast<uint8_t*>(P.dst);
   uint64_t padded = (P.nbytes + 7) & ~7ull;
-  for (uint64_t i = threadIdx.x; i < padded; i += blockDim.x)
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < padded;
+       i += (uint64_t)gridDim.x * blockDim.x)
     d[i] = i < P.nbytes ? in[P.src_off + i] : 0;
 }
 
@@ -397,11 +400,13 @@ void fill_constant(const FieldScal* fs, const uint8_t* active, int64_t n, int nf
 }
 
 void pack_parts(const PackPart* parts, int nparts, uint8_t* out, cudaStream_t st) {
-  if (nparts) pack_kernel<<<nparts, 256, 0, st>>>(parts, out);
+  for (int b = 0; b < nparts; b += 65535)
+    pack_kernel<<<dim3(64, std::min(65535, nparts - b)), 256, 0, st>>>(parts + b, out);
 }
 
 void unpack_parts(const UnpackPart* parts, int nparts, const uint8_t* in, cudaStream_t st) {
-  if (nparts) unpack_kernel<<<nparts, 256, 0, st>>>(parts, in);
+  for (int b = 0; b < nparts; b += 65535)
+    unpack_kernel<<<dim3(64, std::min(65535, nparts - b)), 256, 0, st>>>(parts + b, in);
 }
 
 }  // namespace ebcc
