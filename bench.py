@@ -204,7 +204,12 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e: the public API with host buffers, H2D + D2H inside ----
     e2e_t = e2e_c = 0.0
     e2e_steps = max(1, min(args.steps, 3))
-    blob = None
+    # untimed warm-up of the public path (host staging / page-locked result
+    # blocks are allocated on first use)
+    # (two results alive at once, as in the timed loop below)
+    blob = ebcc.compress(pinned.numpy(), rel_error=EPS, q=Q)
+    warm = [ebcc.decompress(blob), ebcc.decompress(blob)]
+    del warm
     for _ in range(e2e_steps):
         flush.zero_()
         torch.cuda.synchronize()

@@ -92,6 +92,21 @@ int ebcc_compress(ebcc_ctx *ctx, const float *fields, int64_t nfields, int32_t r
 /* Copy the payload of the last ebcc_compress call. */
 int ebcc_fetch_payload(ebcc_ctx *ctx, uint8_t *payload, int64_t payload_cap, int32_t flags);
 
+/* Write the reference container image of the last ebcc_compress call
+ * (container.py:44-73 write_file): the caller's 42-byte file header, then per
+ * chunk its caller-built 25-byte record followed by its payload.  Assembled
+ * on the device, then one device->host (or device->device) copy into `out`.
+ * out_len receives 42 + 25 * nchunks + payload_total. */
+int ebcc_fetch_container(ebcc_ctx *ctx, const uint8_t *header42, const uint8_t *records25,
+                         int64_t nchunks, uint8_t *out, int64_t cap, int32_t flags,
+                         int64_t *out_len);
+
+/* Page-locked host blocks for result arrays, from a per-process cache so that
+ * repeated calls do not pay cudaHostAlloc.  Device->host copies into them run
+ * at full PCIe/C2C speed without a staging hop. */
+int ebcc_host_alloc(int64_t bytes, void **out);
+int ebcc_host_free(void *ptr);
+
 /* Decompress `nfields` same-shape chunks.  recs[i].mode/vmin/vmax/base_len/
  * resid_len come from the container; chunk i's payload starts at
  * payload + payload_offsets[i].  `levels` is the level count stored in the

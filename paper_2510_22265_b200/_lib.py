@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 
 import numpy as np
 
@@ -28,7 +29,7 @@ OUTPUT_ON_DEVICE = 2
 EXPORTS = ("ebcc_abi_version", "ebcc_create", "ebcc_destroy", "ebcc_set_stream",
            "ebcc_last_error", "ebcc_last_error_index", "ebcc_compress", "ebcc_fetch_payload", "ebcc_decompress",
            "ebcc_get_stats", "ebcc_dwt", "ebcc_spiht_encode", "ebcc_spiht_decode",
-           "ebcc_selftest_div")
+           "ebcc_selftest_div", "ebcc_fetch_container", "ebcc_host_alloc", "ebcc_host_free")
 
 
 class ChunkRec(ctypes.Structure):
@@ -87,8 +88,50 @@ def load(path: str = LIB_PATH):
         L.ebcc_spiht_encode.argtypes = [P, P, i32, i32, i32, i32, P, i64, ctypes.POINTER(i64)]
         L.ebcc_spiht_decode.argtypes = [P, P, i64, i64, i32, i32, P, ctypes.POINTER(i32)]
         L.ebcc_selftest_div.argtypes = [P, i64, ctypes.c_uint64, ctypes.POINTER(i64)]
+        L.ebcc_fetch_container.argtypes = [P, P, P, i64, P, i64, i32, ctypes.POINTER(i64)]
+        L.ebcc_host_alloc.argtypes = [i64, ctypes.POINTER(P)]
+        L.ebcc_host_free.argtypes = [P]
         _lib = L
         return L
+
+
+_PyBytes_FromStringAndSize = ctypes.pythonapi.PyBytes_FromStringAndSize
+_PyBytes_FromStringAndSize.argtypes = [ctypes.c_void_p, ctypes.c_ssize_t]
+_PyBytes_FromStringAndSize.restype = ctypes.py_object
+_PyBytes_AsString = ctypes.pythonapi.PyBytes_AsString
+_PyBytes_AsString.argtypes = [ctypes.py_object]
+_PyBytes_AsString.restype = ctypes.c_void_p
+
+
+def _new_bytes(n: int) -> bytes:
+    """A fresh, not yet shared bytes object of length n (filled by the caller
+    before it is handed out, as the C API allows)."""
+    return _PyBytes_FromStringAndSize(None, n)
+
+
+def _bytes_ptr(b: bytes) -> int:
+    return _PyBytes_AsString(b)
+
+
+PINNED_MIN_BYTES = 4 << 20
+
+
+def host_empty(shape, dtype) -> np.ndarray:
+    """Uninitialised host array; large ones live in page-locked blocks from the
+    library's cache (returned to it when the array is garbage collected), so
+    the device->host copy of a result lands without a staging hop."""
+    dtype = np.dtype(dtype)
+    count = int(np.prod(shape, dtype=np.int64))
+    nbytes = count * dtype.itemsize
+    if nbytes < PINNED_MIN_BYTES:
+        return np.empty(shape, dtype)
+    lib = load()
+    ptr = ctypes.c_void_p()
+    if lib.ebcc_host_alloc(nbytes, ctypes.byref(ptr)) != OK or not ptr.value:
+        raise DeviceError(f"cannot allocate {nbytes} page-locked bytes")
+    buf = (ctypes.c_char * nbytes).from_address(ptr.value)
+    weakref.finalize(buf, lib.ebcc_host_free, ctypes.c_void_p(ptr.value))
+    return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
 
 
 class Context:
@@ -176,6 +219,21 @@ class Context:
     def fetch_payload_ptr(self, ptr: int, cap: int, flags: int):
         st = self.lib.ebcc_fetch_payload(self.handle, ctypes.c_void_p(ptr), cap, flags)
         self.raise_for(st, "ebcc_fetch_payload")
+
+    def fetch_container(self, header: bytes, records: np.ndarray, payload_total: int) -> bytes:
+        """The container bytes of the last compress: ``header`` (42 B) and the
+        25-byte ``records`` (RECORD_DTYPE) interleaved with the payloads on the
+        device, copied once into a fresh ``bytes`` object."""
+        recs = np.ascontiguousarray(records)
+        n = len(recs)
+        size = 42 + 25 * n + int(payload_total)
+        out = _new_bytes(size)
+        got = ctypes.c_int64(0)
+        st = self.lib.ebcc_fetch_container(self.handle, header, recs.ctypes.data if n else None,
+                                           n, ctypes.c_void_p(_bytes_ptr(out)), size, 0,
+                                           ctypes.byref(got))
+        self.raise_for(st, "ebcc_fetch_container")
+        return out
 
     # -- decompress ----------------------------------------------------------
     def decompress(self, payload, offsets: np.ndarray, recs: np.ndarray, rows: int, cols: int,

@@ -25,6 +25,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -335,6 +337,10 @@ struct ebcc_ctx {
   int64_t stage_cap = 0;
   float* d_out = nullptr;
   int64_t out_cap = 0;
+  uint8_t* d_cont = nullptr;      // container image (ebcc_fetch_container)
+  int64_t cont_cap = 0;
+  uint8_t* d_cmeta = nullptr;     // its records + parts
+  int64_t cmeta_cap = 0;
   ebcc_stats stats{};
   fused::Level0Timer l0;
   cudaStream_t side = nullptr;   // high-priority stream for the overlapped residual encode
@@ -986,6 +992,8 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->d_stage) cudaFree(c->d_stage);
   if (c->d_out) cudaFree(c->d_out);
   if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->d_cont) cudaFree(c->d_cont);
+  if (c->d_cmeta) cudaFree(c->d_cmeta);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (c->l0.a) cudaEventDestroy(c->l0.a);
   if (c->l0.b) cudaEventDestroy(c->l0.b);
@@ -1289,6 +1297,70 @@ int ebcc_fetch_payload(ebcc_ctx* c, uint8_t* payload, int64_t cap, int32_t flags
                                   c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   return e == cudaSuccess ? EBCC_OK : fail(c, EBCC_E_CUDA, cudaGetErrorString(e));
+}
+
+int ebcc_fetch_container(ebcc_ctx* c, const uint8_t* header42, const uint8_t* records25,
+                         int64_t n, uint8_t* out, int64_t cap, int32_t flags, int64_t* out_len) {
+  if (!c || !header42 || !out || n < 0 || (n && !records25)) return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  const int64_t total = 42 + 25 * n + c->payload_total;
+  if (out_len) *out_len = total;
+  if (cap < total) return fail(c, EBCC_E_CAPACITY, "container buffer too small");
+  std::vector<ContainerPart> parts((size_t)n);
+  int64_t src = 0, dst = 42;
+  for (int64_t i = 0; i < n; i++) {
+    uint32_t bl, rl;
+    memcpy(&bl, records25 + 25 * i + 17, 4);
+    memcpy(&rl, records25 + 25 * i + 21, 4);
+    parts[i] = ContainerPart{src, dst, (int64_t)bl + rl};
+    src += (int64_t)bl + rl;
+    dst += 25 + (int64_t)bl + rl;
+  }
+  if (src != c->payload_total)
+    return fail(c, EBCC_E_ARGUMENT, "records do not match the last compress call's payload");
+  try {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    if (total > c->cont_cap) {
+      if (c->d_cont) CK(cudaFree(c->d_cont));
+      c->d_cont = nullptr;
+      c->cont_cap = 0;
+      c->d_cont = dalloc<uint8_t>((size_t)total);
+      c->cont_cap = total;
+    }
+    const int64_t mb = (int64_t)sizeof(ContainerPart) * n + 25 * n + 16;
+    if (mb > c->cmeta_cap) {
+      if (c->d_cmeta) CK(cudaFree(c->d_cmeta));
+      c->d_cmeta = nullptr;
+      c->cmeta_cap = 0;
+      c->d_cmeta = dalloc<uint8_t>((size_t)mb);
+      c->cmeta_cap = mb;
+    }
+    ContainerPart* d_parts = reinterpret_cast<ContainerPart*>(c->d_cmeta);
+    uint8_t* d_recs = c->d_cmeta + sizeof(ContainerPart) * n;
+    CK(cudaMemcpyAsync(c->d_cont, header42, 42, cudaMemcpyHostToDevice, st));
+    if (n) {
+      CK(cudaMemcpyAsync(d_parts, parts.data(), sizeof(ContainerPart) * n, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(d_recs, records25, 25 * n, cudaMemcpyHostToDevice, st));
+      assemble_container(d_parts, (int)n, d_recs, c->d_payload, c->d_cont, st);
+      CK(cudaGetLastError());
+    }
+    if (flags & EBCC_OUTPUT_ON_DEVICE) {
+      CK(cudaMemcpyAsync(out, c->d_cont, total, cudaMemcpyDeviceToDevice, st));
+    } else if (is_pageable(out)) {
+      uint8_t* stg = host_stage(c, total);
+      CK(cudaMemcpyAsync(stg, c->d_cont, total, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      parallel_memcpy(out, stg, (size_t)total);
+    } else {
+      CK(cudaMemcpyAsync(out, c->d_cont, total, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    return EBCC_OK;
+  } catch (CudaFail& e) {
+    cudaGetLastError();
+    return fail(c, e.e == cudaErrorMemoryAllocation ? EBCC_E_NOMEM : EBCC_E_CUDA,
+                std::string(e.what) + ": " + cudaGetErrorString(e.e));
+  }
 }
 
 int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
@@ -1597,6 +1669,68 @@ int ebcc_spiht_decode(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t pre
     cudaGetLastError();
     return fail(c, EBCC_E_CUDA, std::string(e.what) + ": " + cudaGetErrorString(e.e));
   }
+}
+
+// page-locked result blocks: size-keyed free list, bounded cache
+namespace {
+std::mutex g_pin_mu;
+std::multimap<int64_t, void*> g_pin_free;
+std::unordered_map<void*, int64_t> g_pin_size;
+int64_t g_pin_cached = 0;
+constexpr int64_t kPinCacheMax = 8ll << 30;
+
+void pin_release_cached_locked() {
+  for (auto& kv : g_pin_free) {
+    g_pin_size.erase(kv.second);
+    cudaFreeHost(kv.second);
+  }
+  g_pin_free.clear();
+  g_pin_cached = 0;
+}
+}  // namespace
+
+int ebcc_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return EBCC_E_ARGUMENT;
+  if (bytes == 0) bytes = 1;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  auto it = g_pin_free.lower_bound(bytes);
+  if (it != g_pin_free.end() && it->first <= 2 * bytes) {
+    *out = it->second;
+    g_pin_cached -= it->first;
+    g_pin_free.erase(it);
+    return EBCC_OK;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    pin_release_cached_locked();
+    e = cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return EBCC_E_NOMEM;
+    }
+  }
+  g_pin_size[p] = bytes;
+  *out = p;
+  return EBCC_OK;
+}
+
+int ebcc_host_free(void* p) {
+  if (!p) return EBCC_OK;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  auto it = g_pin_size.find(p);
+  if (it == g_pin_size.end()) return EBCC_E_ARGUMENT;
+  g_pin_free.insert({it->second, p});
+  g_pin_cached += it->second;
+  while (g_pin_cached > kPinCacheMax && !g_pin_free.empty()) {
+    auto v = g_pin_free.begin();  // smallest first
+    g_pin_cached -= v->first;
+    g_pin_size.erase(v->second);
+    cudaFreeHost(v->second);
+    g_pin_free.erase(v);
+  }
+  return EBCC_OK;
 }
 
 int ebcc_selftest_div(ebcc_ctx* c, int64_t n, uint64_t seed, int64_t* mismatches) {

@@ -294,7 +294,26 @@ __global__ void unpack_kernel(const UnpackPart* parts, const uint8_t* in) {
     d[i] = i < P.nbytes ? in[P.src_off + i] : 0;
 }
 
+// container image: chunk i's record (25 bytes) then its payload
+__global__ void container_kernel(const ContainerPart* parts, const uint8_t* records,
+                                 const uint8_t* payload, uint8_t* out) {
+  const int i = blockIdx.y;
+  const ContainerPart P = parts[i];
+  uint8_t* d = out + P.dst_off;
+  const uint8_t* s = payload + P.src_off;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < P.len + 25;
+       k += (int64_t)gridDim.x * blockDim.x)
+    d[k] = k < 25 ? records[(int64_t)i * 25 + k] : s[k - 25];
+}
+
 }  // namespace
+
+void assemble_container(const ContainerPart* parts, int nparts, const uint8_t* records,
+                        const uint8_t* payload, uint8_t* out, cudaStream_t st) {
+  for (int b = 0; b < nparts; b += 65535)
+    container_kernel<<<dim3(64, std::min(65535, nparts - b)), 256, 0, st>>>(
+        parts + b, records + (int64_t)b * 25, payload, out);
+}
 
 void ingest_normalize(const float* x, int64_t n, int nfields, double* norm, FieldScal* fs,
                       unsigned int* mm, double eps_rel, cudaStream_t st) {

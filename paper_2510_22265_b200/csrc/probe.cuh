@@ -104,4 +104,14 @@ struct UnpackPart {
 };
 void unpack_parts(const UnpackPart* parts, int nparts, const uint8_t* in, cudaStream_t st);
 
+// container image (container.py:44-73): record i (25 B, records + 25 i) at
+// dst_off, its payload (len bytes at payload + src_off) right after
+struct ContainerPart {
+  int64_t src_off;
+  int64_t dst_off;
+  int64_t len;
+};
+void assemble_container(const ContainerPart* parts, int nparts, const uint8_t* records,
+                        const uint8_t* payload, uint8_t* out, cudaStream_t st);
+
 }  // namespace ebcc

@@ -46,12 +46,14 @@ def default_levels(rows: int, cols: int) -> int:
 # ---------------------------------------------------------------------------
 # batched device calls
 
-def compress_batch(stack: np.ndarray, params: EbccParams, ctx=None):
+def compress_batch(stack: np.ndarray, params: EbccParams, ctx=None, fetch: bool = True):
     """Compress a (n, rows, cols) float32 stack of chunks on the device.
 
     Returns (records[REC_DTYPE], offsets int64[n], payload uint8[total],
     status).  Raises ArgumentError for bad params; per-chunk
     ResidualInsufficient is reported through records['status'] and status.
+    With ``fetch=False`` the payload stays on the device (payload is the int
+    total) for :meth:`_lib.Context.fetch_container`.
     """
     ctx = ctx or _lib.context()
     stack = np.ascontiguousarray(stack, dtype=np.float32)
@@ -60,6 +62,8 @@ def compress_batch(stack: np.ndarray, params: EbccParams, ctx=None):
                                          params.r0, params.search_tol)
     if st not in (_lib.OK, _lib.E_RESIDUAL):
         ctx.raise_for(st, "ebcc_compress")
+    if not fetch:
+        return recs, offs, total, st
     payload = np.empty(max(total, 1), dtype=np.uint8)
     if st == _lib.OK and total:
         ctx.fetch_payload(payload)
@@ -237,7 +241,8 @@ def decompress_grid(chunks, dims, chunk_shape=None, ctx=None) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # container-level fast paths used by api.compress / api.decompress
 
-def grid_to_records(grid: GridArray, params: EbccParams, ctx=None, orig_shape=None):
+def grid_to_records(grid: GridArray, params: EbccParams, ctx=None, orig_shape=None,
+                    container: bool = False):
     """Compress a grid straight to (records[RECORD_DTYPE], payload, offsets).
 
     Default chunking (one 2D slice per (t, p)) is fed to the device without a
@@ -245,6 +250,8 @@ def grid_to_records(grid: GridArray, params: EbccParams, ctx=None, orig_shape=No
     as IngestError with the index in ``orig_shape``, the caller's array
     shape).  Error semantics and their order equal the reference's
     (ingest before parameter validation, core.py:89-105 / pipeline.py:54).
+    With ``container=True`` the result is the container bytes, assembled on
+    the device for default chunking.
     """
     t, p, h, w = grid.dims
     shape = tuple(orig_shape) if orig_shape is not None else tuple(grid.dims)
@@ -257,8 +264,9 @@ def grid_to_records(grid: GridArray, params: EbccParams, ctx=None, orig_shape=No
             _require_finite(grid.data.reshape(shape))
             raise _chunk_error(origins[0], exc)
         stack = grid.data.reshape(t * p, h, w)
+        ctx = ctx or _lib.context()
         try:
-            recs, offs, payload, st = compress_batch(stack, params, ctx)
+            recs, offs, payload, st = compress_batch(stack, params, ctx, fetch=not container)
         except IngestError as exc:
             at = tuple(int(i) for i in np.unravel_index(int(exc.index), shape))
             raise IngestError(f"non-finite value at index {at}", index=at) from None
@@ -274,6 +282,10 @@ def grid_to_records(grid: GridArray, params: EbccParams, ctx=None, orig_shape=No
         out["vmax"] = recs["vmax"]
         out["base_len"] = recs["base_len"]
         out["resid_len"] = recs["resid_len"]
+        if container:
+            from .container import pack_header
+            return ctx.fetch_container(pack_header(grid.dims, grid.chunk_shape, len(out)), out,
+                                       payload)
         return out, payload, offs, recs
     from .core import _require_finite
     _require_finite(grid.data.reshape(shape))
@@ -288,6 +300,9 @@ def grid_to_records(grid: GridArray, params: EbccParams, ctx=None, orig_shape=No
         pos += len(cc.payload)
     payload = np.frombuffer(b"".join(cc.payload for cc in chunks), np.uint8) if pos else \
         np.zeros(0, np.uint8)
+    if container:
+        from .container import assemble
+        return assemble(grid.dims, grid.chunk_shape, out, payload, offs)
     return out, payload, offs, None
 
 
@@ -297,9 +312,8 @@ def records_to_grid(dims, chunk_shape, recs: np.ndarray, offs: np.ndarray, data:
     dims = tuple(int(d) for d in dims)
     chunk_shape = tuple(int(c) for c in chunk_shape)
     t, p, h, w = dims
-    out = np.empty(dims, dtype=np.float32)
     if len(recs) == 0:
-        return out
+        return np.empty(dims, np.float32)
     if chunk_shape[0] == 1 and chunk_shape[1] == 1 and chunk_shape[2] >= h and chunk_shape[3] >= w:
         # one (h, w) chunk per (t, p): validate headers vectorised, decode in place
         buf = np.frombuffer(data, dtype=np.uint8)
@@ -314,6 +328,7 @@ def records_to_grid(dims, chunk_shape, recs: np.ndarray, offs: np.ndarray, data:
             if levels and lv != levels:
                 return _records_to_grid_slow(dims, chunk_shape, recs, offs, data, ctx)
             levels = lv
+        out = _lib.host_empty(dims, np.float32)
         lrec = np.zeros(len(recs), dtype=_lib.REC_DTYPE)
         lrec["mode"] = mode
         lrec["vmin"] = recs["vmin"].astype(np.float64)

@@ -37,3 +37,18 @@ for it in range(3):
     T["decompress"] = time.perf_counter() - t
     print({k: round(v * 1e3, 1) for k, v in T.items()}, "total", round(sum(T.values()) * 1e3, 1),
           _lib.context().stats()["ms_total"], file=sys.stderr)
+
+# the public API as bench.py times it
+res = []
+for it in range(4):
+    t = time.perf_counter()
+    blob = ebcc.compress(arr, rel_error=0.01)
+    t1 = time.perf_counter()
+    st1 = dict(_lib.context().stats())
+    res.append(ebcc.decompress(blob))
+    t2 = time.perf_counter()
+    st2 = dict(_lib.context().stats())
+    res = res[-2:]
+    print(f"api compress {1e3 * (t1 - t):.1f} ms (device {st1['ms_total']:.1f}), "
+          f"decompress {1e3 * (t2 - t1):.1f} ms (device {st2['ms_total']:.1f})", file=sys.stderr)
+
