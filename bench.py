@@ -220,6 +220,8 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         e2e_t += time.perf_counter() - t0
         e2e_c += t1 - t0
+        print(f"[e2e] compress {1e3 * (t1 - t0):.1f} ms, decompress "
+              f"{1e3 * (time.perf_counter() - t1):.1f} ms", file=sys.stderr)
     assert rec_host.shape == (1, nf, ROWS, COLS)
     if world > 1:
         te = torch.tensor([e2e_t, e2e_c], dtype=torch.float64, device=cdev)
