@@ -271,6 +271,7 @@ struct Workspace {
   int16_t *ec = nullptr, *ed = nullptr, *el = nullptr;
   uint32_t *mant = nullptr, *sign_pos = nullptr, *lsp_rank = nullptr;
   uint8_t* pinfo = nullptr;
+  uint8_t* hrel = nullptr;
   uint4* packed = nullptr;
   uint4* packed2 = nullptr;      // residual metadata (built while the pure search runs)
   double *A2 = nullptr, *B2 = nullptr;  // residual forward-DWT scratch
@@ -294,7 +295,8 @@ struct Workspace {
   bool has_tt = false;
 
   void release() {
-    void* ptrs[] = {x32, norm, A, B, base_dec, ec, ed, el, mant, sign_pos, lsp_rank, pinfo, packed, ninfo,
+    void* ptrs[] = {x32, norm, A, B, base_dec, ec, ed, el, mant, sign_pos, lsp_rank, pinfo, hrel,
+                    packed, ninfo,
                     packed2, A2, B2,
                     lip, lis0, lis1, w0, w1, lsp, bits_base, bits_res, pl_base, pl_res,
                     mo_base, mo_res, fs, prm, res, limit, active, mm};
@@ -372,6 +374,7 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   w.sign_pos = dalloc<uint32_t>(N);
   w.lsp_rank = dalloc<uint32_t>(N);
   w.pinfo = dalloc<uint8_t>(N);
+  w.hrel = dalloc<uint8_t>((size_t)((g.n + 15) & ~15ll) * cap + 16);  // 16-B aligned per field
   w.packed = dalloc<uint4>(N);
   w.packed2 = dalloc<uint4>(N);
   w.A2 = dalloc<double>(N);
@@ -412,6 +415,7 @@ MachineBufs machine_bufs(Workspace& w, int nfields, bool residual) {
   mb.mant = w.mant; mb.sign_pos = w.sign_pos; mb.lsp_rank = w.lsp_rank; mb.pinfo = w.pinfo;
   mb.lip = w.lip; mb.lis0 = w.lis0; mb.lis1 = w.lis1; mb.w0 = w.w0; mb.w1 = w.w1; mb.lsp = w.lsp;
   mb.ninfo = w.ninfo;
+  mb.hrel = w.hrel;
   mb.ginfo = w.tt.ginfo;
   mb.bits = residual ? w.bits_res : w.bits_base;
   mb.planes = residual ? w.pl_res : w.pl_base;

@@ -17,7 +17,10 @@
 // (significance read from the stream at the offset the scan assigns), which is
 // how the reference keeps encoder and decoder in lockstep.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "spiht.cuh"
@@ -332,7 +335,10 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   // planes q+1..r: difference counts over planes, summed across the cluster.
   __shared__ int s_diff[66];
   __shared__ int s_knew[64];
-  __shared__ long long s_bc[2];
+  // encoder: likewise the LIS as a history of kept entries; an entry kept at
+  // plane q with significance plane r is an "old" entry for planes q+1..r
+  __shared__ int s_ldiff[66];
+  __shared__ long long s_bc[3];
   int parity = 0;
   auto cscan = [&](uint64_t v) { return cluster_scan(v, ssm, slots, parity, cl); };
   auto csync = [&]() {
@@ -365,9 +371,13 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   // initial lists (spiht.py:300-303); CTAs split the copy
   if (!DECODE) {
     for (int i = threadIdx.x; i < 66; i += MT) s_diff[i] = 0;
+    for (int i = threadIdx.x; i < 66; i += MT) s_ldiff[i] = 0;
     for (int i = threadIdx.x; i < 64; i += MT) s_knew[i] = 0;
     __syncthreads();
-    if (leader) s_diff[0] = (int)tt.nroots;
+    if (leader) {
+      s_diff[0] = (int)tt.nroots;
+      s_ldiff[0] = (int)tt.nlis_roots;
+    }
   }
   for (int64_t i = (int64_t)crank * MT + threadIdx.x; i < tt.nroots; i += (int64_t)MT * csize) {
     const uint64_t e = info[tt.roots[i]];
@@ -378,14 +388,35 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
       atomicAdd(&s_knew[r], 1);
     }
   }
-  for (int64_t i = (int64_t)crank * MT + threadIdx.x; i < tt.nlis_roots; i += (int64_t)MT * csize)
-    lis_old[i] = info[tt.lis_roots[i]];
+  uint8_t* hrel = DECODE ? nullptr : mb.hrel + (int64_t)f * ((mb.stride + 15) & ~15ll);
+  for (int64_t i = (int64_t)crank * MT + threadIdx.x; i < tt.nlis_roots; i += (int64_t)MT * csize) {
+    const uint64_t e = info[tt.lis_roots[i]];
+    lis_old[i] = e;
+    if (!DECODE) {
+      const int r = e_rel(e, ninfo::RELD);
+      hrel[i] = (uint8_t)r;
+      atomicSub(&s_ldiff[r + 1], 1);
+    }
+  }
   uint64_t nlip = tt.nroots, nlis = tt.nlis_roots, nlsp = 0, pos = 0;
   uint64_t hlen = tt.nroots, lip_run = 0;  // encoder: LIP history length, |LIP_p|
+  uint64_t hlis = tt.nlis_roots, lis_run = 0;  // encoder: LIS history length, old |LIS_p|
   int overflow = 0;
   int p = 0;
   csync();
 
+#ifdef EBCC_MPROF
+  unsigned long long mp_t = clock64(), mp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long mp_waves = 0, mp_tiles = 0, mp_ent = 0, mp_bucket = 0;
+#define MPROF_MARK(k)                      \
+  {                                        \
+    unsigned long long t_ = clock64();     \
+    mp_acc[k] += t_ - mp_t;                \
+    mp_t = t_;                             \
+  }
+#else
+#define MPROF_MARK(k)
+#endif
   for (; p < planes; p++) {
     if (DECODE && pos >= limit) break;  // `while not src.depleted`
     const uint64_t refine_len = nlsp;
@@ -491,13 +522,88 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
       csync();  // compaction visible cluster-wide before the LIS appends / next pass
     }
 
+    MPROF_MARK(0);
     // ---------------- LIS waves ------------------------------------------
     {
       uint64_t nkeep = 0;
       const uint64_t* src = lis_old;
       uint64_t* dst = wav_a;
       uint64_t cnt = nlis;
-      while (cnt) {
+      // encoder: the old entries' wave codes only those turning significant
+      // now (relevant plane == p), gathered from the history in order; their
+      // significance bits (and the old entries' zeros) are left to emit_lis
+      bool w0 = false;
+      uint64_t nbucket = 0;
+      if (!DECODE) {
+        if (threadIdx.x == 0) {
+          long long d = 0;
+          for (int r = 0; r < csize; r++) d += *cl.map_shared_rank(&s_ldiff[p], r);
+          s_bc[2] = d;
+        }
+        __syncthreads();
+        lis_run += (uint64_t)s_bc[2];
+        if (leader) prec[p].lis_start = (uint32_t)pos;
+        // each CTA scans a contiguous share of the history bytes
+        const uint64_t per = ((hlis + csize - 1) / csize + 15) & ~15ull;
+        const uint64_t lo = min(hlis, (uint64_t)crank * per), hi = min(hlis, lo + per);
+        uint64_t* tmp = mb.lis1 + fo + lo;
+        const uint32_t pp4 = 0x01010101u * (uint32_t)p;
+        uint64_t n = 0;
+        for (uint64_t base = lo; base < hi; base += (uint64_t)MT * 16) {
+          const uint64_t i0 = base + (uint64_t)threadIdx.x * 16;
+          uint32_t m = 0;
+          if (i0 + 16 <= hi) {
+            const uint4 v = *reinterpret_cast<const uint4*>(hrel + i0);
+            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+              const uint32_t x = __vcmpeq4(w4[q], pp4);
+              m |= (((x >> 7) & 1u) | ((x >> 14) & 2u) | ((x >> 21) & 4u) | ((x >> 28) & 8u))
+                   << (4 * q);
+            }
+          } else {
+            for (int k = 0; k < 16; k++)
+              if (i0 + k < hi && hrel[i0 + k] == (uint8_t)p) m |= 1u << k;
+          }
+          uint64_t tot;
+          uint64_t o = n + block_exclusive_scan((uint64_t)__popc(m), tot, ssm);
+          while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            tmp[o] = lis_old[i0 + k];
+            o++;
+          }
+          n += tot;
+        }
+        // concatenate the CTAs' matches into the wave list
+        if (threadIdx.x == 0) slots[parity] = n;
+        csync();
+        uint64_t before = 0, all = 0;
+        for (int r = 0; r < csize; r++) {
+          const uint64_t t = csize > 1 ? *cl.map_shared_rank(&slots[parity], r) : slots[parity];
+          if (r < crank) before += t;
+          all += t;
+        }
+        parity ^= 1;
+        for (uint64_t k = threadIdx.x; k < n; k += MT) wav_a[before + k] = tmp[k];
+        csync();
+        nbucket = all;
+        src = wav_a;
+        dst = wav_b;
+        cnt = all;
+        w0 = true;
+      }
+      MPROF_MARK(1);
+#ifdef EBCC_MPROF
+      mp_bucket += nbucket;
+#endif
+      const uint64_t hbase = hlis;
+      while (cnt || w0) {
+#ifdef EBCC_MPROF
+        mp_waves++;
+        mp_ent += cnt;
+        mp_tiles += (cnt + CT - 1) / CT;
+#endif
         // prepass: total children bits of significant type-A entries
         uint64_t TC = 0;
         for (uint64_t base = 0; base < cnt; base += CT) {
@@ -514,8 +620,10 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
           }
           TC += cscan(local).total;
         }
-        const uint64_t ch_seg0 = pos + cnt;       // children significance bits
-        const uint64_t sg_seg0 = pos + cnt + TC;  // their sign bits
+        MPROF_MARK(w0 ? 2 : 3);
+        const uint64_t segw = w0 ? lis_run : cnt;  // entry significance bits
+        const uint64_t ch_seg0 = pos + segw;       // children significance bits
+        const uint64_t sg_seg0 = pos + segw + TC;  // their sign bits
         uint64_t ch_off = 0, sig_off = 0, nxt_off = 0;
         for (uint64_t base = 0; base < cnt; base += CT) {
           uint64_t ent[MI];
@@ -594,7 +702,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
             uint64_t spos = sg_seg0 + sig_off + ex2;
 #pragma unroll
             for (int k = 0; k < MI; k++) {
-              if (sig[k]) stage_set(st_a, seg_a, pos + i0 + k);
+              if (sig[k] && !w0) stage_set(st_a, seg_a, pos + i0 + k);
               for (int s = 0; s < nch[k]; s++) {
                 if ((chs[k] >> s) & 1) {
                   stage_set(st_b, seg_b, cpos);
@@ -605,7 +713,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
               }
             }
             __syncthreads();
-            stage_flush(st_a, seg_a, my_len, bits);
+            if (!w0) stage_flush(st_a, seg_a, my_len, bits);
             stage_flush(st_b, seg_b, lane16(s1.cta_total, 1), bits);
             stage_flush(st_c, seg_c, s2.cta_total, bits);
           }
@@ -621,7 +729,19 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
               if (i >= cnt) break;
               uint64_t e = ent[k];
               if (!sig[k]) {
-                if (kp < cap) lis_new[kp] = e; else overflow = 1;
+                if (DECODE) {
+                  if (kp < cap) lis_new[kp] = e; else overflow = 1;
+                } else {  // kept: appended to the LIS history
+                  const uint64_t hi = hbase + kp;
+                  const int r = e_rel(e, e_isb(e) ? ninfo::RELL : ninfo::RELD);
+                  if (hi < cap) {
+                    lis_old[hi] = e;
+                    hrel[hi] = (uint8_t)r;
+                  } else {
+                    overflow = 1;
+                  }
+                  atomicSub(&s_ldiff[r + 1], 1);
+                }
                 kp++;
                 continue;
               }
@@ -676,7 +796,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
           sig_off += tot2;
           __syncthreads();
         }
-        pos += cnt + TC + sig_off;
+        pos += segw + TC + sig_off;
         nlsp += sig_off;
         nlip += TC - sig_off;
         if (!DECODE) {
@@ -684,14 +804,23 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
           if (leader) s_diff[p + 1] += (int)(TC - sig_off);
         }
         cnt = nxt_off;
+        MPROF_MARK(w0 ? 4 : 5);
         src = dst;
         dst = (dst == wav_a) ? wav_b : wav_a;
+        w0 = false;
         csync();  // the next wave reads entries every CTA wrote
       }
-      nlis = nkeep;
-      uint64_t* t = lis_old; lis_old = lis_new; lis_new = t;
+      if (DECODE) {
+        nlis = nkeep;
+        uint64_t* t = lis_old; lis_old = lis_new; lis_new = t;
+      } else {
+        nlis = lis_run - nbucket + nkeep;
+        hlis += nkeep;
+        if (leader) s_ldiff[p + 1] += (int)nkeep;
+      }
     }
 
+    MPROF_MARK(6);
     // ---------------- refinement (positions only) ------------------------
     if (leader) {
       prec[p].refine_start = (uint32_t)pos;
@@ -711,6 +840,15 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
     mb.out[f].overflow = overflow;
     mb.out[f].lsp_count = (uint32_t)nlsp;
     mb.out[f].hist_len = (uint32_t)hlen;
+    mb.out[f].lis_hist_len = (uint32_t)hlis;
+#ifdef EBCC_MPROF
+    if (f == 0)
+      printf("[mprof %s] planes %d lip %.0f bucket %.0f w0pre %.0f wpre %.0f w0main %.0f wmain %.0f "
+             "tail %.0f kcyc | waves %llu tiles %llu entries %llu bucket %llu hlis %llu hlen %llu\n",
+             DECODE ? "dec" : "enc", p, mp_acc[0] / 1e3, mp_acc[1] / 1e3, mp_acc[2] / 1e3,
+             mp_acc[3] / 1e3, mp_acc[4] / 1e3, mp_acc[5] / 1e3, mp_acc[6] / 1e3, mp_waves,
+             mp_tiles, mp_ent, mp_bucket, (unsigned long long)hlis, (unsigned long long)hlen);
+#endif
   }
 }
 
@@ -833,9 +971,20 @@ __device__ __forceinline__ bool emit_skip(const MachineBufs& mb, int f) {
   return (mb.active && !mb.active[f]) || mb.out[f].overflow;
 }
 
+// LIP history (relevant plane: relc) or LIS history (reld for type A, rell
+// for type B entries)
+template <bool LIS>
 __device__ __forceinline__ uint32_t hist_len_of(const MachineBufs& mb, int f) {
-  const uint32_t h = mb.out[f].hist_len;
+  const uint32_t h = LIS ? mb.out[f].lis_hist_len : mb.out[f].hist_len;
   return (int64_t)h < mb.stride ? h : (uint32_t)mb.stride;
+}
+template <bool LIS>
+__device__ __forceinline__ const uint64_t* hist_of(const MachineBufs& mb, int f) {
+  return (LIS ? mb.lis0 : mb.lip) + (int64_t)f * mb.stride;
+}
+template <bool LIS>
+__device__ __forceinline__ int hist_rel(uint64_t e) {
+  return LIS ? e_rel(e, e_isb(e) ? ninfo::RELL : ninfo::RELD) : e_rel(e, ninfo::RELC);
 }
 
 // entry k of thread tid in a tile: sub-tile k, 32-entry group k*32 + warp
@@ -843,20 +992,21 @@ __device__ __forceinline__ int64_t emit_index(int64_t t0, int k) {
   return t0 + (int64_t)k * ET + threadIdx.x;
 }
 
+template <bool LIS>
 __global__ void __launch_bounds__(ET) lip_hist_kernel(MachineBufs mb, uint32_t* hist, int tiles) {
   const int f = blockIdx.y;
   if (emit_skip(mb, f)) return;
-  const uint32_t hlen = hist_len_of(mb, f);
+  const uint32_t hlen = hist_len_of<LIS>(mb, f);
   const int64_t t0 = (int64_t)blockIdx.x * ETILE;
   if (t0 >= hlen) return;
   __shared__ uint32_t h[64];
   if (threadIdx.x < 64) h[threadIdx.x] = 0;
-  const uint64_t* lip = mb.lip + (int64_t)f * mb.stride;
+  const uint64_t* lip = hist_of<LIS>(mb, f);
   int bk[EPT];
 #pragma unroll
   for (int k = 0; k < EPT; k++) {
     const int64_t i = emit_index(t0, k);
-    bk[k] = i < hlen ? e_rel(lip[i], ninfo::RELC) : 64;
+    bk[k] = i < hlen ? hist_rel<LIS>(lip[i]) : 64;
   }
   __syncthreads();
 #pragma unroll
@@ -870,10 +1020,11 @@ __global__ void __launch_bounds__(ET) lip_hist_kernel(MachineBufs mb, uint32_t* 
 }
 
 // exclusive scan of the tile histograms over tiles, per bucket (in place)
+template <bool LIS>
 __global__ void __launch_bounds__(1024) lip_scan_kernel(MachineBufs mb, uint32_t* hist, int tiles) {
   const int f = blockIdx.x;
   if (emit_skip(mb, f)) return;
-  const int ntiles = (int)((hist_len_of(mb, f) + ETILE - 1) / ETILE);
+  const int ntiles = (int)((hist_len_of<LIS>(mb, f) + ETILE - 1) / ETILE);
   const int v = threadIdx.x & 63, sg = threadIdx.x >> 6;  // 16 segments of tiles
   const int per = (ntiles + 15) / 16;
   const int tb = sg * per, te = min(ntiles, tb + per);
@@ -892,11 +1043,12 @@ __global__ void __launch_bounds__(1024) lip_scan_kernel(MachineBufs mb, uint32_t
   }
 }
 
+template <bool LIS>
 __global__ void __launch_bounds__(ET) lip_emit_kernel(MachineBufs mb, const uint32_t* hist,
                                                       int tiles) {
   const int f = blockIdx.y;
   if (emit_skip(mb, f)) return;
-  const uint32_t hlen = hist_len_of(mb, f);
+  const uint32_t hlen = hist_len_of<LIS>(mb, f);
   const int64_t t0 = (int64_t)blockIdx.x * ETILE;
   if (t0 >= hlen) return;
   const int pr = mb.out[f].planes_run;
@@ -907,7 +1059,7 @@ __global__ void __launch_bounds__(ET) lip_emit_kernel(MachineBufs mb, const uint
   for (int k = tid; k < 64 * (EVW + 1); k += ET) (&wh[0][0])[k] = 0;
   if (tid < kMaxPlaneRecs) {
     const PlaneRec& R = mb.planes[(int64_t)f * kMaxPlaneRecs + tid];
-    s_start[tid] = R.start;
+    s_start[tid] = LIS ? R.lis_start : R.start;
     s_lip[tid] = R.lip_len;
     s_ref[tid] = R.refine_len;
   }
@@ -917,12 +1069,12 @@ __global__ void __launch_bounds__(ET) lip_emit_kernel(MachineBufs mb, const uint
 #pragma unroll
   for (int k = 0; k < EPT; k++) {
     const int64_t i = emit_index(t0, k);
-    ent[k] = i < hlen ? mb.lip[fo + i] : 0;
+    ent[k] = i < hlen ? hist_of<LIS>(mb, f)[i] : 0;
   }
 #pragma unroll
   for (int k = 0; k < EPT; k++) {
     const int64_t i = emit_index(t0, k);
-    bk[k] = i < hlen ? e_rel(ent[k], ninfo::RELC) : 64;
+    bk[k] = i < hlen ? hist_rel<LIS>(ent[k]) : 64;
     mk[k] = __match_any_sync(0xffffffffu, bk[k]);
   }
   __syncthreads();
@@ -996,6 +1148,7 @@ __global__ void __launch_bounds__(ET) lip_emit_kernel(MachineBufs mb, const uint
       const uint32_t v = __reduce_or_sync(g, on ? bit_mask_in_word(sig) : 0u);
       if (on && lane == __ffs(g) - 1 && sig < bit_cap) atomicOr(bits + wd, v);
     }
+    if (LIS) continue;  // old LIS entries: significance bit only
     {
       const bool sn = on && neg;
       const uint32_t wd = sn ? (uint32_t)(sp >> 5) : 0xffffffffu;
@@ -1018,9 +1171,13 @@ void emit_lip_host(MachineBufs& mb, cudaStream_t st) {
   const int tiles = (int)((mb.stride + ETILE - 1) / ETILE);
   // the wave buffers are free once the machine is done: tile histograms
   uint32_t* hist = reinterpret_cast<uint32_t*>(mb.w0);
-  lip_hist_kernel<<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist, tiles);
-  lip_scan_kernel<<<mb.nfields, 1024, 0, st>>>(mb, hist, tiles);
-  lip_emit_kernel<<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist, tiles);
+  lip_hist_kernel<false><<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist, tiles);
+  lip_scan_kernel<false><<<mb.nfields, 1024, 0, st>>>(mb, hist, tiles);
+  lip_emit_kernel<false><<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist, tiles);
+  uint32_t* hist2 = reinterpret_cast<uint32_t*>(mb.w1);
+  lip_hist_kernel<true><<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist2, tiles);
+  lip_scan_kernel<true><<<mb.nfields, 1024, 0, st>>>(mb, hist2, tiles);
+  lip_emit_kernel<true><<<dim3(tiles, mb.nfields), ET, 0, st>>>(mb, hist2, tiles);
 }
 
 // decoder init: nothing placed yet
@@ -1098,17 +1255,58 @@ void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables& tt, cuda
                      st>>>(tt.ginfo, mb, g.n);
 }
 
-int machine_cluster_size(int nfields) {
-  const char* e = getenv("EBCC_MACHINE_CLUSTER");
-  int c = e ? atoi(e) : 148 / (nfields > 0 ? nfields : 1);
-  // measured on B200 (37 fields): 2 CTAs/field beats 1 and 4 (cluster-barrier cost);
-  // 16-bit scan lanes hold at most a 4-CTA cluster tile
-  return c < 1 ? 1 : (c > 2 && !e ? 2 : (c > 4 ? 4 : c));
+// CTAs per field: the machine's time is per-entry work, so more CTAs per
+// field help as long as every field's cluster is resident at once (clusters
+// live inside one GPC, so e.g. 37 fields x 4 CTAs do not all fit on 148 SMs).
+// Largest c <= 4 (the 16-bit scan lanes hold a 4-CTA tile) whose co-resident
+// cluster count covers the batch, from the occupancy calculator.
+int machine_cluster_size(bool decode, int nfields) {
+  if (const char* e = getenv("EBCC_MACHINE_CLUSTER")) {
+    const int c = atoi(e);
+    return c < 1 ? 1 : (c > 4 ? 4 : c);
+  }
+  static std::mutex mu;
+  static std::unordered_map<int64_t, int> memo;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int64_t key = ((int64_t)dev << 40) | ((int64_t)decode << 32) | (uint32_t)nfields;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+  }
+  int best = 1;
+  for (int c = 4; c >= 2; c--) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nfields * c), 1, 1);
+    cfg.blockDim = dim3(MT, 1, 1);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    cudaError_t err = decode ? cudaOccupancyMaxActiveClusters(&n, machine_kernel<true>, &cfg)
+                             : cudaOccupancyMaxActiveClusters(&n, machine_kernel<false>, &cfg);
+    if (err != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (n >= nfields) {
+      best = c;
+      break;
+    }
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  memo[key] = best;
+  return best;
 }
 
 void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& tt, int planes,
                  cudaStream_t st, int cluster) {
-  const int cs = cluster > 0 ? cluster : machine_cluster_size(mb.nfields);
+  const int cs = cluster > 0 ? cluster : machine_cluster_size(decode, mb.nfields);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(mb.nfields * cs), 1, 1);
   cfg.blockDim = dim3(MT, 1, 1);

@@ -11,7 +11,8 @@ struct PlaneRec {
   uint32_t refine_len;    // |LSP| at the start of plane p
   uint32_t lists_end;     // |LIP| + |LIS| + |LSP| after plane p
   uint32_t lip_len;       // |LIP| at the start of plane p (encoder)
-  uint32_t pad[3];
+  uint32_t lis_start;     // bit offset of plane p's first LIS wave (encoder)
+  uint32_t pad[2];
 };
 
 constexpr int kMaxPlaneRecs = 64;
@@ -24,7 +25,8 @@ struct MachineOut {
   int32_t overflow;       // list or bit-buffer capacity exceeded
   uint32_t lsp_count;     // |LSP| at the end
   uint32_t hist_len;      // encoder: entries ever appended to the LIP
-  uint32_t pad[2];
+  uint32_t lis_hist_len;  // encoder: entries ever kept in the LIS
+  uint32_t pad;
 };
 
 // List entries are 64-bit "node info" words carrying everything the machine
@@ -55,6 +57,7 @@ struct MachineBufs {
   const uint64_t* ginfo;     // geometry-only node info (decode; shared by all fields)
   // lists (capacity `stride` each)
   uint64_t* lip; uint64_t* lis0; uint64_t* lis1; uint64_t* w0; uint64_t* w1; uint32_t* lsp;
+  uint8_t* hrel;             // encoder: significance plane of each LIS history entry
   // stream bits
   uint32_t* bits;
   PlaneRec* planes;          // [nfields][kMaxPlaneRecs]
@@ -83,7 +86,8 @@ void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables& tt, cuda
 // cluster > 0 forces the CTAs per field (1..4); 0 picks by batch size
 void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& tt, int planes,
                  cudaStream_t st, int cluster = 0);
-// encoder: the deferred LIP passes (fully parallel over the LIP history);
+// encoder: the deferred LIP passes and old-LIS significance bits (fully
+// parallel over the LIP / LIS histories);
 // must run after run_machine(decode=false) and before write_refinement
 void emit_lip(MachineBufs& mb, int planes, cudaStream_t st);
 // encoder refinement bits (fully parallel over LSP)
