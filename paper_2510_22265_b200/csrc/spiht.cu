@@ -64,7 +64,16 @@ __global__ void tree_info_kernel(Geo g, uint64_t* ginfo) {
       if (r < g.lr[kk - 1] && c < g.lc[kk - 1]) { level = kk; break; }
     orient = (r < g.lr[level]) ? 0 : ((c < g.lc[level]) ? 1 : 2);
   }
+  // 2x2 child block layout of detail nodes (children c0, c0+1, c0+cols, ...)
+  int right = 0, bottom = 0;
+  if (level >= 2 && nc > 0) {
+    for (int s = 1; s < nc; s++) {
+      right |= ch[s] == ch[0] + 1;
+      bottom |= ch[s] == ch[0] + (uint32_t)g.cols;
+    }
+  }
   ginfo[idx] = (uint64_t)(uint32_t)idx | bitsat((uint64_t)nc, ninfo::NCH) |
+               bitsat((uint64_t)right, ninfo::RIGHT) | bitsat((uint64_t)bottom, ninfo::BOTTOM) |
                bitsat((uint64_t)gc, ninfo::HASGC) | bitsat((uint64_t)level, ninfo::LEVEL) |
                bitsat((uint64_t)orient, ninfo::ORIENT) | bitsat(63, ninfo::RELC) |
                bitsat(63, ninfo::RELD) | bitsat(63, ninfo::RELL);
@@ -97,6 +106,39 @@ __device__ __forceinline__ int entry_children(const Geo& g, uint64_t e, uint32_t
       if (ci < C.h && cj < C.w) ch[m++] = (uint32_t)((C.r0 + ci) * g.cols + (C.c0 + cj));
     }
   return m;
+}
+
+// children of a detail node: c0 = 2 * node + K[level][orientation] (the 2x2
+// block at (2i, 2j) of the next finer band), compacted like entry_children
+__device__ __forceinline__ int entry_children_k(const Geo& g, const int64_t* K, uint64_t e,
+                                                uint32_t* ch) {
+  const int lev = (int)((e >> ninfo::LEVEL) & 7);
+  if (lev == 0) {  // LL root: same position in each coarsest detail band, compacted
+    const uint32_t node = (uint32_t)e;
+    const int r = (int)(node / (uint32_t)g.cols), c = (int)(node - (uint32_t)r * (uint32_t)g.cols);
+    uint32_t cand[3];
+    bool ok[3];
+#pragma unroll
+    for (int o = 0; o < 3; o++) {
+      const Rect R = detail_rect(g, g.levels, o);
+      ok[o] = R.h > 0 && R.w > 0 && r < R.h && c < R.w;
+      cand[o] = (uint32_t)((R.r0 + r) * g.cols + (R.c0 + c));
+    }
+    ch[0] = ok[0] ? cand[0] : (ok[1] ? cand[1] : cand[2]);
+    ch[1] = ok[0] ? (ok[1] ? cand[1] : cand[2]) : cand[2];
+    ch[2] = cand[2];
+    ch[3] = 0;
+    return (int)ok[0] + (int)ok[1] + (int)ok[2];
+  }
+  const int o = (int)((e >> ninfo::ORIENT) & 3);
+  const uint32_t c0 = (uint32_t)(2 * (int64_t)(uint32_t)e + K[lev * 3 + o]);
+  const uint32_t R = (uint32_t)((e >> ninfo::RIGHT) & 1), B = (uint32_t)((e >> ninfo::BOTTOM) & 1);
+  const uint32_t cols = (uint32_t)g.cols;
+  ch[0] = c0;
+  ch[1] = R ? c0 + 1 : c0 + cols;
+  ch[2] = c0 + cols;
+  ch[3] = c0 + cols + 1;
+  return (int)(1 + R + B + (R & B));
 }
 
 __device__ __forceinline__ int e_rel(uint64_t e, int at) { return (int)((e >> at) & 63); }
@@ -339,6 +381,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   // plane q with significance plane r is an "old" entry for planes q+1..r
   __shared__ int s_ldiff[66];
   __shared__ long long s_bc[3];
+  __shared__ int64_t s_K[8 * 3];  // child-block offsets per (level, orientation)
   int parity = 0;
   auto cscan = [&](uint64_t v) { return cluster_scan(v, ssm, slots, parity, cl); };
   auto csync = [&]() {
@@ -368,6 +411,16 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
   const uint64_t CT = (uint64_t)TILE * csize;      // entries per cluster tile
   const uint64_t my0 = (uint64_t)crank * TILE;      // my sub-tile offset
 
+  if (threadIdx.x < 8 * 3) {
+    const int lev = threadIdx.x / 3, o = threadIdx.x % 3;
+    int64_t k = 0;
+    if (lev >= 2 && lev <= g.levels) {
+      const Rect P = detail_rect(g, lev, o), C = detail_rect(g, lev - 1, o);
+      k = (int64_t)(C.r0 - 2 * P.r0) * g.cols + (C.c0 - 2 * P.c0);
+    }
+    s_K[threadIdx.x] = k;
+  }
+  __syncthreads();
   // initial lists (spiht.py:300-303); CTAs split the copy
   if (!DECODE) {
     for (int i = threadIdx.x; i < 66; i += MT) s_diff[i] = 0;
@@ -652,17 +705,23 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
           // children of significant entries (A: coded; B: next-wave sets)
           uint32_t chn[MI][4];
           uint64_t cin[MI][4];
+          int nchild[MI];
 #pragma unroll
           for (int k = 0; k < MI; k++) {
+            nchild[k] = 0;
             if (!sig[k] || (!nch[k] && nxt[k] >= 0)) continue;
-            int m = entry_children(g, ent[k], chn[k]);
-            for (int s = 0; s < m; s++) cin[k][s] = info[chn[k][s]];
+            const int m = entry_children_k(g, s_K, ent[k], chn[k]);
+            nchild[k] = m;
+#pragma unroll
+            for (int s = 0; s < 4; s++)
+              if (s < m) cin[k][s] = info[chn[k][s]];
             if (nxt[k] < 0) {
               int q = 0;
-              for (int s = 0; s < m; s++) q += e_nch(cin[k][s]) != 0;
+#pragma unroll
+              for (int s = 0; s < 4; s++)
+                if (s < m) q += e_nch(cin[k][s]) != 0;
               nxt[k] = q;
               nch[k] = 0;
-              chn[k][0] = (uint32_t)m;  // remember the child count for the next-wave copy
             }
           }
 #pragma unroll
@@ -678,7 +737,9 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
 #pragma unroll
             for (int k = 0; k < MI; k++) {
               chs[k] = 0;
-              for (int s = 0; s < nch[k]; s++) {
+#pragma unroll
+              for (int s = 0; s < 4; s++) {
+                if (s >= nch[k]) break;
                 int cs = DECODE ? read_bit(bits, cpos, limit) : (e_rel(cin[k][s], ninfo::RELC) <= p);
                 chs[k] |= (uint8_t)(cs << s);
                 nsig += cs;
@@ -703,7 +764,9 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
 #pragma unroll
             for (int k = 0; k < MI; k++) {
               if (sig[k] && !w0) stage_set(st_a, seg_a, pos + i0 + k);
-              for (int s = 0; s < nch[k]; s++) {
+#pragma unroll
+              for (int s = 0; s < 4; s++) {
+                if (s >= nch[k]) break;
                 if ((chs[k] >> s) & 1) {
                   stage_set(st_b, seg_b, cpos);
                   if (e_neg(cin[k][s])) stage_set(st_c, seg_c, spos);
@@ -745,7 +808,9 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
                 kp++;
                 continue;
               }
-              for (int s = 0; s < nch[k]; s++) {
+#pragma unroll
+              for (int s = 0; s < 4; s++) {
+                if (s >= nch[k]) break;
                 uint32_t c = chn[k][s];
                 if ((chs[k] >> s) & 1) {
                   uint64_t rank = nlsp + sg;
@@ -780,9 +845,9 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
                   if (nx < cap) dst[nx] = e | TYPEB; else overflow = 1;
                   nx++;
                 } else {
-                  int m = (int)chn[k][0];
-                  for (int s = 0; s < m; s++)
-                    if (e_nch(cin[k][s])) {
+#pragma unroll
+                  for (int s = 0; s < 4; s++)
+                    if (s < nchild[k] && e_nch(cin[k][s])) {
                       if (nx < cap) dst[nx] = cin[k][s]; else overflow = 1;
                       nx++;
                     }

@@ -39,10 +39,11 @@ struct MachineOut {
 //   bits 51..53 number of children; bit 54 has grandchildren
 //   bit  55     LIS entry of type B
 //   bits 56..58 band level (0 = LL, 1..5 detail); bits 59..60 orientation
+//   bits 61, 62 a detail node's 2x2 child block has its right column / bottom row
 // "significant at plane index p" is simply rel <= p.
 namespace ninfo {
 constexpr int RELC = 32, RELD = 38, RELL = 44, NEG = 50, NCH = 51, HASGC = 54, TYPEB = 55,
-              LEVEL = 56, ORIENT = 59;
+              LEVEL = 56, ORIENT = 59, RIGHT = 61, BOTTOM = 62;
 }
 
 // Batched buffers, all fields `stride` elements apart (bits: bit_stride words).
