@@ -80,6 +80,16 @@ def config3_precip(steps: int = 24, rows: int = GRID_025[0],
     return out
 
 
+def config4_field(v: int, rows: int = GRID_0625[0], cols: int = GRID_0625[1]) -> np.ndarray:
+    """Variable v of configs[3]: 0-5 smooth k^-3, 6-9 wind-like k^-5/3."""
+    gen = np.random.default_rng(3000 + v)
+    if v < 6:
+        mean = float(gen.uniform(0.0, 300.0))
+        std = float(gen.uniform(1.0, 20.0))
+        return temperature_like(rows, cols, seed=3000 + v, mean=mean, std=std)
+    return temperature_like(rows, cols, seed=3000 + v, mean=0.0, std=10.0, beta=5.0 / 3.0)
+
+
 def config4_fields(nvars: int = 10, rows: int = GRID_0625[0],
                    cols: int = GRID_0625[1]):
     """Ten 2881x5760 variables: 6 smooth k^-3 + 4 wind-like k^-5/3 (configs[3]).
@@ -87,14 +97,7 @@ def config4_fields(nvars: int = 10, rows: int = GRID_0625[0],
     Yields (var_index, float32 field) so callers never hold all of them.
     """
     for v in range(nvars):
-        gen = np.random.default_rng(3000 + v)
-        if v < 6:
-            mean = float(gen.uniform(0.0, 300.0))
-            std = float(gen.uniform(1.0, 20.0))
-            yield v, temperature_like(rows, cols, seed=3000 + v, mean=mean, std=std)
-        else:
-            yield v, temperature_like(rows, cols, seed=3000 + v, mean=0.0, std=10.0,
-                                      beta=5.0 / 3.0)
+        yield v, config4_field(v, rows, cols)
 
 
 def config5_field(field_id: int, rows: int = GRID_025[0],

@@ -177,6 +177,32 @@ def test_large_golden(ebcc, golden_large):
     assert not bad, bad
 
 
+def test_full_size_config3_config4_vs_oracle_fixtures(ebcc):
+    """Largest BASELINE.json shapes (configs[3]: 2881x5760; configs[2] steps):
+    container bytes equal the C oracle's (tests/golden/oracle_large.json,
+    made by tools/oracle_fixture_c4.py; the oracle is pinned to the
+    reference's own goldens)."""
+    import hashlib
+    import json
+    import os
+    from paper_2510_22265_b200 import fields
+    with open(os.path.join(os.path.dirname(__file__), "golden", "oracle_large.json")) as fh:
+        cases = json.load(fh)
+    bad = []
+    for case in cases:
+        name = case["name"]
+        if name.startswith("config4_var"):
+            arr = fields.config4_field(int(name[len("config4_var"):]))
+        else:
+            t = int(name[len("config3_step"):])
+            arr = fields.precip_like(fields.GRID_025[0], fields.GRID_025[1], seed=2000 + t)
+        assert gi.sha(arr) == case["input_sha"], name
+        blob = ebcc.compress(arr, case["eps"], case["q"])
+        if hashlib.sha256(blob).hexdigest() != case["container_sha"]:
+            bad.append((name, len(blob), case["container_len"]))
+    assert not bad, bad
+
+
 def test_random_fields_vs_oracle(ebcc, oracle):
     """Fresh random shapes/kinds/targets (not in the goldens): GPU container
     bytes equal the oracle's."""
