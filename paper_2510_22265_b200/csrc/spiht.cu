@@ -726,13 +726,29 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
           }
 #pragma unroll
           for (int k = 0; k < MI; k++) nxts += nxt[k] > 0 ? nxt[k] : 0;
-          const ClusterScanOut s1 = cscan((uint64_t)keep | ((uint64_t)nchs << 16) |
-                                          ((uint64_t)nxts << 32));
-          const uint64_t ex1 = s1.ex, tot1 = s1.total;
-          // children significance
+          // children significance: the encoder knows it now (one scan for all
+          // four counts); the decoder reads it at the offsets the first scan gives
           uint8_t chs[MI];  // bitmask of significant children
           uint32_t nsig = 0;
-          {
+          if (!DECODE) {
+#pragma unroll
+            for (int k = 0; k < MI; k++) {
+              chs[k] = 0;
+#pragma unroll
+              for (int s = 0; s < 4; s++) {
+                if (s >= nch[k]) break;
+                const int cs = e_rel(cin[k][s], ninfo::RELC) <= p;
+                chs[k] |= (uint8_t)(cs << s);
+                nsig += cs;
+              }
+            }
+          }
+          const ClusterScanOut s1 = cscan((uint64_t)keep | ((uint64_t)nchs << 16) |
+                                          ((uint64_t)nxts << 32) |
+                                          (DECODE ? 0ull : ((uint64_t)nsig << 48)));
+          const uint64_t ex1 = s1.ex, tot1 = s1.total;
+          uint64_t ex2, tot2, s2_before, s2_total;
+          if (DECODE) {
             uint64_t cpos = ch_seg0 + ch_off + lane16(ex1, 1);
 #pragma unroll
             for (int k = 0; k < MI; k++) {
@@ -740,15 +756,23 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
 #pragma unroll
               for (int s = 0; s < 4; s++) {
                 if (s >= nch[k]) break;
-                int cs = DECODE ? read_bit(bits, cpos, limit) : (e_rel(cin[k][s], ninfo::RELC) <= p);
+                const int cs = read_bit(bits, cpos, limit);
                 chs[k] |= (uint8_t)(cs << s);
                 nsig += cs;
                 cpos++;
               }
             }
+            const ClusterScanOut s2 = cscan((uint64_t)nsig);
+            ex2 = s2.ex;
+            tot2 = s2.total;
+            s2_before = s2.cta_before;
+            s2_total = s2.cta_total;
+          } else {
+            ex2 = lane16(ex1, 3);
+            tot2 = lane16(tot1, 3);
+            s2_before = lane16(s1.cta_before, 3);
+            s2_total = lane16(s1.cta_total, 3);
           }
-          const ClusterScanOut s2 = cscan((uint64_t)nsig);
-          const uint64_t ex2 = s2.ex, tot2 = s2.total;
           const uint64_t sub0 = base + my0;
           const uint64_t my_len = cnt > sub0 ? ((cnt - sub0) < TILE ? (cnt - sub0) : TILE) : 0;
           if (!DECODE) {
@@ -758,7 +782,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
             __syncthreads();
             uint64_t seg_a = pos + sub0;
             uint64_t seg_b = ch_seg0 + ch_off + lane16(s1.cta_before, 1);
-            uint64_t seg_c = sg_seg0 + sig_off + s2.cta_before;
+            uint64_t seg_c = sg_seg0 + sig_off + s2_before;
             uint64_t cpos = ch_seg0 + ch_off + lane16(ex1, 1);
             uint64_t spos = sg_seg0 + sig_off + ex2;
 #pragma unroll
@@ -778,7 +802,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
             __syncthreads();
             if (!w0) stage_flush(st_a, seg_a, my_len, bits);
             stage_flush(st_b, seg_b, lane16(s1.cta_total, 1), bits);
-            stage_flush(st_c, seg_c, s2.cta_total, bits);
+            stage_flush(st_c, seg_c, s2_total, bits);
           }
           // list updates
           {
