@@ -133,10 +133,11 @@ struct ChunkSearch {
   size_t vsize = 0;                    // replay timeline position
   std::unordered_map<int64_t, double> trunc[2];  // (24|32) t -> err
 
-  bool constant = false, failed = false;
+  bool constant = false, failed = false, pure_done = false;
   int phase = 0;                       // 0 base, 1 pure, 2 trunc, 3 done
-  int64_t pending = -1;                // budget / offset of the probe in flight
-  int pending_planes = 0;
+  int64_t pending = -1;                // budget of the base-memo probe in flight
+  int64_t tpending = -1;               // offset of the truncation probe in flight
+  int tpending_planes = 0;
   int64_t base_budget = -1, pure_budget = -1;
   int64_t trunc_t = -1;
   int trunc_planes = 0;
@@ -347,6 +348,7 @@ struct ebcc_ctx {
   fused::Level0Timer l0;
   cudaStream_t side = nullptr;   // high-priority stream for the overlapped residual encode
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+  cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr;  // fork/join of the joint probe step
   cudaEvent_t tm_a = nullptr, tm_b = nullptr;
   std::vector<ebcc_ctx*> lanes;  // child contexts for concurrent sub-batches
 };
@@ -395,13 +397,14 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   w.mo_base = dalloc<MachineOut>(cap);
   w.mo_res = dalloc<MachineOut>(cap);
   w.fs = dalloc<FieldScal>(cap);
-  w.prm = dalloc<ProbeParam>(cap);
-  w.res = dalloc<ProbeResult>(cap);
+  // two parameter/result slots: pure-base probes and truncation probes
+  w.prm = dalloc<ProbeParam>(2 * (size_t)cap);
+  w.res = dalloc<ProbeResult>(2 * (size_t)cap);
   w.limit = dalloc<uint64_t>(cap);
   w.active = dalloc<uint8_t>(cap);
   w.mm = dalloc<unsigned int>(4 * cap + 2);
-  CK(cudaMallocHost(&w.h_prm, sizeof(ProbeParam) * cap));
-  CK(cudaMallocHost(&w.h_res, sizeof(ProbeResult) * cap));
+  CK(cudaMallocHost(&w.h_prm, sizeof(ProbeParam) * 2 * cap));
+  CK(cudaMallocHost(&w.h_res, sizeof(ProbeResult) * 2 * cap));
   build_tree_tables(g, w.tt, c->stream);
   w.has_tt = true;
 }
@@ -439,6 +442,16 @@ Meta meta_of(Workspace& w, bool residual) {
 struct PhaseClock;
 void pc_mark(PhaseClock* pc, const char* name);
 PhaseClock* g_pc = nullptr;
+// EBCC_PROFILE=1: host-side split of the base/pure probe steps
+struct StepProf {
+  int64_t n = 0;
+  double prep = 0, launch = 0, wait = 0, post = 0, timer = 0;
+};
+StepProf g_sp;
+using SteadyClock = std::chrono::steady_clock;
+inline double us_since(SteadyClock::time_point t) {
+  return std::chrono::duration<double, std::micro>(SteadyClock::now() - t).count();
+}
 
 // encode the pyramids in `coef` (all fields): exponents, machine (which
 // skips all-zero pyramids itself), refinement, packed metadata.  Async on st.
@@ -540,6 +553,11 @@ struct PhaseClock {
   }
   ~PhaseClock() {
     if (on && !log.empty()) fprintf(stderr, "[ebcc profile]%s\n", log.c_str());
+    if (on && g_sp.n)
+      fprintf(stderr, "[ebcc steps] base/pure steps %lld: per step prep %.1f launch %.1f wait %.1f "
+              "post %.1f us\n", (long long)g_sp.n, g_sp.prep / g_sp.n, g_sp.launch / g_sp.n,
+              g_sp.wait / g_sp.n, g_sp.post / g_sp.n);
+    g_sp = StepProf{};
   }
 };
 
@@ -675,143 +693,167 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   std::vector<ProbeParam> prm(nfields);
   std::vector<ProbeResult> res(nfields);
   Meta mbase = meta_of(w, false);
-  StepGraph base_graph, trunc_graph;
+  StepGraph base_graph, trunc_graph, joint_graph;
 
-  // ---- base-memo searches (phase 0: quantile search, phase 1: pure) ----
+  // ---- base quantile search ----
+  // fill the pure-search requests (phase 1) or base-search requests (phase 0)
   std::vector<size_t> base_entries(nfields, 0);
-  for (int phase = 0; phase < 2; phase++) {
-    for (;;) {
-      bool any = false;
-      auto h0 = std::chrono::steady_clock::now();
-      for (int f = 0; f < nfields; f++) {
-        ChunkSearch& s = cs[f];
-        prm[f] = ProbeParam{};
-        if (s.constant) continue;
-        s.missed = false;
-        int64_t r = phase == 0 ? s.search_base() : s.search_pure(base_entries[f]);
-        if (!s.missed) {
-          if (phase == 0) s.base_budget = r;
-          else s.pure_budget = r;
-        } else {
-          s.pending = s.miss_key;
-          int64_t len = s.stream_len(s.miss_key);
-          uint64_t B = (uint64_t)(len - kHeader) * 8;
-          if (B > s.T_base) B = s.T_base;
-          prm[f].B = B;
-          prm[f].planes = kBasePlanes;
-          prm[f].active = 1;
-          any = true;
-        }
-      }
-      replay_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
-      if (!any) break;
-      EventTimer t(c, &c->stats.ms_probe);
-      memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
-      bool timed = false;
-      base_graph.run(st, [&](bool eager) {
-        timed = eager;
-        CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice,
-                           st));
-        CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
-        fused::g_level0_timer = eager ? &c->l0 : nullptr;
-        probe_base(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.x32, w.fs, w.res, st);
-        fused::g_level0_timer = nullptr;
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost,
-                           st));
-      });
-      c->stats.kernel_launches += g.levels;
-      c->stats.probe_launches++;
-      CK(cudaStreamSynchronize(st));
-      accumulate_level0(c, timed);
-      memcpy(res.data(), w.h_res, sizeof(ProbeResult) * nfields);
-      for (int f = 0; f < nfields; f++) {
-        if (!prm[f].active) continue;
-        ChunkSearch& s = cs[f];
-        const int64_t b = s.pending;  // the budget this probe answered
-        Entry e;
-        e.budget = b;
-        e.len = s.stream_len(b);
-        e.count = res[f].count;
-        uint64_t bitsv = res[f].maxerr;
-        memcpy(&e.maxerr, &bitsv, 8);
-        s.at[b] = (int)s.memo.size();
-        s.memo.push_back(e);
-      }
-    }
-    if (phase == 0)
-      for (int f = 0; f < nfields; f++) base_entries[f] = cs[f].memo.size();
-    pc.mark(phase == 0 ? "base_search" : "pure_search");
-    if (phase == 0) {
-      // ---- residue = norm - base decode at the chosen budget (main stream),
-      // then the residual DWT + 32-plane encode on the high-priority side
-      // stream, overlapped with the pure-base search below (which only reads
-      // the base memo and the base metadata) ----
-      for (int f = 0; f < nfields; f++) {
-        prm[f] = ProbeParam{};
-        if (cs[f].constant) continue;
-        int64_t len = cs[f].stream_len(cs[f].base_budget);
-        uint64_t B = (uint64_t)(len - kHeader) * 8;
-        if (B > cs[f].T_base) B = cs[f].T_base;
-        prm[f].B = B; prm[f].planes = kBasePlanes; prm[f].active = 1;
-      }
-      memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
-      CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
-      // resid overwrites norm in place (nothing reads norm after this point)
-      base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
-      c->stats.kernel_launches += g.levels;
-      static const bool overlap = !(getenv("EBCC_OVERLAP") && getenv("EBCC_OVERLAP")[0] == '0');
-      cudaStream_t rs = overlap ? c->side : st;
-      CK(cudaEventRecord(c->ev_a, st));
-      CK(cudaStreamWaitEvent(rs, c->ev_a, 0));
-      CK(cudaEventRecord(c->ev_s0, rs));
-      CK(cudaMemcpyAsync(w.A2, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, rs));
-      forward_dwt(w.A2, w.B2, N, nfields, g, rs);
-      c->stats.kernel_launches += 2 * g.levels;
-      // off the critical path while overlapped: one CTA per field leaves
-      // more SMs to the pure-search probes running beside it
-      static const int rc = getenv("EBCC_RESID_CLUSTER") ? atoi(getenv("EBCC_RESID_CLUSTER")) : 1;
-      encode_launch(c, nfields, true, kDeepPlanes, w.A2, w.packed2, active, rs,
-                    overlap ? rc : 0);
-      CK(cudaEventRecord(c->ev_s1, rs));
-      CK(cudaEventRecord(c->ev_b, rs));
-      if (!overlap) pc.mark("residual_encode(serial)");
-      // the pure search's first H2D of w.prm must not overtake base_to_residue:
-      // both are on `st`, so stream order already guarantees it
-    }
-  }
-  std::vector<MachineOut> rmo(nfields);
-  std::vector<PlaneRec> rpl((size_t)kMaxPlaneRecs * nfields);
-  CK(cudaStreamWaitEvent(st, c->ev_b, 0));
-  encode_collect(c, nfields, true, active, rmo, rpl, st);
-  {
-    float ms = 0;
-    if (cudaEventElapsedTime(&ms, c->ev_s0, c->ev_s1) == cudaSuccess) c->stats.ms_encode += ms;
-  }
-
-  pc.mark("residual_encode");
-  Meta mres = meta_of(w, true);
-  // stream totals of the 24- and 32-plane variants
-  std::vector<uint64_t> T24(nfields, 0), T32(nfields, 0);
-  for (int f = 0; f < nfields; f++) {
-    if (!active[f] || rmo[f].n_max == kExpNone) continue;
-    const PlaneRec* p = &rpl[(size_t)f * kMaxPlaneRecs];
-    T32[f] = rmo[f].total_bits;
-    T24[f] = p[kBasePlanes].start;
-  }
-  auto total_bytes = [&](int f, int pi) -> int64_t {
-    uint64_t T = pi == 0 ? T24[f] : T32[f];
-    return (int64_t)((T + 7) / 8);
-  };
-
-  // ---- truncation search (24 planes, then 32) ----
-  std::vector<int> pass(nfields, 0);
-  std::vector<int> trunc_calls(nfields, 0);
-  for (;;) {
+  auto base_requests = [&](int phase) {
     bool any = false;
     for (int f = 0; f < nfields; f++) {
       ChunkSearch& s = cs[f];
       prm[f] = ProbeParam{};
+      if (s.constant) continue;
+      if (phase == 1 && s.pure_done) continue;
+      s.missed = false;
+      int64_t r = phase == 0 ? s.search_base() : s.search_pure(base_entries[f]);
+      if (!s.missed) {
+        if (phase == 0) {
+          s.base_budget = r;
+        } else {
+          s.pure_budget = r;
+          s.pure_done = true;
+        }
+      } else {
+        s.pending = s.miss_key;
+        int64_t len = s.stream_len(s.miss_key);
+        uint64_t B = (uint64_t)(len - kHeader) * 8;
+        if (B > s.T_base) B = s.T_base;
+        prm[f].B = B;
+        prm[f].planes = kBasePlanes;
+        prm[f].active = 1;
+        any = true;
+      }
+    }
+    return any;
+  };
+  auto base_results = [&]() {
+    memcpy(res.data(), w.h_res, sizeof(ProbeResult) * nfields);
+    for (int f = 0; f < nfields; f++) {
+      if (!prm[f].active) continue;
+      ChunkSearch& s = cs[f];
+      const int64_t b = s.pending;  // the budget this probe answered
+      Entry e;
+      e.budget = b;
+      e.len = s.stream_len(b);
+      e.count = res[f].count;
+      uint64_t bitsv = res[f].maxerr;
+      memcpy(&e.maxerr, &bitsv, 8);
+      s.at[b] = (int)s.memo.size();
+      s.memo.push_back(e);
+    }
+  };
+  auto enqueue_base = [&](bool eager) {
+    CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
+    fused::g_level0_timer = eager ? &c->l0 : nullptr;
+    probe_base(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.x32, w.fs, w.res, st);
+    fused::g_level0_timer = nullptr;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
+  };
+  for (;;) {
+    auto h0 = SteadyClock::now();
+    const bool any = base_requests(0);
+    replay_ms += std::chrono::duration<double, std::milli>(SteadyClock::now() - h0).count();
+    if (!any) break;
+    auto tp0 = SteadyClock::now();
+    g_sp.prep += std::chrono::duration<double, std::micro>(tp0 - h0).count();
+    g_sp.n++;
+    EventTimer t(c, &c->stats.ms_probe);
+    memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
+    bool timed = false;
+    base_graph.run(st, [&](bool eager) {
+      timed = eager;
+      enqueue_base(eager);
+    });
+    c->stats.kernel_launches += g.levels;
+    c->stats.probe_launches++;
+    auto tp1 = SteadyClock::now();
+    g_sp.launch += std::chrono::duration<double, std::micro>(tp1 - tp0).count();
+    CK(cudaStreamSynchronize(st));
+    auto tp2 = SteadyClock::now();
+    g_sp.wait += std::chrono::duration<double, std::micro>(tp2 - tp1).count();
+    accumulate_level0(c, timed);
+    base_results();
+    g_sp.post += us_since(tp2);
+  }
+  for (int f = 0; f < nfields; f++) base_entries[f] = cs[f].memo.size();
+  pc.mark("base_search");
+
+  // ---- residue = norm - base decode at the chosen budget (main stream),
+  // then the residual DWT + 32-plane encode on the high-priority side
+  // stream, overlapped with the first pure-base probes below (which only
+  // read the base memo and the base metadata) ----
+  for (int f = 0; f < nfields; f++) {
+    prm[f] = ProbeParam{};
+    if (cs[f].constant) continue;
+    int64_t len = cs[f].stream_len(cs[f].base_budget);
+    uint64_t B = (uint64_t)(len - kHeader) * 8;
+    if (B > cs[f].T_base) B = cs[f].T_base;
+    prm[f].B = B; prm[f].planes = kBasePlanes; prm[f].active = 1;
+  }
+  memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
+  CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
+  // resid overwrites norm in place (nothing reads norm after this point)
+  base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
+  c->stats.kernel_launches += g.levels;
+  static const bool overlap = !(getenv("EBCC_OVERLAP") && getenv("EBCC_OVERLAP")[0] == '0');
+  cudaStream_t rs = overlap ? c->side : st;
+  CK(cudaEventRecord(c->ev_a, st));
+  CK(cudaStreamWaitEvent(rs, c->ev_a, 0));
+  CK(cudaEventRecord(c->ev_s0, rs));
+  CK(cudaMemcpyAsync(w.A2, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, rs));
+  forward_dwt(w.A2, w.B2, N, nfields, g, rs);
+  c->stats.kernel_launches += 2 * g.levels;
+  // off the critical path while overlapped: one CTA per field leaves
+  // more SMs to the pure-search probes running beside it
+  static const int rc = getenv("EBCC_RESID_CLUSTER") ? atoi(getenv("EBCC_RESID_CLUSTER")) : 1;
+  encode_launch(c, nfields, true, kDeepPlanes, w.A2, w.packed2, active, rs, overlap ? rc : 0);
+  CK(cudaEventRecord(c->ev_s1, rs));
+  CK(cudaEventRecord(c->ev_b, rs));
+  if (!overlap) pc.mark("residual_encode(serial)");
+
+  // ---- pure-base search and truncation search (24 planes, then 32),
+  // interleaved: they are independent given the base search, so once the
+  // residual stream has landed every step probes both kinds of candidates
+  // as two concurrent graph branches (pure on `st`, truncation on `side`,
+  // with their own parameter/result slots and scratch pyramids) ----
+  std::vector<MachineOut> rmo(nfields);
+  std::vector<PlaneRec> rpl((size_t)kMaxPlaneRecs * nfields);
+  std::vector<uint64_t> T24(nfields, 0), T32(nfields, 0);
+  Meta mres = meta_of(w, true);
+  bool resid_ready = false;
+  auto collect_residual = [&]() {
+    CK(cudaStreamWaitEvent(st, c->ev_b, 0));
+    encode_collect(c, nfields, true, active, rmo, rpl, st);
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, c->ev_s0, c->ev_s1) == cudaSuccess) c->stats.ms_encode += ms;
+    for (int f = 0; f < nfields; f++) {
+      if (!active[f] || rmo[f].n_max == kExpNone) continue;
+      const PlaneRec* p = &rpl[(size_t)f * kMaxPlaneRecs];
+      T32[f] = rmo[f].total_bits;
+      T24[f] = p[kBasePlanes].start;
+    }
+    resid_ready = true;
+  };
+  auto total_bytes = [&](int f, int pi) -> int64_t {
+    uint64_t T = pi == 0 ? T24[f] : T32[f];
+    return (int64_t)((T + 7) / 8);
+  };
+  std::vector<int> pass(nfields, 0);
+  std::vector<int> trunc_calls(nfields, 0);
+  std::vector<ProbeParam> tprm(nfields);
+  std::vector<ProbeResult> tres(nfields);
+  ProbeParam* d_tprm = w.prm + w.cap;
+  ProbeResult* d_tres = w.res + w.cap;
+  ProbeParam* h_tprm = w.h_prm + w.cap;
+  ProbeResult* h_tres = w.h_res + w.cap;
+  auto trunc_requests = [&]() {
+    bool any = false;
+    for (int f = 0; f < nfields; f++) {
+      ChunkSearch& s = cs[f];
+      tprm[f] = ProbeParam{};
       if (s.constant || s.trunc_planes || pass[f] > 1) continue;
       for (;;) {
         s.missed = false;
@@ -828,52 +870,97 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
           if (pass[f] > 1) break;
         } else {
           NeedTrunc nt{s.miss_planes, s.miss_key};
-          s.pending = nt.t;
-          s.pending_planes = nt.planes;
+          s.tpending = nt.t;
+          s.tpending_planes = nt.planes;
           int P = nt.planes == 0 ? kBasePlanes : kDeepPlanes;
           uint64_t T = nt.planes == 0 ? T24[f] : T32[f];
           uint64_t Bfull = (uint64_t)nt.t * 8;
-          prm[f].B = Bfull < T ? Bfull : T;
-          prm[f].planes = P;
-          prm[f].midpoint = 1;
-          prm[f].n_last = rmo[f].n_max == kExpNone
-                              ? 0
-                              : n_last_of(rmo[f], &rpl[(size_t)f * kMaxPlaneRecs], P, Bfull, T);
-          prm[f].active = 1;
+          tprm[f].B = Bfull < T ? Bfull : T;
+          tprm[f].planes = P;
+          tprm[f].midpoint = 1;
+          tprm[f].n_last = rmo[f].n_max == kExpNone
+                               ? 0
+                               : n_last_of(rmo[f], &rpl[(size_t)f * kMaxPlaneRecs], P, Bfull, T);
+          tprm[f].active = 1;
           any = true;
           break;
         }
       }
     }
-    if (!any) break;
+    return any;
+  };
+  auto enqueue_trunc = [&](cudaStream_t ts, double* a, double* b, bool eager) {
+    CK(cudaMemcpyAsync(d_tprm, h_tprm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, ts));
+    CK(cudaMemsetAsync(d_tres, 0, sizeof(ProbeResult) * nfields, ts));
+    fused::g_level0_timer = eager ? &c->l0 : nullptr;
+    probe_trunc(mres, d_tprm, a, b, g, nfields, w.base_dec, w.x32, w.fs, d_tres, ts);
+    fused::g_level0_timer = nullptr;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h_tres, d_tres, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, ts));
+  };
+  auto trunc_results = [&]() {
+    memcpy(tres.data(), h_tres, sizeof(ProbeResult) * nfields);
+    for (int f = 0; f < nfields; f++) {
+      if (!tprm[f].active) continue;
+      ChunkSearch& s = cs[f];
+      double e;
+      uint64_t bitsv = tres[f].maxerr;
+      memcpy(&e, &bitsv, 8);
+      s.trunc[s.tpending_planes][s.tpending] = e;
+    }
+  };
+  bool pure_phase_marked = false;
+  for (;;) {
+    if (!resid_ready && cudaEventQuery(c->ev_b) == cudaSuccess) collect_residual();
+    cudaGetLastError();  // a not-ready query is not an error
+    auto h0 = SteadyClock::now();
+    const bool anyp = base_requests(1);
+    const bool anyt = resid_ready && trunc_requests();
+    replay_ms += std::chrono::duration<double, std::milli>(SteadyClock::now() - h0).count();
+    if (!anyp && !pure_phase_marked) {
+      pc.mark("pure_search");
+      pure_phase_marked = true;
+    }
+    if (!anyp && !anyt) {
+      if (!resid_ready) {
+        collect_residual();
+        pc.mark("residual_encode");
+        continue;
+      }
+      break;
+    }
     EventTimer t(c, &c->stats.ms_probe);
-    memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
     bool timed = false;
+    if (anyp) memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
+    if (anyt) memcpy(h_tprm, tprm.data(), sizeof(ProbeParam) * nfields);
+    if (anyp && anyt) {
+      joint_graph.run(st, [&](bool eager) {
+        timed = eager;
+        CK(cudaEventRecord(c->ev_f0, st));
+        CK(cudaStreamWaitEvent(c->side, c->ev_f0, 0));
+        enqueue_trunc(c->side, w.A2, w.B2, false);
+        enqueue_base(eager);
+        CK(cudaEventRecord(c->ev_f1, c->side));
+        CK(cudaStreamWaitEvent(st, c->ev_f1, 0));
+      });
+    } else if (anyp) {
+      base_graph.run(st, [&](bool eager) {
+        timed = eager;
+        enqueue_base(eager);
+      });
+    } else {
       trunc_graph.run(st, [&](bool eager) {
         timed = eager;
-      CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
-      CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
-      fused::g_level0_timer = eager ? &c->l0 : nullptr;
-      probe_trunc(mres, w.prm, w.A, w.B, g, nfields, w.base_dec, w.x32, w.fs, w.res, st);
-      fused::g_level0_timer = nullptr;
-      CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
-    });
-    c->stats.kernel_launches += g.levels;
+        enqueue_trunc(st, w.A, w.B, eager);
+      });
+    }
+    c->stats.kernel_launches += (anyp + anyt) * g.levels;
     c->stats.probe_launches++;
     CK(cudaStreamSynchronize(st));
     accumulate_level0(c, timed);
-    memcpy(res.data(), w.h_res, sizeof(ProbeResult) * nfields);
-    for (int f = 0; f < nfields; f++) {
-      if (!prm[f].active) continue;
-      ChunkSearch& s = cs[f];
-      double e;
-      uint64_t bitsv = res[f].maxerr;
-      memcpy(&e, &bitsv, 8);
-      s.trunc[s.pending_planes][s.pending] = e;
-    }
+    if (anyp) base_results();
+    if (anyt) trunc_results();
   }
-
   pc.mark("trunc_search");
   g_pc = nullptr;
   if (pc.on) {
@@ -974,6 +1061,8 @@ int ebcc_create(int32_t device, ebcc_ctx** out) {
     cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi);
     cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_f0, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_f1, cudaEventDisableTiming);
     cudaEventCreate(&c->ev_s0);
     cudaEventCreate(&c->ev_s1);
     cudaEventCreate(&c->tm_a);
@@ -1004,6 +1093,8 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
+  if (c->ev_f0) cudaEventDestroy(c->ev_f0);
+  if (c->ev_f1) cudaEventDestroy(c->ev_f1);
   if (c->ev_s0) cudaEventDestroy(c->ev_s0);
   if (c->ev_s1) cudaEventDestroy(c->ev_s1);
   if (c->tm_a) cudaEventDestroy(c->tm_a);
