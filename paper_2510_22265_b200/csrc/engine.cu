@@ -286,6 +286,8 @@ struct Workspace {
   FieldScal* fs = nullptr;
   ProbeParam* prm = nullptr;
   ProbeResult* res = nullptr;
+  uint8_t* tq_base = nullptr;  // per-probe decode tables (Meta::tq)
+  uint8_t* tq_res = nullptr;
   uint64_t* limit = nullptr;
   uint8_t* active = nullptr;
   unsigned int* mm = nullptr;
@@ -300,7 +302,7 @@ struct Workspace {
                     packed, ninfo,
                     packed2, A2, B2,
                     lip, lis0, lis1, w0, w1, lsp, bits_base, bits_res, pl_base, pl_res,
-                    mo_base, mo_res, fs, prm, res, limit, active, mm};
+                    mo_base, mo_res, fs, prm, res, tq_base, tq_res, limit, active, mm};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (h_prm) cudaFreeHost(h_prm);
@@ -398,6 +400,8 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   w.mo_res = dalloc<MachineOut>(cap);
   w.fs = dalloc<FieldScal>(cap);
   // two parameter/result slots: pure-base probes and truncation probes
+  w.tq_base = dalloc<uint8_t>((size_t)kTqBytes * cap);
+  w.tq_res = dalloc<uint8_t>((size_t)kTqBytes * cap);
   w.prm = dalloc<ProbeParam>(2 * (size_t)cap);
   w.res = dalloc<ProbeResult>(2 * (size_t)cap);
   w.limit = dalloc<uint64_t>(cap);
@@ -434,6 +438,7 @@ Meta meta_of(Workspace& w, bool residual) {
   m.planes = residual ? w.pl_res : w.pl_base;
   m.mo = residual ? w.mo_res : w.mo_base;
   m.stride = w.g.n;
+  m.tq = residual ? w.tq_res : w.tq_base;
   return m;
 }
 

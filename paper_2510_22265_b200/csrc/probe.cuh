@@ -40,7 +40,11 @@ struct Meta {  // one field = `stride` entries
   const PlaneRec* planes;
   const MachineOut* mo;
   int64_t stride;
+  // per-probe decode tables, kTqBytes per field (64 plane thresholds + the
+  // rank-bucket table), built once per probe by inverse_fused's first kernel
+  uint8_t* tq;
 };
+constexpr int kTqBytes = 64 * 4 + 2048;
 
 // GPU self-test: FMA-corrected exact divisions vs __ddiv_rn on n random cases
 void selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t st);
