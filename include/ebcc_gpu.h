@@ -131,6 +131,34 @@ int ebcc_spiht_encode(ebcc_ctx *ctx, const double *coeffs, int32_t rows, int32_t
 int ebcc_spiht_decode(ebcc_ctx *ctx, const uint8_t *data, int64_t len, int64_t prefix_len,
                       int32_t rows, int32_t cols, double *coeffs_out, int32_t *n_last);
 
+/* Quality metrics of the reference's benchmark harness (pkg/src/ebcc/bench/
+ * metrics.py), float64 on the device, for nfields fields of n (= rows*cols)
+ * float32 values each; `orig`/`rec` are host pointers unless flags has
+ * EBCC_INPUT_ON_DEVICE.  Statistics and SSIM reduce in a fixed order.
+ *   ebcc_error_stats      core.error_stats (core.py:189-207) ingredients, per
+ *                         field 5 doubles: max|rec-orig|, min(orig),
+ *                         max(orig), sum (rec-orig)^2, count(orig != rec).
+ *   ebcc_error_histogram  metrics.error_histogram (metrics.py:78-99) counts for
+ *                         caller-given edges (nfields x (bins+1), np.linspace);
+ *                         bins [e_k, e_k+1), the last closed; exact counts.
+ *   ebcc_ssim             metrics.ssim (metrics.py:47-75): mean SSIM, 11x11
+ *                         Gaussian (sigma 1.5), range from `orig`, 1 for
+ *                         identical fields; rows, cols >= 11.
+ *   ebcc_radial_spectrum  metrics.radial_power_spectrum (metrics.py:102-125):
+ *                         |fft2(a)/(rows*cols)|^2 summed per wavenumber annulus;
+ *                         bin_idx (rows*cols, host) is the rounded isotropic
+ *                         wavenumber of each mode (bins 1..kmax kept). */
+int ebcc_error_stats(ebcc_ctx *ctx, const float *orig, const float *rec, int64_t nfields,
+                     int64_t n, int32_t flags, double *out);
+int ebcc_error_histogram(ebcc_ctx *ctx, const float *orig, const float *rec, int64_t nfields,
+                         int64_t n, int32_t bins, const double *edges, int32_t flags,
+                         int64_t *counts);
+int ebcc_ssim(ebcc_ctx *ctx, const float *orig, const float *rec, int64_t nfields, int32_t rows,
+              int32_t cols, int32_t flags, double *out);
+int ebcc_radial_spectrum(ebcc_ctx *ctx, const float *data, int64_t nfields, int32_t rows,
+                         int32_t cols, const int32_t *bin_idx, int32_t kmax, int32_t flags,
+                         double *out);
+
 /* Self-test of the FMA-corrected exact divisions used by the kernels
  * (x / SCALE_LOW, x / SCALE_HIGH, x / range) against IEEE __ddiv_rn on n
  * random operands; *mismatches must be 0. */

@@ -29,7 +29,8 @@ OUTPUT_ON_DEVICE = 2
 EXPORTS = ("ebcc_abi_version", "ebcc_create", "ebcc_destroy", "ebcc_set_stream",
            "ebcc_last_error", "ebcc_last_error_index", "ebcc_compress", "ebcc_fetch_payload", "ebcc_decompress",
            "ebcc_get_stats", "ebcc_dwt", "ebcc_spiht_encode", "ebcc_spiht_decode",
-           "ebcc_selftest_div", "ebcc_fetch_container", "ebcc_host_alloc", "ebcc_host_free")
+           "ebcc_selftest_div", "ebcc_fetch_container", "ebcc_host_alloc", "ebcc_host_free",
+           "ebcc_error_stats", "ebcc_error_histogram", "ebcc_ssim", "ebcc_radial_spectrum")
 
 
 class ChunkRec(ctypes.Structure):
@@ -91,6 +92,10 @@ def load(path: str = LIB_PATH):
         L.ebcc_fetch_container.argtypes = [P, P, P, i64, P, i64, i32, ctypes.POINTER(i64)]
         L.ebcc_host_alloc.argtypes = [i64, ctypes.POINTER(P)]
         L.ebcc_host_free.argtypes = [P]
+        L.ebcc_error_stats.argtypes = [P, P, P, i64, i64, i32, P]
+        L.ebcc_error_histogram.argtypes = [P, P, P, i64, i64, i32, P, i32, P]
+        L.ebcc_ssim.argtypes = [P, P, P, i64, i32, i32, i32, P]
+        L.ebcc_radial_spectrum.argtypes = [P, P, i64, i32, i32, P, i32, i32, P]
         _lib = L
         return L
 

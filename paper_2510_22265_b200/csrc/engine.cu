@@ -36,6 +36,7 @@
 #include "idwt_fused.cuh"
 #include "probe.cuh"
 #include "spiht.cuh"
+#include "ctx.cuh"
 
 using namespace ebcc;
 
@@ -1043,6 +1044,12 @@ int fail(ebcc_ctx* c, int code, const std::string& msg) {
 
 }  // namespace
 
+namespace ebcc {
+cudaStream_t ctx_stream(ebcc_ctx* c) { return c->stream; }
+int ctx_device(ebcc_ctx* c) { return c->device; }
+int ctx_fail(ebcc_ctx* c, int code, const char* msg) { return fail(c, code, msg); }
+}  // namespace ebcc
+
 // ===========================================================================
 // C ABI
 extern "C" {
@@ -1080,6 +1087,7 @@ int ebcc_create(int32_t device, ebcc_ctx** out) {
 
 void ebcc_destroy(ebcc_ctx* c) {
   if (!c) return;
+  metrics_release(c);
   for (ebcc_ctx* l : c->lanes) ebcc_destroy(l);
   c->lanes.clear();
   cudaSetDevice(c->device);
