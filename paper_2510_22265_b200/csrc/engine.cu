@@ -642,6 +642,12 @@ void accumulate_level0(ebcc_ctx* c, bool timed) {
   }
 }
 
+// feasibility-only probes may skip settled CTAs (EBCC_EARLY=0 disables)
+bool early_ok() {
+  static const bool on = !(getenv("EBCC_EARLY") && getenv("EBCC_EARLY")[0] == '0');
+  return on;
+}
+
 // one compress batch of nfields (<= workspace capacity); x already in w.x32
 int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0, double tol,
                    ebcc_chunk_rec* recs, int64_t out_base_off, std::vector<PackPart>& parts,
@@ -728,6 +734,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
         prm[f].B = B;
         prm[f].planes = kBasePlanes;
         prm[f].active = 1;
+        prm[f].early = phase == 1 && early_ok();  // the pure search only asks max_err <= eps_abs
         any = true;
       }
     }
@@ -888,6 +895,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
                                ? 0
                                : n_last_of(rmo[f], &rpl[(size_t)f * kMaxPlaneRecs], P, Bfull, T);
           tprm[f].active = 1;
+          tprm[f].early = early_ok();  // err_at(t) <= eps_abs is all the search asks
           any = true;
           break;
         }

@@ -145,26 +145,36 @@ __device__ __forceinline__ void warp_flush(ProbeResult* r, unsigned long long cn
   }
 }
 
+// an error above eps_abs already recorded for chunk f by another CTA
+__device__ __forceinline__ bool settled(const ProbeResult* r, double eps_abs) {
+  const unsigned long long b = *reinterpret_cast<const volatile unsigned long long*>(&r->maxerr);
+  return __longlong_as_double((long long)b) > eps_abs;
+}
+
 struct BaseProbeEpi {
   const double* norm; const float* orig; const FieldScal* fs; const ProbeParam* prm;
   ProbeResult* res; int64_t n;
-  unsigned long long cnt; double mx; FieldScal s;
+  unsigned long long cnt; double mx; FieldScal s; bool count;
   using Pre = float;
   __device__ Pre pre(int f, int64_t off) const { return orig[(int64_t)f * n + off]; }
   __device__ bool begin(int f) {
     cnt = 0; mx = 0.0;
     if (!prm[f].active) return false;
     s = fs[f];
+    count = !prm[f].early;
     return true;
   }
+  __device__ bool skip(int f) const { return !count && settled(&res[f], s.eps_abs); }
   __device__ void put(double*, int f, int64_t off, double dec, float o) {
-    // normalised value recomputed exactly like core.normalize (core.py:179)
-    double nv = fused::div_exact(__dsub_rn((double)o, s.vmin), s.range, s.range_inv);
-    cnt += fabs(__dsub_rn(dec, nv)) <= s.eps_rel;
+    if (count) {  // quantile search: the count of |dec - norm| <= eps_rel
+      // normalised value recomputed exactly like core.normalize (core.py:179)
+      double nv = fused::div_exact(__dsub_rn((double)o, s.vmin), s.range, s.range_inv);
+      cnt += fabs(__dsub_rn(dec, nv)) <= s.eps_rel;
+    }
     double e = denorm_err(s, dec, o);
     mx = fmax(e, mx);
   }
-  __device__ void finish(int f) { warp_flush(&res[f], cnt, mx, true); }
+  __device__ void finish(int f) { warp_flush(&res[f], cnt, mx, count); }
 };
 
 struct TruncPre {
@@ -186,6 +196,7 @@ struct TruncProbeEpi {
     s = fs[f];
     return true;
   }
+  __device__ bool skip(int f) const { return prm[f].early && settled(&res[f], s.eps_abs); }
   __device__ void put(double*, int f, int64_t off, double v, const Pre& p) {
     double rec = __dadd_rn(p.base, v);  // base_field + dequantized
     double e = denorm_err(s, rec, p.orig);
@@ -199,6 +210,7 @@ struct ResidueEpi {
   using Pre = double;
   __device__ Pre pre(int f, int64_t off) const { return norm[(int64_t)f * n + off]; }
   __device__ bool begin(int f) { return prm[f].active != 0; }
+  __device__ bool skip(int) const { return false; }
   __device__ void put(double*, int f, int64_t off, double dec, double nv) {
     int64_t o = (int64_t)f * n + off;
     base_dec[o] = dec;
@@ -212,6 +224,7 @@ struct StoreFieldEpi {
   using Pre = fused::NoPre;
   __device__ Pre pre(int, int64_t) const { return {}; }
   __device__ bool begin(int f) { return prm[f].active != 0; }
+  __device__ bool skip(int) const { return false; }
   __device__ void put(double*, int f, int64_t off, double v, const Pre&) {
     out[(int64_t)f * n + off] = v;
   }
@@ -228,6 +241,7 @@ struct AddDenormEpi {
     s = fs[f];
     return true;
   }
+  __device__ bool skip(int) const { return false; }
   __device__ void put(double*, int f, int64_t off, double v, double b) {
     int64_t o = (int64_t)f * n + off;
     double fld = __dadd_rn(b, v);

@@ -25,6 +25,11 @@ struct ProbeParam {
   int32_t midpoint;    // add sign * 2^(n_last-1) (residual layer)
   int32_t n_last;
   int32_t active;
+  // the caller only needs max_err <= eps_abs (pure-base and truncation
+  // probes): no quantile count, and CTAs starting after another CTA has
+  // already seen an error above eps_abs skip their work
+  int32_t early;
+  int32_t pad;
 };
 
 struct ProbeResult {
