@@ -454,6 +454,23 @@ struct StepProf {
   double prep = 0, launch = 0, wait = 0, post = 0, timer = 0;
 };
 StepProf g_sp;
+// EBCC_SLOWLOG=<ms>: report host intervals longer than that (tail-latency hunt)
+struct SlowLog {
+  double thr = -1;
+  std::chrono::steady_clock::time_point last;
+  SlowLog() {
+    if (const char* e = getenv("EBCC_SLOWLOG")) thr = atof(e);
+    last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what, int i = -1) {
+    if (thr < 0) return;
+    auto now = std::chrono::steady_clock::now();
+    double ms = std::chrono::duration<double, std::milli>(now - last).count();
+    if (ms > thr) fprintf(stderr, "[ebcc slow] %s %d: %.2f ms\n", what, i, ms);
+    last = now;
+  }
+};
+thread_local SlowLog g_slow;
 using SteadyClock = std::chrono::steady_clock;
 inline double us_since(SteadyClock::time_point t) {
   return std::chrono::duration<double, std::micro>(SteadyClock::now() - t).count();
@@ -662,6 +679,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   double replay_ms = 0;
   // ---- ingest + normalise (core.normalize) ----
   CK(cudaGetLastError());
+  g_slow.mark("enter_batch");
   ingest_normalize(w.x32, N, nfields, w.norm, w.fs, w.mm, eps_rel, st);
   CK(cudaGetLastError());
   pc.mark("ingest");
@@ -698,6 +716,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     encode_pyramids(c, nfields, false, kBasePlanes, active, mo, pl);
   }
   pc.mark("base_tail");
+  g_slow.mark("base_encode");
   for (int f = 0; f < nfields; f++) cs[f].T_base = active[f] ? mo[f].total_bits : 0;
   std::vector<int> base_nmax(nfields);
   for (int f = 0; f < nfields; f++) base_nmax[f] = mo[f].n_max;
@@ -790,6 +809,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     accumulate_level0(c, timed);
     base_results();
     g_sp.post += us_since(tp2);
+    g_slow.mark("base_step", (int)g_sp.n);
   }
   for (int f = 0; f < nfields; f++) base_entries[f] = cs[f].memo.size();
   pc.mark("base_search");
@@ -974,6 +994,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     accumulate_level0(c, timed);
     if (anyp) base_results();
     if (anyt) trunc_results();
+    g_slow.mark(anyp && anyt ? "joint_step" : (anyp ? "pure_step" : "trunc_step"));
   }
   pc.mark("trunc_search");
   g_pc = nullptr;
@@ -1174,9 +1195,11 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
     std::vector<PackPart> parts;
     sizes.clear();
     int status = EBCC_OK;
+    g_slow.mark("compress_setup");
     for (int64_t f0 = 0; f0 < nfields; f0 += cap) {
       int nb = (int)std::min<int64_t>(cap, nfields - f0);
       ensure_workspace(c, g, nb);
+      g_slow.mark("ensure_workspace");
       CK(cudaGetLastError());
       const float* src = fields + f0 * g.n;
       const size_t in_bytes = sizeof(float) * g.n * nb;
@@ -1204,6 +1227,7 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
         return fail(c, EBCC_E_INGEST, "non-finite value in the input");
       }
       if (s != EBCC_OK) status = s;
+      g_slow.mark("batch_searches");
       // pack this batch now: the stream buffers are reused by the next batch
       int64_t bytes = done;
       for (int64_t z : bsizes) bytes += z;
@@ -1230,6 +1254,7 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
         CK(cudaStreamSynchronize(st));
       }
       sizes.insert(sizes.end(), bsizes.begin(), bsizes.end());
+      g_slow.mark("batch_pack");
     }
     int64_t total = 0;
     for (int64_t f = 0; f < nfields; f++) total += sizes[f];
