@@ -519,8 +519,14 @@ void encode_collect(ebcc_ctx* c, int nfields, bool residual, const std::vector<u
 void encode_pyramids(ebcc_ctx* c, int nfields, bool residual, int planes,
                      const std::vector<uint8_t>& active, std::vector<MachineOut>& mo,
                      std::vector<PlaneRec>& pl) {
+  // on the high-priority stream: the list machine needs whole SMs, and with
+  // concurrent work (lanes) it must win them as they drain
+  CK(cudaEventRecord(c->ev_a, c->stream));
+  CK(cudaStreamWaitEvent(c->side, c->ev_a, 0));
   encode_launch(c, nfields, residual, planes, c->ws.A, residual ? c->ws.packed2 : c->ws.packed,
-                active, c->stream);
+                active, c->side);
+  CK(cudaEventRecord(c->ev_b, c->side));
+  CK(cudaStreamWaitEvent(c->stream, c->ev_b, 0));
   encode_collect(c, nfields, residual, active, mo, pl, c->stream);
 }
 
