@@ -665,6 +665,13 @@ void accumulate_level0(ebcc_ctx* c, bool timed) {
   }
 }
 
+// chunks per device batch: bounded by free HBM (and EBCC_MAX_BATCH, which the
+// tests use to exercise the multi-batch path)
+int64_t max_batch() {
+  static const int64_t m = getenv("EBCC_MAX_BATCH") ? atoll(getenv("EBCC_MAX_BATCH")) : 4096;
+  return m < 1 ? 1 : m;
+}
+
 // feasibility-only probes may skip settled CTAs (EBCC_EARLY=0 disables)
 bool early_ok() {
   static const bool on = !(getenv("EBCC_EARLY") && getenv("EBCC_EARLY")[0] == '0');
@@ -1194,6 +1201,7 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
     if (cap < 1) cap = 1;
     if (cap > nfields) cap = nfields;
     if (cap > 4096) cap = 4096;
+    if (cap > max_batch()) cap = max_batch();
     cudaEvent_t t0, t1;
     cudaEventCreate(&t0);
     cudaEventCreate(&t1);
@@ -1533,6 +1541,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
     if (cap < 1) cap = 1;
     if (cap > nfields) cap = nfields;
     if (cap > 4096) cap = 4096;
+    if (cap > max_batch()) cap = max_batch();
     for (int64_t f0 = 0; f0 < nfields; f0 += cap) {
       int nb = (int)std::min<int64_t>(cap, nfields - f0);
       ensure_workspace(c, g, nb);

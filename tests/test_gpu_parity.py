@@ -4,11 +4,14 @@ coefficients compared as bytes, streams and containers byte for byte.
 """
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
 
 import golden_inputs as gi
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -251,3 +254,31 @@ def test_ingest_errors_from_device(ebcc):
     with pytest.raises(ebcc.IngestError) as ei:
         ebcc.compress(b)
     assert ei.value.index == (19, 29)
+
+
+@pytest.mark.gpu
+def test_multi_batch_path_equals_single_batch(tmp_path):
+    """Chunks split over several device batches (EBCC_MAX_BATCH, as when HBM
+    bounds the batch) give the same container and decoded array."""
+    import subprocess
+    import sys
+    script = r'''
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, "%s")
+import paper_2510_22265_b200 as ebcc
+from paper_2510_22265_b200 import fields
+a = np.stack([fields.small_field(k, 48, 80, s) for s in range(3)
+              for k in ("smooth", "precip", "noise")])[None]
+blob = ebcc.compress(a, 0.01)
+out = ebcc.decompress(blob)
+print(hashlib.sha256(blob).hexdigest(), hashlib.sha256(out.tobytes()).hexdigest())
+''' % REPO
+    res = {}
+    for mb in ("4096", "2"):
+        env = dict(os.environ, EBCC_MAX_BATCH=mb)
+        r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[mb] = r.stdout.split()
+    assert res["4096"] == res["2"]
