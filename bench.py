@@ -53,50 +53,88 @@ def workload(rank: int = 0, levels: int = LEVELS) -> np.ndarray:
 
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    NVML queries from a background thread (one at start, then every
+    `period` s, one at stop); an `nvidia-smi -lms` poller is the fallback.
+    The poller perturbs this host-synchronised pipeline measurably (more
+    driver work per sample), so NVML at a modest rate is preferred.
+    """
 
-    def __init__(self, index: int = 0):
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
+
+    def __init__(self, index: int = 0, period: float = 0.1):
         self.index = index
-        self.rows = []
+        self.period = period
+        self.rows = []  # (sm_mhz, max_mhz, reason bits)
+        self.stop_ev = threading.Event()
+        self.thread = None
+        self.nvml = None
         self.proc = None
+
+    def _sample(self):
+        nv, h = self.nvml
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                          float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)), int(bits)))
+
+    def _loop(self):
+        while not self.stop_ev.wait(self.period):
+            self._sample()
 
     def start(self):
         try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml = (nv, nv.nvmlDeviceGetHandleByIndex(self.index))
+            self._sample()
+            self.thread = threading.Thread(target=self._loop, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
+        try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread = threading.Thread(target=self._read_smi, daemon=True)
             self.thread.start()
         except OSError:
             self.proc = None
 
-    def _read(self):
+    def _read_smi(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+            try:
+                self.rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+            except (ValueError, IndexError):
+                pass
 
     def stop(self) -> dict:
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4)
-                          if r[2 + k].lower() == "active"})
+        if self.nvml:
+            self.stop_ev.set()
+            self.thread.join(timeout=5)
+            self._sample()
+        elif self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = [r[0] for r in self.rows]
+        mx = [r[1] for r in self.rows]
+        reasons = sorted({name for r in self.rows for name, bit in self.REASONS if r[2] & bit})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
@@ -152,7 +190,8 @@ def run_ours(args, rank, world, local_rank):
     bound_ok = bool(np.all(err <= EPS * rng_))
 
     sampler = ClockSampler(local_rank)
-    sampler.start()
+    if os.environ.get("EBCC_BENCH_NO_CLOCKS") != "1":  # diagnostics only
+        sampler.start()
     t_c = t_d = 0.0
     launches = 0
     probe_ms = probe_steps = 0.0

@@ -331,6 +331,11 @@ struct ebcc_ctx {
   Workspace ws;
   // pinned staging for pageable host buffers (copied by a thread team)
   uint8_t* h_stage = nullptr;
+  // page-locked arena for the small host->device parameter copies of one
+  // call: a pageable source would make cudaMemcpyAsync wait for the stream,
+  // tying the host to the GPU at every copy
+  uint8_t* h_arena = nullptr;
+  size_t arena_cap = 0, arena_used = 0;
   int64_t h_stage_cap = 0;
   // last compress result
   uint8_t* d_payload = nullptr;
@@ -476,6 +481,8 @@ inline double us_since(SteadyClock::time_point t) {
   return std::chrono::duration<double, std::micro>(SteadyClock::now() - t).count();
 }
 
+void h2d_small(ebcc_ctx* c, void* dst, const void* src, size_t n, cudaStream_t st);
+
 // encode the pyramids in `coef` (all fields): exponents, machine (which
 // skips all-zero pyramids itself), refinement, packed metadata.  Async on st.
 void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const double* coef,
@@ -486,9 +493,9 @@ void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const do
   MachineBufs mb = machine_bufs(w, nfields, residual);
   std::vector<MachineOut> init(nfields);
   for (auto& m : init) { m = MachineOut{}; m.n_max = kExpNone; }
-  CK(cudaMemcpyAsync(mb.out, init.data(), sizeof(MachineOut) * nfields, cudaMemcpyHostToDevice, st));
+  h2d_small(c, mb.out, init.data(), sizeof(MachineOut) * nfields, st);
   CK(cudaMemsetAsync(mb.bits, 0, sizeof(uint32_t) * mb.bit_stride * nfields, st));
-  CK(cudaMemcpyAsync(w.active, active.data(), nfields, cudaMemcpyHostToDevice, st));
+  h2d_small(c, w.active, active.data(), nfields, st);
   coef_prepare(coef, w.g.n, mb, w.g, st);
   CK(cudaGetLastError());
   subtree_exponents(mb, w.g, w.tt, st);
@@ -610,6 +617,30 @@ EventTimer::~EventTimer() {
   float ms = 0;
   cudaEventElapsedTime(&ms, c->tm_a, c->tm_b);
   *acc += ms;
+}
+
+// async H2D of a small host array through the page-locked arena
+void arena_reset(ebcc_ctx* c) { c->arena_used = 0; }
+void h2d_small(ebcc_ctx* c, void* dst, const void* src, size_t n, cudaStream_t st) {
+  if (n == 0) return;
+  size_t at = (c->arena_used + 63) & ~size_t(63);
+  if (at + n > c->arena_cap) {
+    // everything staged so far must have been consumed before reuse
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->side) CK(cudaStreamSynchronize(c->side));
+    at = 0;
+    if (n > c->arena_cap) {
+      if (c->h_arena) CK(cudaFreeHost(c->h_arena));
+      c->h_arena = nullptr;
+      c->arena_cap = 0;
+      size_t cap = std::max<size_t>(n, 4u << 20);
+      CK(cudaMallocHost(&c->h_arena, cap));
+      c->arena_cap = cap;
+    }
+  }
+  memcpy(c->h_arena + at, src, n);
+  CK(cudaMemcpyAsync(dst, c->h_arena + at, n, cudaMemcpyHostToDevice, st));
+  c->arena_used = at + n;
 }
 
 uint8_t* host_stage(ebcc_ctx* c, int64_t bytes) {
@@ -1140,6 +1171,7 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->d_stage) cudaFree(c->d_stage);
   if (c->d_out) cudaFree(c->d_out);
   if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->h_arena) cudaFreeHost(c->h_arena);
   if (c->d_cont) cudaFree(c->d_cont);
   if (c->d_cmeta) cudaFree(c->d_cmeta);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -1260,8 +1292,7 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
           c->parts_cap = (int)bparts.size() * 2;
           c->d_parts = dalloc<PackPart>(c->parts_cap);
         }
-        CK(cudaMemcpyAsync(c->d_parts, bparts.data(), sizeof(PackPart) * bparts.size(),
-                           cudaMemcpyHostToDevice, st));
+        h2d_small(c, c->d_parts, bparts.data(), sizeof(PackPart) * bparts.size(), st);
         pack_parts(c->d_parts, (int)bparts.size(), c->d_payload, st);
         c->stats.kernel_launches++;
         CK(cudaGetLastError());
@@ -1342,6 +1373,7 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
   if ((int64_t)rows * cols >= (1ll << 31)) return fail(c, EBCC_E_ARGUMENT, "chunk too large");
   c->err.clear();
   c->err_index = -1;
+  arena_reset(c);  // the previous call ended synchronised
   try {
     CK(cudaSetDevice(c->device));
     const int L = lanes_for(nfields);
@@ -1526,6 +1558,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
     return fail(c, EBCC_E_ARGUMENT, "bad arguments");
   c->stats = ebcc_stats{};
   c->err.clear();
+  arena_reset(c);  // the previous call ended synchronised
   try {
     CK(cudaSetDevice(c->device));
     cudaStream_t st = c->stream;
@@ -1607,7 +1640,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
             (ract[i] && (int64_t)((r.resid_len - kHeader + 3) / 4) + 2 > w.words_res))
           return fail(c, EBCC_E_FORMAT, "stream longer than any encoder output");
       }
-      CK(cudaMemcpyAsync(w.fs, fsv.data(), sizeof(FieldScal) * nb, cudaMemcpyHostToDevice, st));
+      h2d_small(c, w.fs, fsv.data(), sizeof(FieldScal) * nb, st);
       if (hi > lo) {
         int64_t span = hi - lo;
         if (span > c->stage_cap) {
@@ -1624,8 +1657,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           c->unpack_cap = (int)up.size() * 2;
           c->d_unpack = dalloc<UnpackPart>(c->unpack_cap);
         }
-        CK(cudaMemcpyAsync(c->d_unpack, up.data(), sizeof(UnpackPart) * up.size(),
-                           cudaMemcpyHostToDevice, st));
+        h2d_small(c, c->d_unpack, up.data(), sizeof(UnpackPart) * up.size(), st);
         unpack_parts(c->d_unpack, (int)up.size(), c->d_stage, st);
         c->stats.kernel_launches++;
       }
@@ -1648,14 +1680,13 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         for (int i = 0; i < nb; i++) any |= act[i] != 0;
         if (resl && !any) break;
         MachineBufs mb = machine_bufs(w, nb, resl);
-        CK(cudaMemcpyAsync(mb.out, resl ? rmo.data() : bmo.data(), sizeof(MachineOut) * nb,
-                           cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(w.limit, resl ? rlim.data() : blim.data(), sizeof(uint64_t) * nb,
-                           cudaMemcpyHostToDevice, st));
+        h2d_small(c, mb.out, resl ? rmo.data() : bmo.data(), sizeof(MachineOut) * nb, st);
+        h2d_small(c, const_cast<uint64_t*>(w.limit), resl ? rlim.data() : blim.data(),
+                  sizeof(uint64_t) * nb, st);
         std::vector<uint8_t> mact(nb);
         for (int i = 0; i < nb; i++)
           mact[i] = act[i] && (resl ? rmo[i].n_max : bmo[i].n_max) != kExpNone;
-        CK(cudaMemcpyAsync(w.active, mact.data(), nb, cudaMemcpyHostToDevice, st));
+        h2d_small(c, w.active, mact.data(), nb, st);
         decode_init(mb, st);
         run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
         gather_refinement(mb, st);
@@ -1668,7 +1699,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           prm[i].midpoint = resl ? 1 : 0;
           prm[i].active = resl ? act[i] : !cst[i];
         }
-        CK(cudaMemcpyAsync(w.prm, prm.data(), sizeof(ProbeParam) * nb, cudaMemcpyHostToDevice, st));
+        h2d_small(c, w.prm, prm.data(), sizeof(ProbeParam) * nb, st);
         Meta m = meta_of(w, resl);
         if (!resl) {
           decode_field(m, w.prm, w.A, w.B, g, nb, w.base_dec, st);
@@ -1678,10 +1709,9 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         c->stats.kernel_launches += g.levels;
         CK(cudaGetLastError());
       }
-      CK(cudaMemcpyAsync(w.active, pure.data(), nb, cudaMemcpyHostToDevice, st));
+      h2d_small(c, w.active, pure.data(), nb, st);
       denorm_only(w.base_dec, w.fs, w.active, g.n, nb, out_dev, st);
-      CK(cudaStreamSynchronize(st));
-      CK(cudaMemcpyAsync(w.active, cst.data(), nb, cudaMemcpyHostToDevice, st));
+      h2d_small(c, w.active, cst.data(), nb, st);  // stream-ordered after denorm_only
       fill_constant(w.fs, w.active, g.n, nb, out_dev, st);
       c->stats.kernel_launches += 2;
       CK(cudaGetLastError());
