@@ -357,6 +357,8 @@ struct ebcc_ctx {
   cudaStream_t side = nullptr;   // high-priority stream for the overlapped residual encode
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr;  // fork/join of the joint probe step
+  cudaEvent_t cev0 = nullptr, cev1 = nullptr;    // per-call timing (batch loop)
+  cudaEvent_t oev0 = nullptr, oev1 = nullptr;    // per-call timing (ebcc_compress)
   cudaEvent_t tm_a = nullptr, tm_b = nullptr;
   std::vector<ebcc_ctx*> lanes;  // child contexts for concurrent sub-batches
 };
@@ -467,6 +469,7 @@ struct SlowLog {
     if (const char* e = getenv("EBCC_SLOWLOG")) thr = atof(e);
     last = std::chrono::steady_clock::now();
   }
+  bool on() const { return thr >= 0; }
   void mark(const char* what, int i = -1) {
     if (thr < 0) return;
     auto now = std::chrono::steady_clock::now();
@@ -702,6 +705,10 @@ int64_t max_batch() {
   static const int64_t m = getenv("EBCC_MAX_BATCH") ? atoll(getenv("EBCC_MAX_BATCH")) : 4096;
   return m < 1 ? 1 : m;
 }
+
+// chunks per batch: free-memory bound, queried only when the workspace does
+// not already cover the call (cudaMemGetInfo can stall for milliseconds)
+int64_t batch_cap(ebcc_ctx* c, const Geo& g, int64_t nfields, double share);
 
 // feasibility-only probes may skip settled CTAs (EBCC_EARLY=0 disables)
 bool early_ok() {
@@ -1148,6 +1155,10 @@ int ebcc_create(int32_t device, ebcc_ctx** out) {
     cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_f0, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_f1, cudaEventDisableTiming);
+    cudaEventCreate(&c->cev0);
+    cudaEventCreate(&c->cev1);
+    cudaEventCreate(&c->oev0);
+    cudaEventCreate(&c->oev1);
     cudaEventCreate(&c->ev_s0);
     cudaEventCreate(&c->ev_s1);
     cudaEventCreate(&c->tm_a);
@@ -1182,6 +1193,8 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->ev_b) cudaEventDestroy(c->ev_b);
   if (c->ev_f0) cudaEventDestroy(c->ev_f0);
   if (c->ev_f1) cudaEventDestroy(c->ev_f1);
+  for (cudaEvent_t e : {c->cev0, c->cev1, c->oev0, c->oev1})
+    if (e) cudaEventDestroy(e);
   if (c->ev_s0) cudaEventDestroy(c->ev_s0);
   if (c->ev_s1) cudaEventDestroy(c->ev_s1);
   if (c->tm_a) cudaEventDestroy(c->tm_a);
@@ -1212,6 +1225,19 @@ int ebcc_get_stats(const ebcc_ctx* c, ebcc_stats* out) {
 namespace {
 // compress nfields chunks on one context; the packed payload is left in
 // c->d_payload (c->payload_total bytes), per-chunk sizes in `sizes`
+int64_t batch_cap(ebcc_ctx* c, const Geo& g, int64_t nfields, double share) {
+  int64_t want = std::min<int64_t>(std::min<int64_t>(nfields, 4096), max_batch());
+  if (want < 1) want = 1;
+  const Workspace& w = c->ws;
+  if (w.cap >= want && w.g.rows == g.rows && w.g.cols == g.cols && w.g.levels == g.levels)
+    return want;
+  size_t freeb = 0, totalb = 0;
+  CK(cudaMemGetInfo(&freeb, &totalb));
+  const int64_t per_field = g.n * 160 + 4096;  // ~160 B per point per chunk in flight
+  int64_t cap = (int64_t)((freeb * 0.6 * share) / per_field);
+  return cap < 1 ? 1 : (cap > want ? want : cap);
+}
+
 int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t rows, int32_t cols,
                   double eps_rel, double q, double r0, double search_tol, int32_t flags,
                   ebcc_chunk_rec* recs, std::vector<int64_t>& sizes, cudaEvent_t start_after,
@@ -1225,18 +1251,8 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
     if (start_after) CK(cudaStreamWaitEvent(st, start_after, 0));
     int levels = clamp_levels(rows, cols, default_levels(rows, cols));
     Geo g = make_geo(rows, cols, levels);
-    // batch capacity from free memory (~100 B per point per field in flight)
-    size_t freeb = 0, totalb = 0;
-    CK(cudaMemGetInfo(&freeb, &totalb));
-    int64_t per_field = g.n * 160 + 4096;
-    int64_t cap = (int64_t)((freeb * 0.6 * mem_share) / per_field);
-    if (cap < 1) cap = 1;
-    if (cap > nfields) cap = nfields;
-    if (cap > 4096) cap = 4096;
-    if (cap > max_batch()) cap = max_batch();
-    cudaEvent_t t0, t1;
-    cudaEventCreate(&t0);
-    cudaEventCreate(&t1);
+    const int64_t cap = batch_cap(c, g, nfields, mem_share);
+    cudaEvent_t t0 = c->cev0, t1 = c->cev1;
     cudaEventRecord(t0, st);
     std::vector<PackPart> parts;
     sizes.clear();
@@ -1310,8 +1326,6 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
     cudaEventElapsedTime(&ms, t0, t1);
     c->stats.ms_total = ms;
     c->stats.ms_other = ms - c->stats.ms_encode - c->stats.ms_probe;
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
     return status;
   } catch (CudaFail& e) {
     cudaGetLastError();
@@ -1380,9 +1394,7 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
     const int64_t n = (int64_t)rows * cols;
     std::vector<int64_t> sizes;
     int status = EBCC_OK;
-    cudaEvent_t t0, t1;
-    CK(cudaEventCreate(&t0));
-    CK(cudaEventCreate(&t1));
+    cudaEvent_t t0 = c->oev0, t1 = c->oev1;
     CK(cudaEventRecord(t0, c->stream));
     ebcc_stats total_stats{};
     if (L == 1) {
@@ -1445,8 +1457,6 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
     CK(cudaEventSynchronize(t1));
     float ms = 0;
     cudaEventElapsedTime(&ms, t0, t1);
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
     c->stats = total_stats;
     c->stats.ms_total = ms;
     c->stats.ms_other = ms - c->stats.ms_encode / L - c->stats.ms_probe / L;
@@ -1559,25 +1569,19 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
   c->stats = ebcc_stats{};
   c->err.clear();
   arena_reset(c);  // the previous call ended synchronised
+  g_slow.mark("dec_enter");
   try {
     CK(cudaSetDevice(c->device));
     cudaStream_t st = c->stream;
     Geo g = make_geo(rows, cols, levels);
-    cudaEvent_t t0, t1;
-    cudaEventCreate(&t0);
-    cudaEventCreate(&t1);
+    cudaEvent_t t0 = c->cev0, t1 = c->cev1;
     cudaEventRecord(t0, st);
-    size_t freeb = 0, totalb = 0;
-    CK(cudaMemGetInfo(&freeb, &totalb));
-    int64_t per_field = g.n * 160 + 4096;
-    int64_t cap = (int64_t)((freeb * 0.6) / per_field);
-    if (cap < 1) cap = 1;
-    if (cap > nfields) cap = nfields;
-    if (cap > 4096) cap = 4096;
-    if (cap > max_batch()) cap = max_batch();
+    const int64_t cap = batch_cap(c, g, nfields, 1.0);
+    g_slow.mark("dec_meminfo");
     for (int64_t f0 = 0; f0 < nfields; f0 += cap) {
       int nb = (int)std::min<int64_t>(cap, nfields - f0);
       ensure_workspace(c, g, nb);
+      g_slow.mark("dec_workspace");
       Workspace& w = c->ws;
       // gather this batch's payload bytes into a staging buffer
       int64_t lo = INT64_MAX, hi = 0;
@@ -1687,8 +1691,16 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         for (int i = 0; i < nb; i++)
           mact[i] = act[i] && (resl ? rmo[i].n_max : bmo[i].n_max) != kExpNone;
         h2d_small(c, w.active, mact.data(), nb, st);
+        if (g_slow.on()) {
+          CK(cudaStreamSynchronize(st));
+          g_slow.mark(resl ? "dec_prep_resid" : "dec_prep_base");
+        }
         decode_init(mb, st);
         run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
+        if (g_slow.on()) {
+          CK(cudaStreamSynchronize(st));
+          g_slow.mark(resl ? "dec_machine_resid" : "dec_machine_base");
+        }
         gather_refinement(mb, st);
         pack_meta(mb, resl ? w.packed2 : w.packed, st);
         c->stats.kernel_launches += 4;
@@ -1708,6 +1720,10 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         }
         c->stats.kernel_launches += g.levels;
         CK(cudaGetLastError());
+        if (g_slow.on()) {
+          CK(cudaStreamSynchronize(st));
+          g_slow.mark(resl ? "dec_field_resid" : "dec_field_base");
+        }
       }
       h2d_small(c, w.active, pure.data(), nb, st);
       denorm_only(w.base_dec, w.fs, w.active, g.n, nb, out_dev, st);
@@ -1733,8 +1749,6 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
     float ms = 0;
     cudaEventElapsedTime(&ms, t0, t1);
     c->stats.ms_total = ms;
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
     return EBCC_OK;
   } catch (CudaFail& e) {
     cudaGetLastError();
