@@ -342,10 +342,10 @@ def records_to_grid(dims, chunk_shape, recs: np.ndarray, offs: np.ndarray, data:
 
 
 def _validate_payload(data, off, blen, rlen, mode, rows, cols) -> int:
-    base = data[off: off + blen]
-    _, levels = _parse_sp(base, rows, cols, "base")
+    mv = memoryview(data)  # header checks without copying the streams
+    _, levels = _parse_sp(mv[off: off + blen], rows, cols, "base")
     if mode == int(Mode.TWO_LAYER) and rlen > 0:
-        _, rl = _parse_sp(data[off + blen: off + blen + rlen], rows, cols, "residual")
+        _, rl = _parse_sp(mv[off + blen: off + blen + rlen], rows, cols, "residual")
         if rl != levels:
             raise FormatError("residual stream levels differ from the base stream's", offset=3)
     if levels > 5:
