@@ -920,6 +920,14 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       T24[f] = p[kBasePlanes].start;
     }
     resid_ready = true;
+    if (pc.on) {
+      float e = 0;
+      cudaEventElapsedTime(&e, c->ev_s0, c->ev_s1);
+      char b[96];
+      snprintf(b, sizeof b, " resid_ready_after_steps=%lld resid_encode_gpu=%.2fms",
+               (long long)c->stats.probe_launches, e);
+      pc.log += b;
+    }
   };
   auto total_bytes = [&](int f, int pi) -> int64_t {
     uint64_t T = pi == 0 ? T24[f] : T32[f];
