@@ -158,8 +158,9 @@ def test_grids(ebcc, golden_chunks):
 def test_batched_equals_single(ebcc):
     """One batch of many chunks gives the same bytes as one call per chunk."""
     from paper_2510_22265_b200 import fields
+    # 20 chunks: large enough for the concurrent two-lane split
     stack = np.stack([fields.small_field(k, 40, 56, s) for s, k in
-                      enumerate(["smooth", "spiky", "precip", "noise"] * 3)])
+                      enumerate(["smooth", "spiky", "precip", "noise"] * 5)])
     whole = ebcc.compress(stack, 0.01)
     parts = [ebcc.compress(stack[i], 0.01) for i in range(len(stack))]
     from paper_2510_22265_b200.container import read_file
