@@ -361,6 +361,7 @@ struct ebcc_ctx {
   cudaEvent_t oev0 = nullptr, oev1 = nullptr;    // per-call timing (ebcc_compress)
   cudaEvent_t tm_a = nullptr, tm_b = nullptr;
   std::vector<ebcc_ctx*> lanes;  // child contexts for concurrent sub-batches
+  int machine_fields = 0;        // lanes: chunks whose machines run concurrently in total
 };
 
 namespace {
@@ -533,8 +534,9 @@ void encode_pyramids(ebcc_ctx* c, int nfields, bool residual, int planes,
   // concurrent work (lanes) it must win them as they drain
   CK(cudaEventRecord(c->ev_a, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_a, 0));
+  const int cluster = machine_cluster_size(false, std::max(nfields, c->machine_fields));
   encode_launch(c, nfields, residual, planes, c->ws.A, residual ? c->ws.packed2 : c->ws.packed,
-                active, c->side);
+                active, c->side, cluster);
   CK(cudaEventRecord(c->ev_b, c->side));
   CK(cudaStreamWaitEvent(c->stream, c->ev_b, 0));
   encode_collect(c, nfields, residual, active, mo, pl, c->stream);
@@ -1418,7 +1420,10 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
       // thread) runs the whole pipeline on a contiguous block of chunks, so
       // one lane's latency-bound list machine overlaps another's probes
       std::vector<ebcc_ctx*> ls(L);
-      for (int k = 0; k < L; k++) ls[k] = lane_ctx(c, k);
+      for (int k = 0; k < L; k++) {
+        ls[k] = lane_ctx(c, k);
+        ls[k]->machine_fields = (int)nfields;  // every lane's clusters resident at once
+      }
       std::vector<int64_t> lo(L + 1);
       for (int k = 0; k <= L; k++) lo[k] = nfields * k / L;
       std::vector<std::vector<int64_t>> lsz(L);

@@ -939,6 +939,9 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
              mp_tiles, mp_ent, mp_bucket, (unsigned long long)hlis, (unsigned long long)hlen);
 #endif
   }
+  // no CTA may exit while a peer can still read its shared memory (the last
+  // cluster scan reads every CTA's slots through DSMEM)
+  if (csize > 1) cl.sync();
 }
 
 // encoder refinement, word aligned.  Refinement bit of plane p for rank i

@@ -87,6 +87,9 @@ void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables& tt, cuda
 // cluster > 0 forces the CTAs per field (1..4); 0 picks by batch size
 void run_machine(bool decode, MachineBufs& mb, const Geo& g, const TreeTables& tt, int planes,
                  cudaStream_t st, int cluster = 0);
+// CTAs per chunk the machine uses when `concurrent_fields` chunks' clusters
+// must be resident at once (cudaOccupancyMaxActiveClusters; EBCC_MACHINE_CLUSTER)
+int machine_cluster_size(bool decode, int concurrent_fields);
 // encoder: the deferred LIP passes and old-LIS significance bits (fully
 // parallel over the LIP / LIS histories);
 // must run after run_machine(decode=false) and before write_refinement
