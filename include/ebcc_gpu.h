@@ -175,6 +175,8 @@ typedef struct {
   int64_t probe_launches;     /* probe steps (batched over fields)   */
   double ms_probe_kernel;     /* summed duration of the dominant probe kernels */
   int64_t probe_kernel_count;
+  int64_t probe_kernel_fields; /* chunks covered by those launches, summed */
+  int64_t lanes;               /* concurrent sub-batches the call used */
 } ebcc_stats;
 
 int ebcc_get_stats(const ebcc_ctx *ctx, ebcc_stats *out);

@@ -51,7 +51,8 @@ class Stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_int64), ("ms_total", ctypes.c_double),
                 ("ms_encode", ctypes.c_double), ("ms_probe", ctypes.c_double),
                 ("ms_other", ctypes.c_double), ("probe_launches", ctypes.c_int64),
-                ("ms_probe_kernel", ctypes.c_double), ("probe_kernel_count", ctypes.c_int64)]
+                ("ms_probe_kernel", ctypes.c_double), ("probe_kernel_count", ctypes.c_int64),
+                ("probe_kernel_fields", ctypes.c_int64), ("lanes", ctypes.c_int64)]
 
 
 _lib = None

@@ -690,12 +690,13 @@ struct StepGraph {
 };
 
 // level-0 kernel timing: only eager (uncaptured) steps record the events
-void accumulate_level0(ebcc_ctx* c, bool timed) {
+void accumulate_level0(ebcc_ctx* c, bool timed, int nfields) {
   if (!timed) return;
   float ms = 0;
   if (cudaEventElapsedTime(&ms, c->l0.a, c->l0.b) == cudaSuccess) {
     c->stats.ms_probe_kernel += ms;
     c->stats.probe_kernel_count++;
+    c->stats.probe_kernel_fields += nfields;
   } else {
     cudaGetLastError();
   }
@@ -859,7 +860,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     CK(cudaStreamSynchronize(st));
     auto tp2 = SteadyClock::now();
     g_sp.wait += std::chrono::duration<double, std::micro>(tp2 - tp1).count();
-    accumulate_level0(c, timed);
+    accumulate_level0(c, timed, nfields);
     base_results();
     g_sp.post += us_since(tp2);
     g_slow.mark("base_step", (int)g_sp.n);
@@ -1052,7 +1053,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     c->stats.kernel_launches += (anyp + anyt) * g.levels;
     c->stats.probe_launches++;
     CK(cudaStreamSynchronize(st));
-    accumulate_level0(c, timed);
+    accumulate_level0(c, timed, nfields);
     if (anyp) base_results();
     if (anyt) trunc_results();
     g_slow.mark(anyp && anyt ? "joint_step" : (anyp ? "pure_step" : "trunc_step"));
@@ -1366,6 +1367,7 @@ void add_stats(ebcc_stats& a, const ebcc_stats& b) {
   a.probe_launches += b.probe_launches;
   a.ms_probe_kernel += b.ms_probe_kernel;
   a.probe_kernel_count += b.probe_kernel_count;
+  a.probe_kernel_fields += b.probe_kernel_fields;
 }
 
 }  // namespace
@@ -1474,6 +1476,7 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
     float ms = 0;
     cudaEventElapsedTime(&ms, t0, t1);
     c->stats = total_stats;
+    c->stats.lanes = L;
     c->stats.ms_total = ms;
     c->stats.ms_other = ms - c->stats.ms_encode / L - c->stats.ms_probe / L;
     if (status != EBCC_OK) {
