@@ -32,7 +32,10 @@ namespace ebcc {
 
 namespace {
 
-constexpr int MT = 512;          // machine threads
+#ifndef EBCC_MT
+#define EBCC_MT 512
+#endif
+constexpr int MT = EBCC_MT;      // machine threads
 constexpr int MI = 4;            // entries per thread per tile
 constexpr int TILE = MT * MI;    // 2048
 constexpr int NW = MT / 32;
