@@ -274,8 +274,10 @@ struct Workspace {
   uint32_t *mant = nullptr, *sign_pos = nullptr, *lsp_rank = nullptr;
   uint8_t* pinfo = nullptr;
   uint8_t* hrel = nullptr;
-  uint4* packed = nullptr;
-  uint4* packed2 = nullptr;      // residual metadata (built while the pure search runs)
+  uint2* packed = nullptr;
+  uint2* packed2 = nullptr;      // residual metadata (built while the pure search runs)
+  uint32_t* sprank = nullptr;    // sign bit offsets by LSP rank (base / residual)
+  uint32_t* sprank2 = nullptr;
   double *A2 = nullptr, *B2 = nullptr;  // residual forward-DWT scratch
   uint64_t *lip = nullptr, *lis0 = nullptr, *lis1 = nullptr, *w0 = nullptr, *w1 = nullptr;
   uint32_t* lsp = nullptr;
@@ -301,7 +303,7 @@ struct Workspace {
   void release() {
     void* ptrs[] = {x32, norm, A, B, base_dec, ec, ed, el, mant, sign_pos, lsp_rank, pinfo, hrel,
                     packed, ninfo,
-                    packed2, A2, B2,
+                    packed2, sprank, sprank2, A2, B2,
                     lip, lis0, lis1, w0, w1, lsp, bits_base, bits_res, pl_base, pl_res,
                     mo_base, mo_res, fs, prm, res, tq_base, tq_res, limit, active, mm};
     for (void* p : ptrs)
@@ -388,8 +390,10 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   w.lsp_rank = dalloc<uint32_t>(N);
   w.pinfo = dalloc<uint8_t>(N);
   w.hrel = dalloc<uint8_t>((size_t)((g.n + 15) & ~15ll) * cap + 16);  // 16-B aligned per field
-  w.packed = dalloc<uint4>(N);
-  w.packed2 = dalloc<uint4>(N);
+  w.packed = dalloc<uint2>(N);
+  w.packed2 = dalloc<uint2>(N);
+  w.sprank = dalloc<uint32_t>(N);
+  w.sprank2 = dalloc<uint32_t>(N);
   w.A2 = dalloc<double>(N);
   w.B2 = dalloc<double>(N);
   w.lip = dalloc<uint64_t>(N);
@@ -444,6 +448,7 @@ MachineBufs machine_bufs(Workspace& w, int nfields, bool residual) {
 Meta meta_of(Workspace& w, bool residual) {
   Meta m{};
   m.packed = residual ? w.packed2 : w.packed;
+  m.sprank = residual ? w.sprank2 : w.sprank;
   m.planes = residual ? w.pl_res : w.pl_base;
   m.mo = residual ? w.mo_res : w.mo_base;
   m.stride = w.g.n;
@@ -490,7 +495,7 @@ void h2d_small(ebcc_ctx* c, void* dst, const void* src, size_t n, cudaStream_t s
 // encode the pyramids in `coef` (all fields): exponents, machine (which
 // skips all-zero pyramids itself), refinement, packed metadata.  Async on st.
 void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const double* coef,
-                   uint4* packed, const std::vector<uint8_t>& active, cudaStream_t st,
+                   bool packed_residual, const std::vector<uint8_t>& active, cudaStream_t st,
                    int cluster = 0) {
   Workspace& w = c->ws;
   CK(cudaGetLastError());  // surface anything deferred from before this encode
@@ -510,7 +515,8 @@ void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const do
   CK(cudaGetLastError());
   write_refinement(mb, planes, st);
   CK(cudaGetLastError());
-  pack_meta(mb, packed, st);
+  pack_meta(mb, packed_residual ? w.packed2 : w.packed, packed_residual ? w.sprank2 : w.sprank,
+            st);
   c->stats.kernel_launches += 9 + w.g.levels;
   CK(cudaGetLastError());
 }
@@ -535,8 +541,7 @@ void encode_pyramids(ebcc_ctx* c, int nfields, bool residual, int planes,
   CK(cudaEventRecord(c->ev_a, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_a, 0));
   const int cluster = machine_cluster_size(false, std::max(nfields, c->machine_fields));
-  encode_launch(c, nfields, residual, planes, c->ws.A, residual ? c->ws.packed2 : c->ws.packed,
-                active, c->side, cluster);
+  encode_launch(c, nfields, residual, planes, c->ws.A, residual, active, c->side, cluster);
   CK(cudaEventRecord(c->ev_b, c->side));
   CK(cudaStreamWaitEvent(c->stream, c->ev_b, 0));
   encode_collect(c, nfields, residual, active, mo, pl, c->stream);
@@ -896,7 +901,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   // off the critical path while overlapped: one CTA per field leaves
   // more SMs to the pure-search probes running beside it
   static const int rc = getenv("EBCC_RESID_CLUSTER") ? atoi(getenv("EBCC_RESID_CLUSTER")) : 1;
-  encode_launch(c, nfields, true, kDeepPlanes, w.A2, w.packed2, active, rs, overlap ? rc : 0);
+  encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, active, rs, overlap ? rc : 0);
   CK(cudaEventRecord(c->ev_s1, rs));
   CK(cudaEventRecord(c->ev_b, rs));
   if (!overlap) pc.mark("residual_encode(serial)");
@@ -1399,7 +1404,8 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
   if (!(q > 0.0 && q <= 1.0)) return fail(c, EBCC_E_ARGUMENT, "q must be in (0, 1]");
   if (r0 < 1.0) return fail(c, EBCC_E_ARGUMENT, "r0 must be >= 1");
   if (!(search_tol > 0.0)) return fail(c, EBCC_E_ARGUMENT, "search_tol must be positive");
-  if ((int64_t)rows * cols >= (1ll << 31)) return fail(c, EBCC_E_ARGUMENT, "chunk too large");
+  if ((int64_t)rows * cols > kMaxChunkPoints)
+    return fail(c, EBCC_E_ARGUMENT, "chunk too large (at most 2^26 - 2 points)");
   c->err.clear();
   c->err_index = -1;
   arena_reset(c);  // the previous call ended synchronised
@@ -1585,6 +1591,8 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
   if (!c || !recs || !out || nfields < 0 || rows < 1 || cols < 1 || levels < 1 ||
       levels > kMaxLevels)
     return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  if ((int64_t)rows * cols > kMaxChunkPoints)
+    return fail(c, EBCC_E_ARGUMENT, "chunk too large (at most 2^26 - 2 points)");
   c->stats = ebcc_stats{};
   c->err.clear();
   arena_reset(c);  // the previous call ended synchronised
@@ -1721,7 +1729,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           g_slow.mark(resl ? "dec_machine_resid" : "dec_machine_base");
         }
         gather_refinement(mb, st);
-        pack_meta(mb, resl ? w.packed2 : w.packed, st);
+        pack_meta(mb, resl ? w.packed2 : w.packed, resl ? w.sprank2 : w.sprank, st);
         c->stats.kernel_launches += 4;
         for (int i = 0; i < nb; i++) {
           prm[i] = ProbeParam{};
@@ -1807,6 +1815,7 @@ int ebcc_spiht_encode(ebcc_ctx* c, const double* coeffs, int32_t rows, int32_t c
   if (!c || !coeffs || !out || rows < 1 || cols < 1 || levels < 1 || levels > kMaxLevels ||
       planes < 1 || planes > kDeepPlanes || cap < kHeader)
     return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  if ((int64_t)rows * cols > kMaxChunkPoints) return fail(c, EBCC_E_ARGUMENT, "chunk too large");
   try {
     CK(cudaSetDevice(c->device));
     Geo g = make_geo(rows, cols, levels);
@@ -1841,6 +1850,7 @@ int ebcc_spiht_decode(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t pre
                       int32_t rows, int32_t cols, double* coeffs_out, int32_t* n_last) {
   if (!c || !data || !coeffs_out || !n_last || rows < 1 || cols < 1)
     return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  if ((int64_t)rows * cols > kMaxChunkPoints) return fail(c, EBCC_E_ARGUMENT, "chunk too large");
   if (len < kHeader || data[0] != 'S' || data[1] != 'P') return fail(c, EBCC_E_FORMAT, "bad header");
   int levels = data[3];
   uint32_t hr, hc;
@@ -1872,7 +1882,7 @@ int ebcc_spiht_decode(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t pre
     decode_init(mb, st);
     run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
     gather_refinement(mb, st);
-    pack_meta(mb, w.packed2, st);
+    pack_meta(mb, w.packed2, w.sprank2, st);
     ProbeParam p{};
     p.B = ~0ull; p.planes = -1; p.active = 1;
     CK(cudaMemcpyAsync(w.prm, &p, sizeof(p), cudaMemcpyHostToDevice, st));

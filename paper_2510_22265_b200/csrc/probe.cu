@@ -105,22 +105,29 @@ __global__ void decode_coeffs_kernel(Meta m, const ProbeParam* __restrict__ prm,
     n_last = planes > 0 ? n_max - (planes - 1) : n_max;
   }
   fused::build_thresholds(T, m.planes + (int64_t)f * kMaxPlaneRecs, planes, P.B);
-  __syncthreads();
   const int64_t fo = (int64_t)f * m.stride;
+  const uint32_t RB = fused::rank_bound(m.sprank + fo, m.mo[f].lsp_count, P.B);
+  __syncthreads();
   const double off = P.midpoint ? scalbn(0.5, n_last) : 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    out[(int64_t)f * n + i] = fused::decode_raw_scan(m.packed[fo + i], P.B, planes, n_max,
+    out[(int64_t)f * n + i] = fused::decode_raw_scan(m.packed[fo + i], RB, planes, n_max,
                                                      P.midpoint != 0, off, T);
 }
 
-__global__ void pack_meta_kernel(MachineBufs mb, uint4* packed) {
+// 8-byte probe records + sign offsets by rank (sprank preset to kNone)
+__global__ void pack_meta_kernel(MachineBufs mb, uint2* packed, uint32_t* sprank) {
   const int f = blockIdx.y;
   const int64_t fo = (int64_t)f * mb.stride;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < mb.stride;
-       i += (int64_t)gridDim.x * blockDim.x)
-    packed[fo + i] = make_uint4(mb.sign_pos[fo + i], mb.lsp_rank[fo + i], mb.mant[fo + i],
-                                mb.pinfo[fo + i]);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t sp = mb.sign_pos[fo + i];
+    const uint32_t pi = mb.pinfo[fo + i];
+    const uint32_t rank = sp == kNone ? kRankNone : mb.lsp_rank[fo + i];
+    packed[fo + i] = make_uint2(rank | ((pi & 0x3fu) << kRankBits),
+                                ((pi & 0x80u) << 24) | (mb.mant[fo + i] & 0x7fffffffu));
+    if (sp != kNone) sprank[fo + rank] = sp;
+  }
 }
 
 // ---- epilogues for the last (level-0 row) pass -----------------------------
@@ -379,8 +386,10 @@ void selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_
   selftest_div_kernel<<<148 * 8, 256, 0, st>>>(n, seed, bad);
 }
 
-void pack_meta(const MachineBufs& mb, uint4* packed, cudaStream_t st) {
-  pack_meta_kernel<<<dim3(grid_for(mb.stride, 1024), mb.nfields), 256, 0, st>>>(mb, packed);
+void pack_meta(const MachineBufs& mb, uint2* packed, uint32_t* sprank, cudaStream_t st) {
+  cudaMemsetAsync(sprank, 0xff, sizeof(uint32_t) * mb.stride * mb.nfields, st);
+  pack_meta_kernel<<<dim3(grid_for(mb.stride, 1024), mb.nfields), 256, 0, st>>>(mb, packed,
+                                                                                 sprank);
 }
 
 void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, int nfields,

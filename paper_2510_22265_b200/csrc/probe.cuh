@@ -40,8 +40,19 @@ struct ProbeResult {
 // Per-coefficient closed-form metadata packed for the probes: one 16-byte
 // load per coefficient = {sign bit offset, LSP rank, top-32 significand bits,
 // pinfo (plane index | sign << 7)}.
+// Per-coefficient probe record, 8 bytes (the dominant probe stream):
+//   x = LSP rank (26 bits; kRankNone = never placed) | significance plane << 26
+//   y = negative << 31 | the 31 significand bits after the leading one
+// The sign bit offset is not stored: it grows with the LSP rank, so "sign bit
+// read within B bits" is rank < R(B), R(B) found once per probe by a binary
+// search over the sign offsets in rank order (Meta::sprank).
+constexpr uint32_t kRankBits = 26;
+constexpr uint32_t kRankNone = (1u << kRankBits) - 1;
+constexpr int64_t kMaxChunkPoints = (int64_t)kRankNone - 1;
+
 struct Meta {  // one field = `stride` entries
-  const uint4* packed;
+  const uint2* packed;
+  const uint32_t* sprank;  // sign bit offset by LSP rank (kNone: sign not read)
   const PlaneRec* planes;
   const MachineOut* mo;
   int64_t stride;
@@ -49,13 +60,14 @@ struct Meta {  // one field = `stride` entries
   // rank-bucket table), built once per probe by inverse_fused's first kernel
   uint8_t* tq;
 };
-constexpr int kTqBytes = 64 * 4 + 2048;
+constexpr int kTqBytes = 64 * 4 + 2048 + 16;  // thresholds, bucket table, R(B)
+constexpr int kTqRankOffset = 64 * 4 + 2048;
 
 // GPU self-test: FMA-corrected exact divisions vs __ddiv_rn on n random cases
 void selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t st);
 
 // build Meta::packed from the machine's per-coefficient arrays
-void pack_meta(const MachineBufs& mb, uint4* packed, cudaStream_t st);
+void pack_meta(const MachineBufs& mb, uint2* packed, uint32_t* sprank, cudaStream_t st);
 
 // f32 input -> per-field vmin/vmax/constant flag/first non-finite index and
 // the float64 normalised field.  `mm` holds 2*nfields u32 + nfields u64.
