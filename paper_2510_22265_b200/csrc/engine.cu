@@ -293,6 +293,15 @@ struct Workspace {
   uint8_t* tq_res = nullptr;
   uint64_t* limit = nullptr;
   uint8_t* active = nullptr;
+  // decompress: a second decoder state so the residual stream decodes
+  // concurrently with the base stream (allocated on first use)
+  struct DecSet {
+    uint32_t *mant = nullptr, *sign_pos = nullptr, *lsp_rank = nullptr, *lsp = nullptr;
+    uint8_t* pinfo = nullptr;
+    uint64_t *lip = nullptr, *lis0 = nullptr, *lis1 = nullptr, *w0 = nullptr, *w1 = nullptr;
+    uint64_t* limit = nullptr;
+    uint8_t* active = nullptr;
+  } dec2;
   unsigned int* mm = nullptr;
   // pinned host mirrors of the per-step control arrays
   ProbeParam* h_prm = nullptr;
@@ -307,6 +316,10 @@ struct Workspace {
                     lip, lis0, lis1, w0, w1, lsp, bits_base, bits_res, pl_base, pl_res,
                     mo_base, mo_res, fs, prm, res, tq_base, tq_res, limit, active, mm};
     for (void* p : ptrs)
+      if (p) cudaFree(p);
+    void* d2[] = {dec2.mant, dec2.sign_pos, dec2.lsp_rank, dec2.lsp, dec2.pinfo, dec2.lip,
+                  dec2.lis0, dec2.lis1, dec2.w0, dec2.w1, dec2.limit, dec2.active};
+    for (void* p : d2)
       if (p) cudaFree(p);
     if (h_prm) cudaFreeHost(h_prm);
     if (h_res) cudaFreeHost(h_res);
@@ -442,6 +455,35 @@ MachineBufs machine_bufs(Workspace& w, int nfields, bool residual) {
   mb.out = residual ? w.mo_res : w.mo_base;
   mb.limit = w.limit;
   mb.active = w.active;
+  return mb;
+}
+
+void ensure_dec2(Workspace& w) {
+  if (w.dec2.mant) return;
+  const size_t N = (size_t)w.g.n * w.cap;
+  w.dec2.mant = dalloc<uint32_t>(N);
+  w.dec2.sign_pos = dalloc<uint32_t>(N);
+  w.dec2.lsp_rank = dalloc<uint32_t>(N);
+  w.dec2.lsp = dalloc<uint32_t>(N);
+  w.dec2.pinfo = dalloc<uint8_t>(N);
+  w.dec2.lip = dalloc<uint64_t>(N);
+  w.dec2.lis0 = dalloc<uint64_t>(N);
+  w.dec2.lis1 = dalloc<uint64_t>(N);
+  w.dec2.w0 = dalloc<uint64_t>(N);
+  w.dec2.w1 = dalloc<uint64_t>(N);
+  w.dec2.limit = dalloc<uint64_t>(w.cap);
+  w.dec2.active = dalloc<uint8_t>(w.cap);
+}
+
+// the residual decoder's state (decompress)
+MachineBufs machine_bufs_dec2(Workspace& w, int nfields) {
+  MachineBufs mb = machine_bufs(w, nfields, true);
+  mb.mant = w.dec2.mant; mb.sign_pos = w.dec2.sign_pos; mb.lsp_rank = w.dec2.lsp_rank;
+  mb.pinfo = w.dec2.pinfo; mb.lsp = w.dec2.lsp;
+  mb.lip = w.dec2.lip; mb.lis0 = w.dec2.lis0; mb.lis1 = w.dec2.lis1;
+  mb.w0 = w.dec2.w0; mb.w1 = w.dec2.w1;
+  mb.limit = w.dec2.limit;
+  mb.active = w.dec2.active;
   return mb;
 }
 
@@ -1624,6 +1666,22 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
       std::vector<uint64_t> blim(nb, 0), rlim(nb, 0);
       std::vector<uint8_t> bact(nb, 0), ract(nb, 0), pure(nb, 0), cst(nb, 0);
       std::vector<FieldScal> fsv(nb);
+      // stream headers of device-resident payloads: all copied, one wait
+      uint8_t* hdrs = nullptr;
+      if (flags & EBCC_INPUT_ON_DEVICE) {
+        hdrs = host_stage(c, (int64_t)2 * kHeader * nb);
+        for (int i = 0; i < nb; i++) {
+          const ebcc_chunk_rec& r = recs[f0 + i];
+          if (r.mode == EBCC_MODE_CONSTANT || r.base_len < kHeader) continue;
+          CK(cudaMemcpyAsync(hdrs + 2 * kHeader * i, payload + offsets[f0 + i], kHeader,
+                             cudaMemcpyDeviceToHost, st));
+          if (r.mode == EBCC_MODE_TWO_LAYER && r.resid_len >= kHeader)
+            CK(cudaMemcpyAsync(hdrs + 2 * kHeader * i + kHeader,
+                               payload + offsets[f0 + i] + r.base_len, kHeader,
+                               cudaMemcpyDeviceToHost, st));
+        }
+        CK(cudaStreamSynchronize(st));
+      }
       for (int i = 0; i < nb; i++) {
         const ebcc_chunk_rec& r = recs[f0 + i];
         fsv[i] = FieldScal{};
@@ -1634,14 +1692,8 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         if (r.mode == EBCC_MODE_CONSTANT) { cst[i] = 1; continue; }
         if (r.base_len < kHeader || (r.mode == EBCC_MODE_TWO_LAYER && r.resid_len > 0 && r.resid_len < kHeader))
           return fail(c, EBCC_E_FORMAT, "stream shorter than header");
-        const uint8_t* bh = nullptr;
-        uint8_t hb[kHeader], hr[kHeader];
-        if (flags & EBCC_INPUT_ON_DEVICE) {
-          CK(cudaMemcpy(hb, payload + offsets[f0 + i], kHeader, cudaMemcpyDeviceToHost));
-          bh = hb;
-        } else {
-          bh = payload + offsets[f0 + i];
-        }
+        const uint8_t* bh = (flags & EBCC_INPUT_ON_DEVICE) ? hdrs + 2 * kHeader * i
+                                                            : payload + offsets[f0 + i];
         int nb_max = (int8_t)bh[2];
         bmo[i].n_max = nb_max == kZeroSentinel ? kExpNone : nb_max;
         blim[i] = (uint64_t)(r.base_len - kHeader) * 8;
@@ -1650,13 +1702,9 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
                                 (uint64_t)(r.base_len - kHeader),
                                 w.bits_base + (int64_t)i * w.words_base});
         if (r.mode == EBCC_MODE_TWO_LAYER && r.resid_len > 0) {
-          const uint8_t* rh;
-          if (flags & EBCC_INPUT_ON_DEVICE) {
-            CK(cudaMemcpy(hr, payload + offsets[f0 + i] + r.base_len, kHeader, cudaMemcpyDeviceToHost));
-            rh = hr;
-          } else {
-            rh = payload + offsets[f0 + i] + r.base_len;
-          }
+          const uint8_t* rh = (flags & EBCC_INPUT_ON_DEVICE)
+                                  ? hdrs + 2 * kHeader * i + kHeader
+                                  : payload + offsets[f0 + i] + r.base_len;
           int rn = (int8_t)rh[2];
           rmo[i].n_max = rn == kZeroSentinel ? kExpNone : rn;
           rlim[i] = (uint64_t)(r.resid_len - kHeader) * 8;
@@ -1703,54 +1751,71 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         }
         out_dev = c->d_out;
       }
-      // two decodes: base (lower bound) then residual (midpoint)
-      for (int layer = 0; layer < 2; layer++) {
-        bool resl = layer == 1;
-        std::vector<uint8_t>& act = resl ? ract : bact;
-        bool any = false;
-        for (int i = 0; i < nb; i++) any |= act[i] != 0;
-        if (resl && !any) break;
-        MachineBufs mb = machine_bufs(w, nb, resl);
-        h2d_small(c, mb.out, resl ? rmo.data() : bmo.data(), sizeof(MachineOut) * nb, st);
-        h2d_small(c, const_cast<uint64_t*>(w.limit), resl ? rlim.data() : blim.data(),
-                  sizeof(uint64_t) * nb, st);
+      // two decodes: the residual stream (midpoint) on the high-priority side
+      // stream with its own decoder state, concurrently with the base stream
+      // (lower bound) on `st`; joined before the residual field is added to
+      // the base field
+      bool any_res = false;
+      for (int i = 0; i < nb; i++) any_res |= ract[i] != 0;
+      if (any_res) {
+        ensure_dec2(w);
+        MachineBufs rb = machine_bufs_dec2(w, nb);
+        CK(cudaEventRecord(c->ev_a, st));  // streams unpacked
+        CK(cudaStreamWaitEvent(c->side, c->ev_a, 0));
+        h2d_small(c, rb.out, rmo.data(), sizeof(MachineOut) * nb, c->side);
+        h2d_small(c, w.dec2.limit, rlim.data(), sizeof(uint64_t) * nb, c->side);
         std::vector<uint8_t> mact(nb);
-        for (int i = 0; i < nb; i++)
-          mact[i] = act[i] && (resl ? rmo[i].n_max : bmo[i].n_max) != kExpNone;
+        for (int i = 0; i < nb; i++) mact[i] = ract[i] && rmo[i].n_max != kExpNone;
+        h2d_small(c, w.dec2.active, mact.data(), nb, c->side);
+        decode_init(rb, c->side);
+        // one CTA per chunk: fits beside the base machine's clusters
+        run_machine(true, rb, g, w.tt, kMaxDecodePlanes, c->side, 1);
+        gather_refinement(rb, c->side);
+        pack_meta(rb, w.packed2, w.sprank2, c->side);
+        CK(cudaEventRecord(c->ev_b, c->side));
+        c->stats.kernel_launches += 4;
+      }
+      {
+        MachineBufs mb = machine_bufs(w, nb, false);
+        h2d_small(c, mb.out, bmo.data(), sizeof(MachineOut) * nb, st);
+        h2d_small(c, const_cast<uint64_t*>(w.limit), blim.data(), sizeof(uint64_t) * nb, st);
+        std::vector<uint8_t> mact(nb);
+        for (int i = 0; i < nb; i++) mact[i] = bact[i] && bmo[i].n_max != kExpNone;
         h2d_small(c, w.active, mact.data(), nb, st);
-        if (g_slow.on()) {
-          CK(cudaStreamSynchronize(st));
-          g_slow.mark(resl ? "dec_prep_resid" : "dec_prep_base");
-        }
         decode_init(mb, st);
         run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
-        if (g_slow.on()) {
-          CK(cudaStreamSynchronize(st));
-          g_slow.mark(resl ? "dec_machine_resid" : "dec_machine_base");
-        }
         gather_refinement(mb, st);
-        pack_meta(mb, resl ? w.packed2 : w.packed, resl ? w.sprank2 : w.sprank, st);
+        pack_meta(mb, w.packed, w.sprank, st);
         c->stats.kernel_launches += 4;
         for (int i = 0; i < nb; i++) {
           prm[i] = ProbeParam{};
           prm[i].B = ~0ull;
           prm[i].planes = -1;
-          prm[i].midpoint = resl ? 1 : 0;
-          prm[i].active = resl ? act[i] : !cst[i];
+          prm[i].active = !cst[i];
         }
         h2d_small(c, w.prm, prm.data(), sizeof(ProbeParam) * nb, st);
-        Meta m = meta_of(w, resl);
-        if (!resl) {
-          decode_field(m, w.prm, w.A, w.B, g, nb, w.base_dec, st);
-        } else {
-          decode_field_add_denorm(m, w.prm, w.A, w.B, g, nb, w.base_dec, w.fs, out_dev, st);
-        }
+        decode_field(meta_of(w, false), w.prm, w.A, w.B, g, nb, w.base_dec, st);
         c->stats.kernel_launches += g.levels;
         CK(cudaGetLastError());
         if (g_slow.on()) {
           CK(cudaStreamSynchronize(st));
-          g_slow.mark(resl ? "dec_field_resid" : "dec_field_base");
+          g_slow.mark("dec_base");
         }
+      }
+      if (any_res) {
+        CK(cudaStreamWaitEvent(st, c->ev_b, 0));
+        for (int i = 0; i < nb; i++) {
+          prm[i] = ProbeParam{};
+          prm[i].B = ~0ull;
+          prm[i].planes = -1;
+          prm[i].midpoint = 1;
+          prm[i].active = ract[i];
+        }
+        h2d_small(c, w.prm, prm.data(), sizeof(ProbeParam) * nb, st);
+        decode_field_add_denorm(meta_of(w, true), w.prm, w.A, w.B, g, nb, w.base_dec, w.fs,
+                                out_dev, st);
+        c->stats.kernel_launches += g.levels;
+        CK(cudaGetLastError());
       }
       h2d_small(c, w.active, pure.data(), nb, st);
       denorm_only(w.base_dec, w.fs, w.active, g.n, nb, out_dev, st);
