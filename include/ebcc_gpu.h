@@ -177,6 +177,8 @@ typedef struct {
   int64_t probe_kernel_count;
   int64_t probe_kernel_fields; /* chunks covered by those launches, summed */
   int64_t lanes;               /* concurrent sub-batches the call used */
+  int64_t tiles_computed;      /* level-0 probe tiles recomputed (incremental probes) */
+  int64_t tiles_probed;        /* level-0 probe tiles the probes covered */
 } ebcc_stats;
 
 int ebcc_get_stats(const ebcc_ctx *ctx, ebcc_stats *out);

@@ -52,7 +52,8 @@ class Stats(ctypes.Structure):
                 ("ms_encode", ctypes.c_double), ("ms_probe", ctypes.c_double),
                 ("ms_other", ctypes.c_double), ("probe_launches", ctypes.c_int64),
                 ("ms_probe_kernel", ctypes.c_double), ("probe_kernel_count", ctypes.c_int64),
-                ("probe_kernel_fields", ctypes.c_int64), ("lanes", ctypes.c_int64)]
+                ("probe_kernel_fields", ctypes.c_int64), ("lanes", ctypes.c_int64),
+                ("tiles_computed", ctypes.c_int64), ("tiles_probed", ctypes.c_int64)]
 
 
 _lib = None

@@ -293,6 +293,16 @@ struct Workspace {
   uint8_t* tq_res = nullptr;
   uint64_t* limit = nullptr;
   uint8_t* active = nullptr;
+  // incremental probes (probe.cuh): per stream (0 base, 1 residual) the
+  // persistent LL levels, node by LSP rank, tile flags/results, plans, states
+  double* Linc[2] = {nullptr, nullptr};
+  uint32_t* lspn[2] = {nullptr, nullptr};
+  uint8_t* iflags[2] = {nullptr, nullptr};
+  TileStat* its[2] = {nullptr, nullptr};
+  IncPlan* iplan[2] = {nullptr, nullptr};
+  IncState* istate[2] = {nullptr, nullptr};
+  unsigned long long* icomputed = nullptr;  // [2][kMaxLevels]
+  int64_t inc_tiles = 0, inc_tiles0 = 0, inc_lstride = 0;
   // decompress: a second decoder state so the residual stream decodes
   // concurrently with the base stream (allocated on first use)
   struct DecSet {
@@ -317,6 +327,12 @@ struct Workspace {
                     mo_base, mo_res, fs, prm, res, tq_base, tq_res, limit, active, mm};
     for (void* p : ptrs)
       if (p) cudaFree(p);
+    for (int i = 0; i < 2; i++) {
+      void* ip[] = {Linc[i], lspn[i], iflags[i], its[i], iplan[i], istate[i]};
+      for (void* p : ip)
+        if (p) cudaFree(p);
+    }
+    if (icomputed) cudaFree(icomputed);
     void* d2[] = {dec2.mant, dec2.sign_pos, dec2.lsp_rank, dec2.lsp, dec2.pinfo, dec2.lip,
                   dec2.lis0, dec2.lis1, dec2.w0, dec2.w1, dec2.limit, dec2.active};
     for (void* p : d2)
@@ -433,6 +449,18 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   w.limit = dalloc<uint64_t>(cap);
   w.active = dalloc<uint8_t>(cap);
   w.mm = dalloc<unsigned int>(4 * cap + 2);
+  inc_capacity(g, &w.inc_tiles, &w.inc_tiles0);
+  w.inc_lstride = g.levels > 1 ? (int64_t)g.lr[1] * g.cols : 1;
+  for (int i = 0; i < 2; i++) {
+    w.Linc[i] = dalloc<double>((size_t)w.inc_lstride * cap);
+    w.lspn[i] = dalloc<uint32_t>(N);
+    w.iflags[i] = dalloc<uint8_t>((size_t)w.inc_tiles * cap);
+    w.its[i] = dalloc<TileStat>((size_t)w.inc_tiles0 * cap);
+    w.iplan[i] = dalloc<IncPlan>(cap);
+    w.istate[i] = dalloc<IncState>(cap);
+    CK(cudaMemset(w.iflags[i], kTileDirty, (size_t)w.inc_tiles * cap));
+  }
+  w.icomputed = dalloc<unsigned long long>(2 * kMaxLevels);
   CK(cudaMallocHost(&w.h_prm, sizeof(ProbeParam) * 2 * cap));
   CK(cudaMallocHost(&w.h_res, sizeof(ProbeResult) * 2 * cap));
   build_tree_tables(g, w.tt, c->stream);
@@ -558,7 +586,7 @@ void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const do
   write_refinement(mb, planes, st);
   CK(cudaGetLastError());
   pack_meta(mb, packed_residual ? w.packed2 : w.packed, packed_residual ? w.sprank2 : w.sprank,
-            st);
+            st, w.lspn[packed_residual ? 1 : 0]);
   c->stats.kernel_launches += 9 + w.g.levels;
   CK(cudaGetLastError());
 }
@@ -827,6 +855,33 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   Meta mbase = meta_of(w, false);
   StepGraph base_graph, trunc_graph, joint_graph;
 
+  // incremental probes: one state per stream, invalid at the batch start
+  static const bool inc_env = !(getenv("EBCC_INC") && getenv("EBCC_INC")[0] == '0');
+  static const int klim_div = getenv("EBCC_INC_KDIV") ? std::max(1, atoi(getenv("EBCC_INC_KDIV"))) : 16;
+  Inc inc_s[2];
+  bool inc_ok = inc_env;
+  for (int i = 0; i < 2; i++) {
+    Inc& I = inc_s[i];
+    I = Inc{};
+    inc_ok = inc_geometry(g, nfields, I) && inc_ok;
+    inc_ok = inc_ok && I.ig.tiles <= w.inc_tiles && I.ig.tiles0 <= w.inc_tiles0 &&
+             (g.levels == 1 || I.lstride <= w.inc_lstride);
+    I.flags = w.iflags[i];
+    I.plan = w.iplan[i];
+    I.state = w.istate[i];
+    I.ts = w.its[i];
+    I.lspn = w.lspn[i];
+    I.computed = w.icomputed + i * kMaxLevels;
+    I.klimit = (uint32_t)std::min<int64_t>(N / klim_div, 0xffffffffll);
+    static const int dbg = getenv("EBCC_INC_LOG") ? atoi(getenv("EBCC_INC_LOG")) : 0;
+    I.debug = dbg;
+    CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields, st));
+  }
+  CK(cudaMemsetAsync(w.icomputed, 0, sizeof(unsigned long long) * 2 * kMaxLevels, st));
+  const Inc* inc_base = inc_ok ? &inc_s[0] : nullptr;
+  const Inc* inc_res = inc_ok ? &inc_s[1] : nullptr;
+  int64_t tiles_probed = 0;  // level-0 tiles the probes cover (instrumentation)
+
   // ---- base quantile search ----
   // fill the pure-search requests (phase 1) or base-search requests (phase 0)
   std::vector<size_t> base_entries(nfields, 0);
@@ -874,13 +929,15 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       memcpy(&e.maxerr, &bitsv, 8);
       s.at[b] = (int)s.memo.size();
       s.memo.push_back(e);
+      tiles_probed += inc_s[0].ig.tiles0;
     }
   };
   auto enqueue_base = [&](bool eager) {
     CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
     fused::g_level0_timer = eager ? &c->l0 : nullptr;
-    probe_base(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.x32, w.fs, w.res, st);
+    probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32, w.fs,
+               w.res, st, inc_base);
     fused::g_level0_timer = nullptr;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
@@ -1036,7 +1093,8 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     CK(cudaMemcpyAsync(d_tprm, h_tprm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, ts));
     CK(cudaMemsetAsync(d_tres, 0, sizeof(ProbeResult) * nfields, ts));
     fused::g_level0_timer = eager ? &c->l0 : nullptr;
-    probe_trunc(mres, d_tprm, a, b, g, nfields, w.base_dec, w.x32, w.fs, d_tres, ts);
+    probe_trunc(mres, d_tprm, inc_res ? w.Linc[1] : a, b, g, nfields, w.base_dec, w.x32, w.fs,
+                d_tres, ts, inc_res);
     fused::g_level0_timer = nullptr;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h_tres, d_tres, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, ts));
@@ -1050,6 +1108,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       uint64_t bitsv = tres[f].maxerr;
       memcpy(&e, &bitsv, 8);
       s.trunc[s.tpending_planes][s.tpending] = e;
+      tiles_probed += inc_s[1].ig.tiles0;
     }
   };
   bool pure_phase_marked = false;
@@ -1107,6 +1166,12 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   }
   pc.mark("trunc_search");
   g_pc = nullptr;
+  if (inc_ok) {
+    unsigned long long comp[2 * kMaxLevels];
+    CK(cudaMemcpy(comp, w.icomputed, sizeof comp, cudaMemcpyDeviceToHost));
+    c->stats.tiles_computed += (int64_t)(comp[0] + comp[kMaxLevels]);
+    c->stats.tiles_probed += tiles_probed;
+  }
   if (pc.on) {
     char b[64];
     snprintf(b, sizeof b, " (host replay %.2fms)", replay_ms);
@@ -1291,7 +1356,7 @@ int64_t batch_cap(ebcc_ctx* c, const Geo& g, int64_t nfields, double share) {
     return want;
   size_t freeb = 0, totalb = 0;
   CK(cudaMemGetInfo(&freeb, &totalb));
-  const int64_t per_field = g.n * 160 + 4096;  // ~160 B per point per chunk in flight
+  const int64_t per_field = g.n * 176 + 4096;  // ~176 B per point per chunk in flight
   int64_t cap = (int64_t)((freeb * 0.6 * share) / per_field);
   return cap < 1 ? 1 : (cap > want ? want : cap);
 }
@@ -1415,6 +1480,8 @@ void add_stats(ebcc_stats& a, const ebcc_stats& b) {
   a.ms_probe_kernel += b.ms_probe_kernel;
   a.probe_kernel_count += b.probe_kernel_count;
   a.probe_kernel_fields += b.probe_kernel_fields;
+  a.tiles_computed += b.tiles_computed;
+  a.tiles_probed += b.tiles_probed;
 }
 
 }  // namespace

@@ -116,7 +116,8 @@ __global__ void decode_coeffs_kernel(Meta m, const ProbeParam* __restrict__ prm,
 }
 
 // 8-byte probe records + sign offsets by rank (sprank preset to kNone)
-__global__ void pack_meta_kernel(MachineBufs mb, uint2* packed, uint32_t* sprank) {
+__global__ void pack_meta_kernel(MachineBufs mb, uint2* packed, uint32_t* sprank,
+                                 uint32_t* lspn) {
   const int f = blockIdx.y;
   const int64_t fo = (int64_t)f * mb.stride;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < mb.stride;
@@ -126,7 +127,10 @@ __global__ void pack_meta_kernel(MachineBufs mb, uint2* packed, uint32_t* sprank
     const uint32_t rank = sp == kNone ? kRankNone : mb.lsp_rank[fo + i];
     packed[fo + i] = make_uint2(rank | ((pi & 0x3fu) << kRankBits),
                                 ((pi & 0x80u) << 24) | (mb.mant[fo + i] & 0x7fffffffu));
-    if (sp != kNone) sprank[fo + rank] = sp;
+    if (sp != kNone) {
+      sprank[fo + rank] = sp;
+      if (lspn) lspn[fo + rank] = (uint32_t)i;
+    }
   }
 }
 
@@ -149,6 +153,33 @@ __device__ __forceinline__ void warp_flush(ProbeResult* r, unsigned long long cn
   if ((threadIdx.x & 31) == 0) {
     if (do_count && cnt) atomicAdd(&r->count, cnt);
     atomicMax(&r->maxerr, mxb);
+  }
+}
+
+// incremental probes: the CTA's tile total -> TileStat, the tile's flag
+// (clean, or count stale when this probe did not count) and the result
+__device__ __forceinline__ void tile_flush(ProbeResult* r, TileStat* t, volatile uint8_t* flag,
+                                           unsigned long long cnt, double mx, bool do_count) {
+  __shared__ unsigned long long s_cnt, s_mx;
+  if (threadIdx.x == 0) { s_cnt = 0; s_mx = 0; }
+  __syncthreads();
+  unsigned long long mxb = (unsigned long long)__double_as_longlong(mx);
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    unsigned long long y = __shfl_xor_sync(0xffffffffu, mxb, o);
+    mxb = y > mxb ? y : mxb;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (do_count && cnt) atomicAdd(&s_cnt, cnt);
+    atomicMax(&s_mx, mxb);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    t->count = s_cnt;
+    t->maxerr = s_mx;
+    *flag = do_count ? 0 : kTileCountStale;
+    if (do_count && s_cnt) atomicAdd(&r->count, s_cnt);
+    atomicMax(&r->maxerr, s_mx);
   }
 }
 
@@ -182,6 +213,16 @@ struct BaseProbeEpi {
     mx = fmax(e, mx);
   }
   __device__ void finish(int f) { warp_flush(&res[f], cnt, mx, count); }
+  // incremental probes
+  static constexpr bool kFinal = true;
+  __device__ bool counting() const { return count; }
+  __device__ void add_stored(int f, const TileStat& t) {
+    if (count && t.count) atomicAdd(&res[f].count, t.count);
+    atomicMax(&res[f].maxerr, t.maxerr);
+  }
+  __device__ void finish_inc(int f, TileStat* t, volatile uint8_t* flag) {
+    tile_flush(&res[f], t, flag, cnt, mx, count);
+  }
 };
 
 struct TruncPre {
@@ -210,6 +251,12 @@ struct TruncProbeEpi {
     mx = fmax(e, mx);
   }
   __device__ void finish(int f) { warp_flush(&res[f], 0, mx, false); }
+  static constexpr bool kFinal = true;
+  __device__ bool counting() const { return false; }
+  __device__ void add_stored(int f, const TileStat& t) { atomicMax(&res[f].maxerr, t.maxerr); }
+  __device__ void finish_inc(int f, TileStat* t, volatile uint8_t* flag) {
+    tile_flush(&res[f], t, flag, 0, mx, false);
+  }
 };
 
 struct ResidueEpi {
@@ -386,10 +433,11 @@ void selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_
   selftest_div_kernel<<<148 * 8, 256, 0, st>>>(n, seed, bad);
 }
 
-void pack_meta(const MachineBufs& mb, uint2* packed, uint32_t* sprank, cudaStream_t st) {
+void pack_meta(const MachineBufs& mb, uint2* packed, uint32_t* sprank, cudaStream_t st,
+               uint32_t* lspn) {
   cudaMemsetAsync(sprank, 0xff, sizeof(uint32_t) * mb.stride * mb.nfields, st);
   pack_meta_kernel<<<dim3(grid_for(mb.stride, 1024), mb.nfields), 256, 0, st>>>(mb, packed,
-                                                                                 sprank);
+                                                                                 sprank, lspn);
 }
 
 void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, int nfields,
@@ -399,16 +447,62 @@ void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, i
 
 void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                 int nfields, const double* norm, const float* orig, const FieldScal* fs,
-                ProbeResult* res, cudaStream_t st) {
+                ProbeResult* res, cudaStream_t st, const Inc* inc) {
   BaseProbeEpi e{norm, orig, fs, prm, res, g.n, 0, 0.0, FieldScal{}};
-  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false);
+  if (inc) fused::inverse_inc(m, prm, *inc, a, g, nfields, st, e, false);
+  else fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false);
 }
 
 void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                  int nfields, const double* base_dec, const float* orig, const FieldScal* fs,
-                 ProbeResult* res, cudaStream_t st) {
+                 ProbeResult* res, cudaStream_t st, const Inc* inc) {
   TruncProbeEpi e{base_dec, orig, fs, prm, res, g.n, 0.0, FieldScal{}};
-  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, true);
+  if (inc) fused::inverse_inc(m, prm, *inc, a, g, nfields, st, e, true);
+  else fused::inverse_fused(m, prm, a, b, g, nfields, st, e, true);
+}
+
+// the level kernels' CTA tiling per level (fused::level_rows) and the
+// persistent LL layout: level k >= 1 at columns coloff[k].. of an
+// lr[1] x cols field, side by side
+bool inc_geometry(const Geo& g, int nfields, Inc& inc) {
+  IncGeo& ig = inc.ig;
+  ig = IncGeo{};
+  ig.levels = g.levels;
+  ig.cols = g.cols;
+  for (int k = 0; k <= kMaxLevels; k++) { ig.lr[k] = g.lr[k]; ig.lc[k] = g.lc[k]; }
+  int off = 0;
+  for (int k = 0; k < g.levels; k++) {
+    IncLevel& lv = ig.lv[k];
+    lv.R = g.lr[k];
+    lv.C = g.lc[k];
+    lv.th = fused::level_rows(g, k, nfields);
+    lv.ct = (lv.C + fused::TW - 1) / fused::TW;
+    lv.rt = (lv.R + lv.th - 1) / lv.th;
+    lv.off = off;
+    off += lv.ct * lv.rt;
+  }
+  ig.tiles = (off + 15) & ~15;
+  ig.tiles0 = ig.lv[0].ct * ig.lv[0].rt;
+  int c = 0;
+  for (int k = 1; k < g.levels; k++) {
+    inc.coloff[k] = c;
+    c += g.lc[k];
+  }
+  inc.lstride = g.levels > 1 ? (int64_t)g.lr[1] * g.cols : 0;
+  return c <= g.cols;
+}
+
+// worst-case flag / tile-stat sizes per field: the shortest tiles, which
+// fused::level_rows picks for a batch of one chunk
+void inc_capacity(const Geo& g, int64_t* tiles, int64_t* tiles0) {
+  int64_t t = 0;
+  for (int k = 0; k < g.levels; k++) {
+    const int th = fused::level_rows(g, k, 1);
+    int64_t n = (int64_t)((g.lc[k] + fused::TW - 1) / fused::TW) * ((g.lr[k] + th - 1) / th);
+    if (k == 0) *tiles0 = n;
+    t += n;
+  }
+  *tiles = (t + 15) & ~15ll;
 }
 
 void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,

@@ -63,11 +63,66 @@ struct Meta {  // one field = `stride` entries
 constexpr int kTqBytes = 64 * 4 + 2048 + 16;  // thresholds, bucket table, R(B)
 constexpr int kTqRankOffset = 64 * 4 + 2048;
 
+// ---- incremental probes ----------------------------------------------------
+// Consecutive probes of one chunk's search read B and B' stream bits of the
+// same stream.  A coefficient's decoded value changes only if its sign bit or
+// one of its refinement bits lies in [min(B,B'), max(B,B')): the LSP ranks of
+// the sign-offset range plus, per plane, one contiguous rank range of the
+// refinement segment.  Every IDWT level is deterministic, so an output tile
+// whose inputs did not change is bit-identical to the previous probe's: the
+// probe recomputes only the tiles reachable from the changed coefficients,
+// keeping each level's LL output (and level 0's per-tile count / max error)
+// from the previous probe of the same stream.
+constexpr int kIncMaxIv = kMaxPlaneRecs + 1;
+struct IncState {        // the last probe of this chunk on this stream
+  uint64_t B;
+  int32_t planes, midpoint, n_last, valid;
+};
+struct IncPlan {         // this probe: changed LSP ranks as intervals
+  int32_t full;          // recompute everything (no state, or too many changes)
+  int32_t niv;
+  uint32_t K;            // changed ranks in total
+  uint32_t pad;
+  uint32_t start[kIncMaxIv];
+  uint32_t pre[kIncMaxIv + 1];
+};
+struct TileStat {        // level-0 tile result of the last computation
+  unsigned long long count, maxerr;
+};
+// tile flag bits: the tile must be recomputed / its count is not valid
+constexpr uint8_t kTileDirty = 1, kTileCountStale = 2;
+struct IncLevel {        // the level kernel's CTA tiling of region k
+  int off;               // first flag of level k within a field's flags
+  int ct, rt, th;        // column tiles (TW columns each), row tiles, rows per tile
+  int R, C;
+};
+struct IncGeo {
+  int levels, tiles;     // tiles = flag bytes per field
+  int tiles0;            // level-0 tiles (TileStat entries per field)
+  int cols;
+  int lr[kMaxLevels + 1], lc[kMaxLevels + 1];
+  IncLevel lv[kMaxLevels];
+};
+struct Inc {
+  uint8_t* flags;              // per field: IncGeo::tiles
+  IncPlan* plan;               // per field
+  IncState* state;             // per field
+  TileStat* ts;                // per field: IncGeo::tiles0
+  const uint32_t* lspn;        // node by LSP rank (Meta::stride per field)
+  unsigned long long* computed;  // [kMaxLevels] tiles computed (instrumentation)
+  int64_t lstride;             // per-field stride of the persistent LL buffer
+  uint32_t klimit;             // more changed ranks than this: recompute in full
+  int32_t debug;               // EBCC_INC_LOG: per-probe plan of chunk 0 (printf)
+  int coloff[kMaxLevels + 1];  // column offset of level k's LL output in it
+  IncGeo ig;
+};
+
 // GPU self-test: FMA-corrected exact divisions vs __ddiv_rn on n random cases
 void selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t st);
 
 // build Meta::packed from the machine's per-coefficient arrays
-void pack_meta(const MachineBufs& mb, uint2* packed, uint32_t* sprank, cudaStream_t st);
+void pack_meta(const MachineBufs& mb, uint2* packed, uint32_t* sprank, cudaStream_t st,
+               uint32_t* lspn = nullptr);
 
 // f32 input -> per-field vmin/vmax/constant flag/first non-finite index and
 // the float64 normalised field.  `mm` holds 2*nfields u32 + nfields u64.
@@ -81,12 +136,17 @@ void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, i
 // base probe: decode (lower bound) -> IDWT -> count & max error
 void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                 int nfields, const double* norm, const float* orig, const FieldScal* fs,
-                ProbeResult* res, cudaStream_t st);
+                ProbeResult* res, cudaStream_t st, const Inc* inc = nullptr);
 
 // residual probe: decode (midpoint) -> IDWT -> + base -> max error
 void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                  int nfields, const double* base_dec, const float* orig, const FieldScal* fs,
-                 ProbeResult* res, cudaStream_t st);
+                 ProbeResult* res, cudaStream_t st, const Inc* inc = nullptr);
+
+// tiling of the incremental probes (the level kernels' CTA grids); false if
+// the persistent LL layout does not fit (the probes then run in full)
+bool inc_geometry(const Geo& g, int nfields, Inc& inc);
+void inc_capacity(const Geo& g, int64_t* tiles, int64_t* tiles0);
 
 // decode the chosen base prefix; write base_dec and resid = norm - base_dec
 void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
