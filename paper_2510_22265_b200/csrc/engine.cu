@@ -19,6 +19,7 @@
 // the order is observably identical, and running both base-memo searches
 // first lets the residual encode reuse the base coefficient metadata arrays.
 #include <algorithm>
+#include <atomic>
 #include <thread>
 #include <chrono>
 #include <cstdlib>
@@ -386,6 +387,10 @@ struct ebcc_ctx {
   ebcc_stats stats{};
   fused::Level0Timer l0;
   cudaStream_t side = nullptr;   // high-priority stream for the overlapped residual encode
+  cudaStream_t copy = nullptr;   // decompress: device->host copies of finished field groups
+  cudaEvent_t ev_copy = nullptr;
+  cudaEvent_t ev_in = nullptr;   // lanes: this lane's input copy has landed (CopyChain)
+  std::vector<cudaEvent_t> ev_groups;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr;  // fork/join of the joint probe step
   cudaEvent_t cev0 = nullptr, cev1 = nullptr;    // per-call timing (batch loop)
@@ -1278,6 +1283,7 @@ int ebcc_create(int32_t device, ebcc_ctx** out) {
     cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_f0, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_f1, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming);
     cudaEventCreate(&c->cev0);
     cudaEventCreate(&c->cev1);
     cudaEventCreate(&c->oev0);
@@ -1312,6 +1318,10 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->l0.a) cudaEventDestroy(c->l0.a);
   if (c->l0.b) cudaEventDestroy(c->l0.b);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->copy) cudaStreamDestroy(c->copy);
+  if (c->ev_copy) cudaEventDestroy(c->ev_copy);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  for (cudaEvent_t e : c->ev_groups) cudaEventDestroy(e);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
   if (c->ev_f0) cudaEventDestroy(c->ev_f0);
@@ -1361,10 +1371,26 @@ int64_t batch_cap(ebcc_ctx* c, const Geo& g, int64_t nfields, double share) {
   return cap < 1 ? 1 : (cap > want ? want : cap);
 }
 
+// lanes: their input copies run one after another (lane k's copy starts
+// when lane k-1's has finished), so lane 0 computes while lane 1's input is
+// still arriving instead of every lane waiting for the whole input
+struct CopyChain {
+  std::atomic<int> issued{0};  // lanes whose copy (and its event) are enqueued
+  std::vector<cudaEvent_t> done;
+};
+
 int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t rows, int32_t cols,
                   double eps_rel, double q, double r0, double search_tol, int32_t flags,
                   ebcc_chunk_rec* recs, std::vector<int64_t>& sizes, cudaEvent_t start_after,
-                  double mem_share) {
+                  double mem_share, CopyChain* chain = nullptr, int lane = 0) {
+  struct ChainRelease {  // a lane that fails before its copy must not stall the next
+    CopyChain* ch; int k; bool done = false;
+    ~ChainRelease() {
+      if (!ch || done) return;
+      while (ch->issued.load() < k) std::this_thread::yield();
+      ch->issued.store(k + 1);
+    }
+  } chain_release{chain, lane};
   c->stats = ebcc_stats{};
   c->err.clear();
   try {
@@ -1396,10 +1422,20 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
         src = reinterpret_cast<const float*>(stg);
       }
       CK(cudaGetLastError());
+      const bool chained = chain && f0 == 0 && !(flags & EBCC_INPUT_ON_DEVICE);
+      if (chained && lane > 0) {
+        while (chain->issued.load() < lane) std::this_thread::yield();
+        CK(cudaStreamWaitEvent(st, chain->done[lane - 1], 0));
+      }
       CK(cudaMemcpyAsync(c->ws.x32, src, in_bytes,
                          (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
                                                         : cudaMemcpyHostToDevice,
                          st));
+      if (chained) {
+        CK(cudaEventRecord(chain->done[lane], st));
+        chain->issued.store(lane + 1);
+        chain_release.done = true;
+      }
       std::vector<PackPart> bparts;
       int64_t done = 0;
       for (int64_t z : sizes) done += z;
@@ -1546,11 +1582,14 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
       std::vector<std::vector<int64_t>> lsz(L);
       std::vector<int> lst(L, EBCC_OK);
       std::vector<std::thread> th;
+      CopyChain chain;
+      for (int k = 0; k < L; k++) chain.done.push_back(ls[k]->ev_in);
       for (int k = 0; k < L; k++)
         th.emplace_back([&, k] {
           cudaSetDevice(c->device);
           lst[k] = compress_impl(ls[k], fields + lo[k] * n, lo[k + 1] - lo[k], rows, cols, eps_rel,
-                                 q, r0, search_tol, flags, recs + lo[k], lsz[k], t0, 1.0 / L);
+                                 q, r0, search_tol, flags, recs + lo[k], lsz[k], t0, 1.0 / L,
+                                 &chain, k);
         });
       for (auto& t : th) t.join();
       for (int k = 0; k < L; k++) {
@@ -1854,11 +1893,38 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         gather_refinement(mb, st);
         pack_meta(mb, w.packed, w.sprank, st);
         c->stats.kernel_launches += 4;
+      }
+      bool res_joined = false;  // st has waited for the residual decoder
+      // IDWT + denormalise in field groups; with a page-locked host
+      // destination each group's device->host copy (copy stream) overlaps
+      // the next group's IDWT
+      const bool to_host = !(flags & EBCC_OUTPUT_ON_DEVICE);
+      const bool pageable = to_host && is_pageable(dst);
+      static const int groups_env =
+          getenv("EBCC_DEC_GROUPS") ? std::max(1, atoi(getenv("EBCC_DEC_GROUPS"))) : 4;
+      const int G = (to_host && !pageable && nb >= 2 * groups_env) ? groups_env : 1;
+      if (G > 1 && !c->copy) {
+        CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming));
+      }
+      while ((int)c->ev_groups.size() < G) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_groups.push_back(e);
+      }
+      for (int j = 0; j < G; j++) {
+        const int a = (int)((int64_t)nb * j / G), b = (int)((int64_t)nb * (j + 1) / G);
+        bool g_res = false;
+        std::vector<uint8_t> gpure(nb, 0), gcst(nb, 0);
         for (int i = 0; i < nb; i++) {
+          const bool in = i >= a && i < b;
           prm[i] = ProbeParam{};
           prm[i].B = ~0ull;
           prm[i].planes = -1;
-          prm[i].active = !cst[i];
+          prm[i].active = in && !cst[i];
+          g_res |= in && ract[i];
+          gpure[i] = in && pure[i];
+          gcst[i] = in && cst[i];
         }
         h2d_small(c, w.prm, prm.data(), sizeof(ProbeParam) * nb, st);
         decode_field(meta_of(w, false), w.prm, w.A, w.B, g, nb, w.base_dec, st);
@@ -1868,31 +1934,42 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           CK(cudaStreamSynchronize(st));
           g_slow.mark("dec_base");
         }
-      }
-      if (any_res) {
-        CK(cudaStreamWaitEvent(st, c->ev_b, 0));
-        for (int i = 0; i < nb; i++) {
-          prm[i] = ProbeParam{};
-          prm[i].B = ~0ull;
-          prm[i].planes = -1;
-          prm[i].midpoint = 1;
-          prm[i].active = ract[i];
+        if (g_res) {
+          if (!res_joined) CK(cudaStreamWaitEvent(st, c->ev_b, 0));
+          res_joined = true;
+          for (int i = 0; i < nb; i++) {
+            prm[i] = ProbeParam{};
+            prm[i].B = ~0ull;
+            prm[i].planes = -1;
+            prm[i].midpoint = 1;
+            prm[i].active = i >= a && i < b && ract[i];
+          }
+          h2d_small(c, w.prm, prm.data(), sizeof(ProbeParam) * nb, st);
+          decode_field_add_denorm(meta_of(w, true), w.prm, w.A, w.B, g, nb, w.base_dec, w.fs,
+                                  out_dev, st);
+          c->stats.kernel_launches += g.levels;
+          CK(cudaGetLastError());
         }
-        h2d_small(c, w.prm, prm.data(), sizeof(ProbeParam) * nb, st);
-        decode_field_add_denorm(meta_of(w, true), w.prm, w.A, w.B, g, nb, w.base_dec, w.fs,
-                                out_dev, st);
-        c->stats.kernel_launches += g.levels;
+        h2d_small(c, w.active, gpure.data(), nb, st);
+        denorm_only(w.base_dec, w.fs, w.active, g.n, nb, out_dev, st);
+        h2d_small(c, w.active, gcst.data(), nb, st);  // stream-ordered after denorm_only
+        fill_constant(w.fs, w.active, g.n, nb, out_dev, st);
+        c->stats.kernel_launches += 2;
         CK(cudaGetLastError());
+        if (G > 1) {
+          CK(cudaEventRecord(c->ev_groups[j], st));
+          CK(cudaStreamWaitEvent(c->copy, c->ev_groups[j], 0));
+          CK(cudaMemcpyAsync(dst + (int64_t)a * g.n, out_dev + (int64_t)a * g.n,
+                             sizeof(float) * g.n * (b - a), cudaMemcpyDeviceToHost, c->copy));
+        }
       }
-      h2d_small(c, w.active, pure.data(), nb, st);
-      denorm_only(w.base_dec, w.fs, w.active, g.n, nb, out_dev, st);
-      h2d_small(c, w.active, cst.data(), nb, st);  // stream-ordered after denorm_only
-      fill_constant(w.fs, w.active, g.n, nb, out_dev, st);
-      c->stats.kernel_launches += 2;
-      CK(cudaGetLastError());
-      if (!(flags & EBCC_OUTPUT_ON_DEVICE)) {
+      if (any_res && !res_joined) CK(cudaStreamWaitEvent(st, c->ev_b, 0));
+      if (G > 1) {
+        CK(cudaEventRecord(c->ev_copy, c->copy));
+        CK(cudaStreamWaitEvent(st, c->ev_copy, 0));
+      } else if (to_host) {
         const size_t ob = sizeof(float) * g.n * nb;
-        if (is_pageable(dst)) {
+        if (pageable) {
           uint8_t* stg = host_stage(c, (int64_t)ob);
           CK(cudaMemcpyAsync(stg, out_dev, ob, cudaMemcpyDeviceToHost, st));
           CK(cudaStreamSynchronize(st));
