@@ -41,6 +41,10 @@ extern "C" {
 /* flags */
 #define EBCC_INPUT_ON_DEVICE 1   /* `fields` / `payload` are device pointers  */
 #define EBCC_OUTPUT_ON_DEVICE 2  /* `payload` / `out` are device pointers     */
+#define EBCC_FULL_SEARCH 4       /* compress: run every probe of the reference's
+                                    searches (no candidate pruning; same bytes,
+                                    n_base_probes / n_trunc_probes equal the
+                                    reference's probe counts)                 */
 
 /* Chunk modes (pipeline.py:38-41). */
 #define EBCC_MODE_CONSTANT 0

@@ -24,6 +24,7 @@ LIB_PATH = os.environ.get("EBCC_LIB") or os.path.join(HERE, "libebcc_gpu.so")
 OK, E_ARGUMENT, E_FORMAT, E_RESIDUAL, E_CAPACITY, E_CUDA, E_NOMEM, E_INGEST = range(8)
 INPUT_ON_DEVICE = 1
 OUTPUT_ON_DEVICE = 2
+FULL_SEARCH = 4  # compress: every probe of the reference's searches (no candidate pruning)
 
 # the exported symbols include/ebcc_gpu.h declares (checked by the CPU tests)
 EXPORTS = ("ebcc_abi_version", "ebcc_create", "ebcc_destroy", "ebcc_set_stream",

@@ -144,6 +144,12 @@ struct ChunkSearch {
   int64_t trunc_t = -1;
   int trunc_planes = 0;
   int n_trunc_calls = 0;
+  // Candidate pruning: bounds on the two candidates' sizes at the first
+  // replay miss (the bisections keep the answer inside their bracket and
+  // stream_len is non-decreasing).  -1 = unknown.
+  int64_t p_lb = 0, p_ub = -1;     // pure-base payload bytes
+  int64_t t_lb = 0, t_ub = -1;     // residual prefix bytes t
+  bool pure_pruned = false, trunc_pruned = false;
 
   int64_t clamp_budget(int64_t b) const {
     if (b > raw) b = raw;
@@ -233,7 +239,10 @@ struct ChunkSearch {
   // pipeline._search_pure (pipeline.py:215-236) -> budget or -1
   int64_t search_pure(size_t base_entries) {
     vsize = base_entries;
+    p_lb = kHeader;
+    p_ub = -1;
     if (pure_ok(kHeader)) return at_budget(kHeader).budget;
+    if (!missed) p_lb = kHeader + 1;
     if (!pure_ok(raw)) return -1;
     int64_t lo = kHeader, hi = raw;
     std::vector<int64_t> cached;
@@ -243,8 +252,19 @@ struct ChunkSearch {
       if (pure_ok(b)) hi = std::min(hi, b);
     for (int64_t b : cached)
       if (b < hi && !pure_ok(b)) lo = std::max(lo, b);
-    int64_t best = bisect(lo, hi, [&](int64_t b) { return pure_ok(b); });
-    return at_budget(best).budget;
+    // _bisect_min_feasible, noting the bracket (lo, hi] at the first miss
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) / 2;
+      const bool before = missed;
+      const bool ok = pure_ok(mid);
+      if (!before && missed) {
+        p_lb = stream_len(lo + 1);
+        p_ub = stream_len(hi);
+      }
+      if (ok) hi = mid;
+      else lo = mid;
+    }
+    return at_budget(hi).budget;
   }
 
   // pipeline._truncation_search for one planes variant -> t or -1
@@ -259,9 +279,24 @@ struct ChunkSearch {
       return it->second;
     };
     n_trunc_calls = 0;
+    t_lb = 0;
+    t_ub = -1;
     if (err_at(0) <= eps_abs) return 0;
     if (err_at(total) > eps_abs) return -1;
-    return bisect(0, total, [&](int64_t t) { return err_at(t) <= eps_abs; });
+    // this pass holds the answer: it lies in the bracket (lo, hi]
+    int64_t lo = 0, hi = total;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) / 2;
+      const bool before = missed;
+      const bool ok = err_at(mid) <= eps_abs;
+      if (!before && missed) {
+        t_lb = lo + 1;
+        t_ub = hi;
+      }
+      if (ok) hi = mid;
+      else lo = mid;
+    }
+    return hi;
   }
 };
 
@@ -801,6 +836,7 @@ bool early_ok() {
 
 // one compress batch of nfields (<= workspace capacity); x already in w.x32
 int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0, double tol,
+                   bool prune,
                    ebcc_chunk_rec* recs, int64_t out_base_off, std::vector<PackPart>& parts,
                    std::vector<int64_t>& sizes) {
   Workspace& w = c->ws;
@@ -1121,8 +1157,39 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     if (!resid_ready && cudaEventQuery(c->ev_b) == cudaSuccess) collect_residual();
     cudaGetLastError();  // a not-ready query is not an error
     auto h0 = SteadyClock::now();
-    const bool anyp = base_requests(1);
-    const bool anyt = resid_ready && trunc_requests();
+    bool anyp = base_requests(1);
+    bool anyt = resid_ready && trunc_requests();
+    if (prune && (anyp || anyt)) {
+      // candidate pruning (pipeline.py:315-329 picks min((len, 0|1))): stop
+      // a search whose candidate can no longer win; the chosen candidate and
+      // so the container bytes are unchanged
+      anyp = anyt = false;
+      for (int f = 0; f < nfields; f++) {
+        ChunkSearch& s = cs[f];
+        if (s.constant) continue;
+        const int64_t base_len = s.stream_len(s.base_budget);
+        const bool p_open = prm[f].active != 0, t_open = tprm[f].active != 0;
+        int64_t two_ub = -1, pure_ub = -1;
+        if (s.trunc_planes) two_ub = base_len + kHeader + s.trunc_t;
+        else if (t_open && s.t_ub >= 0) two_ub = base_len + kHeader + s.t_ub;
+        if (s.pure_done && s.pure_budget >= 0) pure_ub = s.stream_len(s.pure_budget);
+        else if (p_open && s.p_ub >= 0) pure_ub = s.p_ub;
+        const int64_t two_lb = base_len + kHeader + (t_open ? s.t_lb : 0);
+        if (p_open && two_ub >= 0 && s.p_lb > two_ub) {
+          s.pure_done = true;  // the two-layer candidate is strictly shorter
+          s.pure_budget = -1;
+          s.pure_pruned = true;
+          prm[f] = ProbeParam{};
+        } else if (t_open && pure_ub >= 0 && two_lb >= pure_ub) {
+          s.trunc_pruned = true;  // pure-base is no longer (ties go to pure-base)
+          s.trunc_t = -1;
+          pass[f] = 2;
+          tprm[f] = ProbeParam{};
+        }
+        anyp |= prm[f].active != 0;
+        anyt |= tprm[f].active != 0;
+      }
+    }
     replay_ms += std::chrono::duration<double, std::milli>(SteadyClock::now() - h0).count();
     if (!anyp && !pure_phase_marked) {
       pc.mark("pure_search");
@@ -1442,7 +1509,8 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
       std::vector<int64_t> bsizes;
       int s;
       try {
-        s = compress_batch(c, nb, eps_rel, q, r0, search_tol, recs + f0, done, bparts, bsizes);
+        s = compress_batch(c, nb, eps_rel, q, r0, search_tol, !(flags & EBCC_FULL_SEARCH),
+                           recs + f0, done, bparts, bsizes);
       } catch (IngestFail&) {
         c->err_index += f0 * g.n;
         return fail(c, EBCC_E_INGEST, "non-finite value in the input");

@@ -82,7 +82,7 @@ struct IncPlan {         // this probe: changed LSP ranks as intervals
   int32_t full;          // recompute everything (no state, or too many changes)
   int32_t niv;
   uint32_t K;            // changed ranks in total
-  uint32_t pad;
+  int32_t dense0;        // so many changes that every level-0 tile is taken as dirty
   uint32_t start[kIncMaxIv];
   uint32_t pre[kIncMaxIv + 1];
 };

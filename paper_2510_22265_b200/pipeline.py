@@ -46,20 +46,24 @@ def default_levels(rows: int, cols: int) -> int:
 # ---------------------------------------------------------------------------
 # batched device calls
 
-def compress_batch(stack: np.ndarray, params: EbccParams, ctx=None, fetch: bool = True):
+def compress_batch(stack: np.ndarray, params: EbccParams, ctx=None, fetch: bool = True,
+                   full_search: bool = False):
     """Compress a (n, rows, cols) float32 stack of chunks on the device.
 
     Returns (records[REC_DTYPE], offsets int64[n], payload uint8[total],
     status).  Raises ArgumentError for bad params; per-chunk
     ResidualInsufficient is reported through records['status'] and status.
     With ``fetch=False`` the payload stays on the device (payload is the int
-    total) for :meth:`_lib.Context.fetch_container`.
+    total) for :meth:`_lib.Context.fetch_container`.  ``full_search`` runs
+    every probe of the reference's searches (the default stops a search whose
+    candidate can no longer be chosen: same bytes, fewer probes).
     """
     ctx = ctx or _lib.context()
     stack = np.ascontiguousarray(stack, dtype=np.float32)
     n, rows, cols = stack.shape
     recs, offs, total, st = ctx.compress(stack, n, rows, cols, params.epsilon_rel, params.q,
-                                         params.r0, params.search_tol)
+                                         params.r0, params.search_tol,
+                                         flags=_lib.FULL_SEARCH if full_search else 0)
     if st not in (_lib.OK, _lib.E_RESIDUAL):
         ctx.raise_for(st, "ebcc_compress")
     if not fetch:

@@ -134,7 +134,8 @@ def test_probe_counts_match_reference(golden_chunks):
         if "error" in case or case["kind"] == "const":
             continue
         a = gi.chunk_input(case)
-        recs, _, _, st = compress_batch(a[None], EbccParams(case["eps"], case["q"]))
+        recs, _, _, st = compress_batch(a[None], EbccParams(case["eps"], case["q"]),
+                                        full_search=True)
         if st != 0:
             continue
         nb, nt = int(recs[0]["n_base_probes"]), int(recs[0]["n_trunc_probes"])
@@ -168,6 +169,30 @@ def test_batched_equals_single(ebcc):
     for i, blob in enumerate(parts):
         c1, _, _ = read_file(blob)
         assert c1[0].payload == chunks[i].payload
+
+
+@pytest.mark.parametrize("eps", [0.001, 0.01, 0.1])
+def test_candidate_pruning_keeps_bytes(ebcc, eps):
+    """Stopping a search whose candidate can no longer win (the default)
+    gives the same records and payload as running every probe of the
+    reference's searches (EBCC_FULL_SEARCH), with no more probes."""
+    from paper_2510_22265_b200 import fields
+    from paper_2510_22265_b200.chunk import EbccParams
+    from paper_2510_22265_b200.pipeline import compress_batch
+    stack = np.stack([fields.small_field(k, 96, 160, 100 + s) for s, k in
+                      enumerate(["smooth", "spiky", "precip", "noise"] * 5)])
+    stack = np.concatenate([stack, fields.temperature_like(96, 160, seed=7)[None],
+                            fields.precip_like(96, 160, seed=8)[None]])
+    p = EbccParams(eps)
+    r_fast, o_fast, pay_fast, st_fast = compress_batch(stack, p)
+    r_full, o_full, pay_full, st_full = compress_batch(stack, p, full_search=True)
+    assert st_fast == st_full
+    for key in ("mode", "base_len", "resid_len", "status"):
+        assert np.array_equal(r_fast[key], r_full[key]), key
+    assert np.array_equal(o_fast, o_full)
+    assert bytes(pay_fast) == bytes(pay_full)
+    assert np.all(r_fast["n_base_probes"] <= r_full["n_base_probes"])
+    assert np.all(r_fast["n_trunc_probes"] <= r_full["n_trunc_probes"])
 
 
 def test_large_golden(ebcc, golden_large):
