@@ -168,6 +168,12 @@ int ebcc_radial_spectrum(ebcc_ctx *ctx, const float *data, int64_t nfields, int3
  * random operands; *mismatches must be 0. */
 int ebcc_selftest_div(ebcc_ctx *ctx, int64_t n, uint64_t seed, int64_t *mismatches);
 
+/* Developer instrumentation: time full base probes (decode + inverse DWT +
+ * count / max-error reduction) of the last single-lane compress batch on
+ * this context at B = frac * (full base stream bits); averages over iters. */
+int ebcc_dev_probe_bench(ebcc_ctx *ctx, double frac, int32_t iters, int32_t early,
+                         double *us_level0, double *us_probe);
+
 /* Instrumentation for bench.py: kernels launched and device milliseconds
  * (CUDA events on the library stream) of the last call, split by stage. */
 typedef struct {

@@ -31,7 +31,8 @@ EXPORTS = ("ebcc_abi_version", "ebcc_create", "ebcc_destroy", "ebcc_set_stream",
            "ebcc_last_error", "ebcc_last_error_index", "ebcc_compress", "ebcc_fetch_payload", "ebcc_decompress",
            "ebcc_get_stats", "ebcc_dwt", "ebcc_spiht_encode", "ebcc_spiht_decode",
            "ebcc_selftest_div", "ebcc_fetch_container", "ebcc_host_alloc", "ebcc_host_free",
-           "ebcc_error_stats", "ebcc_error_histogram", "ebcc_ssim", "ebcc_radial_spectrum")
+           "ebcc_error_stats", "ebcc_error_histogram", "ebcc_ssim", "ebcc_radial_spectrum",
+           "ebcc_dev_probe_bench")
 
 
 class ChunkRec(ctypes.Structure):
@@ -92,6 +93,9 @@ def load(path: str = LIB_PATH):
         L.ebcc_spiht_encode.argtypes = [P, P, i32, i32, i32, i32, P, i64, ctypes.POINTER(i64)]
         L.ebcc_spiht_decode.argtypes = [P, P, i64, i64, i32, i32, P, ctypes.POINTER(i32)]
         L.ebcc_selftest_div.argtypes = [P, i64, ctypes.c_uint64, ctypes.POINTER(i64)]
+        L.ebcc_dev_probe_bench.argtypes = [P, ctypes.c_double, i32, i32,
+                                           ctypes.POINTER(ctypes.c_double),
+                                           ctypes.POINTER(ctypes.c_double)]
         L.ebcc_fetch_container.argtypes = [P, P, P, i64, P, i64, i32, ctypes.POINTER(i64)]
         L.ebcc_host_alloc.argtypes = [i64, ctypes.POINTER(P)]
         L.ebcc_host_free.argtypes = [P]
@@ -286,6 +290,15 @@ class Context:
         self.raise_for(st, "ebcc_spiht_decode")
         return out, (None if nl.value == -999 else nl.value)
 
+
+    def dev_probe_bench(self, frac: float, iters: int = 20, early: bool = False):
+        """Microseconds of the level-0 kernel and of the whole full base probe
+        (developer instrumentation; needs a single-lane compress first)."""
+        a, b = ctypes.c_double(0), ctypes.c_double(0)
+        st = self.lib.ebcc_dev_probe_bench(self.handle, float(frac), int(iters), int(early),
+                                           ctypes.byref(a), ctypes.byref(b))
+        self.raise_for(st, "ebcc_dev_probe_bench")
+        return a.value, b.value
 
     def selftest_div(self, n: int, seed: int = 1) -> int:
         bad = ctypes.c_int64(0)

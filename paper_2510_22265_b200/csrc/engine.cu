@@ -433,6 +433,7 @@ struct ebcc_ctx {
   cudaEvent_t tm_a = nullptr, tm_b = nullptr;
   std::vector<ebcc_ctx*> lanes;  // child contexts for concurrent sub-batches
   int machine_fields = 0;        // lanes: chunks whose machines run concurrently in total
+  int last_batch = 0;            // chunks of the last compress batch (dev probe bench)
 };
 
 namespace {
@@ -847,6 +848,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   PhaseClock pc(st);
   g_pc = pc.on ? &pc : nullptr;
   double replay_ms = 0;
+  c->last_batch = nfields;
   // ---- ingest + normalise (core.normalize) ----
   CK(cudaGetLastError());
   g_slow.mark("enter_batch");
@@ -2237,6 +2239,52 @@ int ebcc_host_free(void* p) {
     g_pin_free.erase(v);
   }
   return EBCC_OK;
+}
+
+// developer instrumentation: time full (non-incremental) base probes of the
+// last compress batch on this context (single-lane calls) at B = frac * T_base
+int ebcc_dev_probe_bench(ebcc_ctx* c, double frac, int32_t iters, int32_t early, double* us_l0,
+                         double* us_probe) {
+  if (!c || iters < 1 || !us_l0 || !us_probe) return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  Workspace& w = c->ws;
+  const int nf = c->last_batch;
+  if (nf < 1 || !w.packed) return fail(c, EBCC_E_ARGUMENT, "no compress batch on this context");
+  try {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    std::vector<MachineOut> mo(nf);
+    CK(cudaMemcpy(mo.data(), w.mo_base, sizeof(MachineOut) * nf, cudaMemcpyDeviceToHost));
+    std::vector<ProbeParam> prm(nf);
+    for (int f = 0; f < nf; f++) {
+      prm[f] = ProbeParam{};
+      prm[f].B = (uint64_t)(frac * mo[f].total_bits);
+      prm[f].planes = kBasePlanes;
+      prm[f].active = mo[f].n_max != kExpNone;
+      prm[f].early = early;
+    }
+    CK(cudaMemcpy(w.prm, prm.data(), sizeof(ProbeParam) * nf, cudaMemcpyHostToDevice));
+    Meta mb = meta_of(w, false);
+    double l0 = 0, all = 0;
+    for (int it = 0; it < iters + 1; it++) {
+      CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nf, st));
+      CK(cudaEventRecord(c->tm_a, st));
+      fused::g_level0_timer = &c->l0;
+      probe_base(mb, w.prm, w.A, w.B, w.g, nf, w.norm, w.x32, w.fs, w.res, st);
+      fused::g_level0_timer = nullptr;
+      CK(cudaEventRecord(c->tm_b, st));
+      CK(cudaStreamSynchronize(st));
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, c->l0.a, c->l0.b);
+      cudaEventElapsedTime(&b, c->tm_a, c->tm_b);
+      if (it > 0) { l0 += a; all += b; }
+    }
+    *us_l0 = 1e3 * l0 / iters;
+    *us_probe = 1e3 * all / iters;
+    return EBCC_OK;
+  } catch (CudaFail& e) {
+    cudaGetLastError();
+    return fail(c, EBCC_E_CUDA, std::string(e.what) + ": " + cudaGetErrorString(e.e));
+  }
 }
 
 int ebcc_selftest_div(ebcc_ctx* c, int64_t n, uint64_t seed, int64_t* mismatches) {

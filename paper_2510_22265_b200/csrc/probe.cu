@@ -210,9 +210,23 @@ struct BaseProbeEpi {
       cnt += fabs(__dsub_rn(dec, nv)) <= s.eps_rel;
     }
     double e = denorm_err(s, dec, o);
+#if EBCC_MAXSEL
+    mx = e > mx ? e : mx;  // e >= 0 and never NaN
+#else
     mx = fmax(e, mx);
+#endif
   }
   __device__ void finish(int f) { warp_flush(&res[f], cnt, mx, count); }
+  // every lane computes; invalid lanes contribute nothing (no divergence)
+  static constexpr bool kMasked = true, kProbe = true;
+  __device__ void put_masked(double dec, float o, bool valid) {
+    if (count) {
+      double nv = fused::div_exact(__dsub_rn((double)o, s.vmin), s.range, s.range_inv);
+      cnt += (valid && fabs(__dsub_rn(dec, nv)) <= s.eps_rel) ? 1 : 0;
+    }
+    const double e = denorm_err(s, dec, o);
+    mx = (valid && e > mx) ? e : mx;  // e >= 0, never NaN
+  }
   // incremental probes
   static constexpr bool kFinal = true;
   __device__ bool counting() const { return count; }
@@ -248,9 +262,19 @@ struct TruncProbeEpi {
   __device__ void put(double*, int f, int64_t off, double v, const Pre& p) {
     double rec = __dadd_rn(p.base, v);  // base_field + dequantized
     double e = denorm_err(s, rec, p.orig);
+#if EBCC_MAXSEL
+    mx = e > mx ? e : mx;
+#else
     mx = fmax(e, mx);
+#endif
   }
   __device__ void finish(int f) { warp_flush(&res[f], 0, mx, false); }
+  static constexpr bool kMasked = true, kProbe = true;
+  __device__ void put_masked(double v, const Pre& p, bool valid) {
+    const double rec = __dadd_rn(p.base, v);
+    const double e = denorm_err(s, rec, p.orig);
+    mx = (valid && e > mx) ? e : mx;
+  }
   static constexpr bool kFinal = true;
   __device__ bool counting() const { return false; }
   __device__ void add_stored(int f, const TileStat& t) { atomicMax(&res[f].maxerr, t.maxerr); }
@@ -260,6 +284,8 @@ struct TruncProbeEpi {
 };
 
 struct ResidueEpi {
+  static constexpr bool kMasked = false, kProbe = false;
+  template <class P> __device__ void put_masked(double, const P&, bool) {}
   const double* norm; double* base_dec; double* resid; const ProbeParam* prm; int64_t n;
   using Pre = double;
   __device__ Pre pre(int f, int64_t off) const { return norm[(int64_t)f * n + off]; }
@@ -274,6 +300,8 @@ struct ResidueEpi {
 };
 
 struct StoreFieldEpi {
+  static constexpr bool kMasked = false, kProbe = false;
+  template <class P> __device__ void put_masked(double, const P&, bool) {}
   double* out; const ProbeParam* prm; int64_t n;
   using Pre = fused::NoPre;
   __device__ Pre pre(int, int64_t) const { return {}; }
@@ -286,6 +314,8 @@ struct StoreFieldEpi {
 };
 
 struct AddDenormEpi {
+  static constexpr bool kMasked = false, kProbe = false;
+  template <class P> __device__ void put_masked(double, const P&, bool) {}
   const double* base; const FieldScal* fs; const ProbeParam* prm; float* out32; int64_t n;
   FieldScal s;
   using Pre = double;
