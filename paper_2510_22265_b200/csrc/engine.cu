@@ -891,7 +891,11 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   g_slow.mark("base_encode");
   for (int f = 0; f < nfields; f++) cs[f].T_base = active[f] ? mo[f].total_bits : 0;
   std::vector<int> base_nmax(nfields);
-  for (int f = 0; f < nfields; f++) base_nmax[f] = mo[f].n_max;
+  bool xe_base = false, xe_res = false;  // exponents outside the normal range (rare)
+  for (int f = 0; f < nfields; f++) {
+    base_nmax[f] = mo[f].n_max;
+    if (active[f] && mo[f].n_max != kExpNone) xe_base |= exps_extreme(mo[f].n_max);
+  }
 
   std::vector<ProbeParam> prm(nfields);
   std::vector<ProbeResult> res(nfields);
@@ -980,7 +984,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
     fused::g_level0_timer = eager ? &c->l0 : nullptr;
     probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32, w.fs,
-               w.res, st, inc_base);
+               w.res, st, inc_base, xe_base);
     fused::g_level0_timer = nullptr;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
@@ -1068,6 +1072,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       const PlaneRec* p = &rpl[(size_t)f * kMaxPlaneRecs];
       T32[f] = rmo[f].total_bits;
       T24[f] = p[kBasePlanes].start;
+      xe_res |= exps_extreme(rmo[f].n_max);
     }
     resid_ready = true;
     if (pc.on) {
@@ -1137,7 +1142,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     CK(cudaMemsetAsync(d_tres, 0, sizeof(ProbeResult) * nfields, ts));
     fused::g_level0_timer = eager ? &c->l0 : nullptr;
     probe_trunc(mres, d_tprm, inc_res ? w.Linc[1] : a, b, g, nfields, w.base_dec, w.x32, w.fs,
-                d_tres, ts, inc_res);
+                d_tres, ts, inc_res, xe_res);
     fused::g_level0_timer = nullptr;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h_tres, d_tres, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, ts));
@@ -1965,6 +1970,11 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         c->stats.kernel_launches += 4;
       }
       bool res_joined = false;  // st has waited for the residual decoder
+      bool xe_b = false, xe_r = false;  // stream exponents outside the normal range
+      for (int i = 0; i < nb; i++) {
+        if (bact[i] && bmo[i].n_max != kExpNone) xe_b |= exps_extreme(bmo[i].n_max);
+        if (ract[i] && rmo[i].n_max != kExpNone) xe_r |= exps_extreme(rmo[i].n_max);
+      }
       // IDWT + denormalise in field groups; with a page-locked host
       // destination each group's device->host copy (copy stream) overlaps
       // the next group's IDWT
@@ -1997,7 +2007,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           gcst[i] = in && cst[i];
         }
         h2d_small(c, w.prm, prm.data(), sizeof(ProbeParam) * nb, st);
-        decode_field(meta_of(w, false), w.prm, w.A, w.B, g, nb, w.base_dec, st);
+        decode_field(meta_of(w, false), w.prm, w.A, w.B, g, nb, w.base_dec, st, xe_b);
         c->stats.kernel_launches += g.levels;
         CK(cudaGetLastError());
         if (g_slow.on()) {
@@ -2016,7 +2026,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           }
           h2d_small(c, w.prm, prm.data(), sizeof(ProbeParam) * nb, st);
           decode_field_add_denorm(meta_of(w, true), w.prm, w.A, w.B, g, nb, w.base_dec, w.fs,
-                                  out_dev, st);
+                                  out_dev, st, xe_r);
           c->stats.kernel_launches += g.levels;
           CK(cudaGetLastError());
         }
@@ -2264,12 +2274,15 @@ int ebcc_dev_probe_bench(ebcc_ctx* c, double frac, int32_t iters, int32_t early,
     }
     CK(cudaMemcpy(w.prm, prm.data(), sizeof(ProbeParam) * nf, cudaMemcpyHostToDevice));
     Meta mb = meta_of(w, false);
+    bool xe = false;
+    for (int f = 0; f < nf; f++)
+      if (mo[f].n_max != kExpNone) xe |= exps_extreme(mo[f].n_max);
     double l0 = 0, all = 0;
     for (int it = 0; it < iters + 1; it++) {
       CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nf, st));
       CK(cudaEventRecord(c->tm_a, st));
       fused::g_level0_timer = &c->l0;
-      probe_base(mb, w.prm, w.A, w.B, w.g, nf, w.norm, w.x32, w.fs, w.res, st);
+      probe_base(mb, w.prm, w.A, w.B, w.g, nf, w.norm, w.x32, w.fs, w.res, st, nullptr, xe);
       fused::g_level0_timer = nullptr;
       CK(cudaEventRecord(c->tm_b, st));
       CK(cudaStreamSynchronize(st));

@@ -193,15 +193,19 @@ struct BaseProbeEpi {
   const double* norm; const float* orig; const FieldScal* fs; const ProbeParam* prm;
   ProbeResult* res; int64_t n;
   unsigned long long cnt; double mx; FieldScal s; bool count;
+  // masked path: only "some error exceeds eps_abs" is tracked; the reported
+  // maximum is then +inf or 0 (every consumer only asks max_err <= eps_abs)
+  bool bad;
   using Pre = float;
   __device__ Pre pre(int f, int64_t off) const { return orig[(int64_t)f * n + off]; }
   __device__ bool begin(int f) {
-    cnt = 0; mx = 0.0;
+    cnt = 0; mx = 0.0; bad = false;
     if (!prm[f].active) return false;
     s = fs[f];
     count = !prm[f].early;
     return true;
   }
+  __device__ double mxv() const { return bad ? (double)INFINITY : mx; }
   __device__ bool skip(int f) const { return !count && settled(&res[f], s.eps_abs); }
   __device__ void put(double*, int f, int64_t off, double dec, float o) {
     if (count) {  // quantile search: the count of |dec - norm| <= eps_rel
@@ -216,7 +220,7 @@ struct BaseProbeEpi {
     mx = fmax(e, mx);
 #endif
   }
-  __device__ void finish(int f) { warp_flush(&res[f], cnt, mx, count); }
+  __device__ void finish(int f) { warp_flush(&res[f], cnt, mxv(), count); }
   // every lane computes; invalid lanes contribute nothing (no divergence)
   static constexpr bool kMasked = true, kProbe = true;
   __device__ void put_masked(double dec, float o, bool valid) {
@@ -224,8 +228,7 @@ struct BaseProbeEpi {
       double nv = fused::div_exact(__dsub_rn((double)o, s.vmin), s.range, s.range_inv);
       cnt += (valid && fabs(__dsub_rn(dec, nv)) <= s.eps_rel) ? 1 : 0;
     }
-    const double e = denorm_err(s, dec, o);
-    mx = (valid && e > mx) ? e : mx;  // e >= 0, never NaN
+    bad |= valid && denorm_err(s, dec, o) > s.eps_abs;
   }
   // incremental probes
   static constexpr bool kFinal = true;
@@ -235,7 +238,7 @@ struct BaseProbeEpi {
     atomicMax(&res[f].maxerr, t.maxerr);
   }
   __device__ void finish_inc(int f, TileStat* t, volatile uint8_t* flag) {
-    tile_flush(&res[f], t, flag, cnt, mx, count);
+    tile_flush(&res[f], t, flag, cnt, mxv(), count);
   }
 };
 
@@ -248,16 +251,18 @@ struct TruncProbeEpi {
   const double* base; const float* orig; const FieldScal* fs; const ProbeParam* prm;
   ProbeResult* res; int64_t n;
   double mx; FieldScal s;
+  bool bad;  // masked path (see BaseProbeEpi)
   using Pre = TruncPre;
   __device__ Pre pre(int f, int64_t off) const {
     return {base[(int64_t)f * n + off], orig[(int64_t)f * n + off]};
   }
   __device__ bool begin(int f) {
-    mx = 0.0;
+    mx = 0.0; bad = false;
     if (!prm[f].active) return false;
     s = fs[f];
     return true;
   }
+  __device__ double mxv() const { return bad ? (double)INFINITY : mx; }
   __device__ bool skip(int f) const { return prm[f].early && settled(&res[f], s.eps_abs); }
   __device__ void put(double*, int f, int64_t off, double v, const Pre& p) {
     double rec = __dadd_rn(p.base, v);  // base_field + dequantized
@@ -268,18 +273,17 @@ struct TruncProbeEpi {
     mx = fmax(e, mx);
 #endif
   }
-  __device__ void finish(int f) { warp_flush(&res[f], 0, mx, false); }
+  __device__ void finish(int f) { warp_flush(&res[f], 0, mxv(), false); }
   static constexpr bool kMasked = true, kProbe = true;
   __device__ void put_masked(double v, const Pre& p, bool valid) {
     const double rec = __dadd_rn(p.base, v);
-    const double e = denorm_err(s, rec, p.orig);
-    mx = (valid && e > mx) ? e : mx;
+    bad |= valid && denorm_err(s, rec, p.orig) > s.eps_abs;
   }
   static constexpr bool kFinal = true;
   __device__ bool counting() const { return false; }
   __device__ void add_stored(int f, const TileStat& t) { atomicMax(&res[f].maxerr, t.maxerr); }
   __device__ void finish_inc(int f, TileStat* t, volatile uint8_t* flag) {
-    tile_flush(&res[f], t, flag, 0, mx, false);
+    tile_flush(&res[f], t, flag, 0, mxv(), false);
   }
 };
 
@@ -477,18 +481,18 @@ void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, i
 
 void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                 int nfields, const double* norm, const float* orig, const FieldScal* fs,
-                ProbeResult* res, cudaStream_t st, const Inc* inc) {
+                ProbeResult* res, cudaStream_t st, const Inc* inc, bool xe) {
   BaseProbeEpi e{norm, orig, fs, prm, res, g.n, 0, 0.0, FieldScal{}};
-  if (inc) fused::inverse_inc(m, prm, *inc, a, g, nfields, st, e, false);
-  else fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false);
+  if (inc) fused::inverse_inc(m, prm, *inc, a, g, nfields, st, e, false, xe);
+  else fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false, xe);
 }
 
 void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                  int nfields, const double* base_dec, const float* orig, const FieldScal* fs,
-                 ProbeResult* res, cudaStream_t st, const Inc* inc) {
+                 ProbeResult* res, cudaStream_t st, const Inc* inc, bool xe) {
   TruncProbeEpi e{base_dec, orig, fs, prm, res, g.n, 0.0, FieldScal{}};
-  if (inc) fused::inverse_inc(m, prm, *inc, a, g, nfields, st, e, true);
-  else fused::inverse_fused(m, prm, a, b, g, nfields, st, e, true);
+  if (inc) fused::inverse_inc(m, prm, *inc, a, g, nfields, st, e, true, xe);
+  else fused::inverse_fused(m, prm, a, b, g, nfields, st, e, true, xe);
 }
 
 // the level kernels' CTA tiling per level (fused::level_rows) and the
@@ -543,16 +547,16 @@ void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b,
 }
 
 void decode_field(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
-                  int nfields, double* out, cudaStream_t st) {
+                  int nfields, double* out, cudaStream_t st, bool xe) {
   StoreFieldEpi e{out, prm, g.n};
-  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false, xe);
 }
 
 void decode_field_add_denorm(const Meta& m, const ProbeParam* prm, double* a, double* b,
                              const Geo& g, int nfields, const double* base, const FieldScal* fs,
-                             float* out32, cudaStream_t st) {
+                             float* out32, cudaStream_t st, bool xe) {
   AddDenormEpi e{base, fs, prm, out32, g.n, FieldScal{}};
-  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, true);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, true, xe);
 }
 
 void denorm_only(const double* base, const FieldScal* fs, const uint8_t* active, int64_t n,

@@ -136,12 +136,16 @@ void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, i
 // base probe: decode (lower bound) -> IDWT -> count & max error
 void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                 int nfields, const double* norm, const float* orig, const FieldScal* fs,
-                ProbeResult* res, cudaStream_t st, const Inc* inc = nullptr);
+                ProbeResult* res, cudaStream_t st, const Inc* inc = nullptr, bool xe = true);
 
 // residual probe: decode (midpoint) -> IDWT -> + base -> max error
 void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                  int nfields, const double* base_dec, const float* orig, const FieldScal* fs,
-                 ProbeResult* res, cudaStream_t st, const Inc* inc = nullptr);
+                 ProbeResult* res, cudaStream_t st, const Inc* inc = nullptr, bool xe = true);
+
+// some exponent n_max - p (p < 64 planes) outside the normal float64 range:
+// the level kernels' decode then keeps its scalbn path
+inline bool exps_extreme(int n_max) { return n_max - 63 <= -1022 || n_max >= 1024; }
 
 // tiling of the incremental probes (the level kernels' CTA grids); false if
 // the persistent LL layout does not fit (the probes then run in full)
@@ -155,11 +159,11 @@ void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b,
 
 // decompress: decode a stream to a float64 field (out), optionally midpoint
 void decode_field(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
-                  int nfields, double* out, cudaStream_t st);
+                  int nfields, double* out, cudaStream_t st, bool xe = true);
 // decompress: residual decode fused with base add + denormalise to f32
 void decode_field_add_denorm(const Meta& m, const ProbeParam* prm, double* a, double* b,
                              const Geo& g, int nfields, const double* base, const FieldScal* fs,
-                             float* out32, cudaStream_t st);
+                             float* out32, cudaStream_t st, bool xe = true);
 // decompress: f32(vmin + base*range) for fields without residual (gate: active)
 void denorm_only(const double* base, const FieldScal* fs, const uint8_t* active, int64_t n,
                  int nfields, float* out32, cudaStream_t st);
