@@ -900,7 +900,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   std::vector<ProbeParam> prm(nfields);
   std::vector<ProbeResult> res(nfields);
   Meta mbase = meta_of(w, false);
-  StepGraph base_graph, trunc_graph, joint_graph;
+  StepGraph base_graph, pure_graph, trunc_graph, joint_graph;
 
   // incremental probes: one state per stream, invalid at the batch start
   static const bool inc_env = !(getenv("EBCC_INC") && getenv("EBCC_INC")[0] == '0');
@@ -979,12 +979,13 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       tiles_probed += inc_s[0].ig.tiles0;
     }
   };
-  auto enqueue_base = [&](bool eager) {
+  // early: the pure-base search's feasibility probes (no quantile count)
+  auto enqueue_base = [&](bool eager, bool early) {
     CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
     fused::g_level0_timer = eager ? &c->l0 : nullptr;
     probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32, w.fs,
-               w.res, st, inc_base, xe_base);
+               w.res, st, inc_base, xe_base, early);
     fused::g_level0_timer = nullptr;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
@@ -1002,7 +1003,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     bool timed = false;
     base_graph.run(st, [&](bool eager) {
       timed = eager;
-      enqueue_base(eager);
+      enqueue_base(eager, false);
     });
     c->stats.kernel_launches += g.levels;
     c->stats.probe_launches++;
@@ -1046,7 +1047,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   c->stats.kernel_launches += 2 * g.levels;
   // off the critical path while overlapped: one CTA per field leaves
   // more SMs to the pure-search probes running beside it
-  static const int rc = getenv("EBCC_RESID_CLUSTER") ? atoi(getenv("EBCC_RESID_CLUSTER")) : 1;
+  static const int rc = getenv("EBCC_RESID_CLUSTER") ? atoi(getenv("EBCC_RESID_CLUSTER")) : 2;
   encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, active, rs, overlap ? rc : 0);
   CK(cudaEventRecord(c->ev_s1, rs));
   CK(cudaEventRecord(c->ev_b, rs));
@@ -1220,14 +1221,14 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
         CK(cudaEventRecord(c->ev_f0, st));
         CK(cudaStreamWaitEvent(c->side, c->ev_f0, 0));
         enqueue_trunc(c->side, w.A2, w.B2, false);
-        enqueue_base(eager);
+        enqueue_base(eager, true);
         CK(cudaEventRecord(c->ev_f1, c->side));
         CK(cudaStreamWaitEvent(st, c->ev_f1, 0));
       });
     } else if (anyp) {
-      base_graph.run(st, [&](bool eager) {
+      pure_graph.run(st, [&](bool eager) {
         timed = eager;
-        enqueue_base(eager);
+        enqueue_base(eager, true);
       });
     } else {
       trunc_graph.run(st, [&](bool eager) {
@@ -2282,7 +2283,8 @@ int ebcc_dev_probe_bench(ebcc_ctx* c, double frac, int32_t iters, int32_t early,
       CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nf, st));
       CK(cudaEventRecord(c->tm_a, st));
       fused::g_level0_timer = &c->l0;
-      probe_base(mb, w.prm, w.A, w.B, w.g, nf, w.norm, w.x32, w.fs, w.res, st, nullptr, xe);
+      probe_base(mb, w.prm, w.A, w.B, w.g, nf, w.norm, w.x32, w.fs, w.res, st, nullptr, xe,
+                 early != 0);
       fused::g_level0_timer = nullptr;
       CK(cudaEventRecord(c->tm_b, st));
       CK(cudaStreamSynchronize(st));

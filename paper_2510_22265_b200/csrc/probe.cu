@@ -159,7 +159,8 @@ __device__ __forceinline__ void warp_flush(ProbeResult* r, unsigned long long cn
 // incremental probes: the CTA's tile total -> TileStat, the tile's flag
 // (clean, or count stale when this probe did not count) and the result
 __device__ __forceinline__ void tile_flush(ProbeResult* r, TileStat* t, volatile uint8_t* flag,
-                                           unsigned long long cnt, double mx, bool do_count) {
+                                           unsigned long long cnt, double mx, bool do_count,
+                                           bool aborted) {
   __shared__ unsigned long long s_cnt, s_mx;
   if (threadIdx.x == 0) { s_cnt = 0; s_mx = 0; }
   __syncthreads();
@@ -175,6 +176,11 @@ __device__ __forceinline__ void tile_flush(ProbeResult* r, TileStat* t, volatile
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (aborted) {  // the tile stopped early: recompute it on the next probe
+      *flag = kTileDirty;
+      atomicMax(&r->maxerr, s_mx);
+      return;
+    }
     t->count = s_cnt;
     t->maxerr = s_mx;
     *flag = do_count ? 0 : kTileCountStale;
@@ -189,24 +195,32 @@ __device__ __forceinline__ bool settled(const ProbeResult* r, double eps_abs) {
   return __longlong_as_double((long long)b) > eps_abs;
 }
 
+// COUNT: base-search probes (quantile count + max error); otherwise a
+// pure-base feasibility probe (max error only, abortable)
+template <bool COUNT>
 struct BaseProbeEpi {
   const double* norm; const float* orig; const FieldScal* fs; const ProbeParam* prm;
   ProbeResult* res; int64_t n;
-  unsigned long long cnt; double mx; FieldScal s; bool count;
+  unsigned long long cnt; double mx; FieldScal s;
+  static constexpr bool count = COUNT;
+  static constexpr bool kAbort = !COUNT;
+  static constexpr int kMinBlocks = COUNT ? EBCC_MINB : EBCC_MINB_EARLY;
   // masked path: only "some error exceeds eps_abs" is tracked; the reported
   // maximum is then +inf or 0 (every consumer only asks max_err <= eps_abs)
   bool bad;
   using Pre = float;
   __device__ Pre pre(int f, int64_t off) const { return orig[(int64_t)f * n + off]; }
+  __device__ Pre pre_masked(int f, int64_t off) const { return pre(f, off); }
   __device__ bool begin(int f) {
     cnt = 0; mx = 0.0; bad = false;
     if (!prm[f].active) return false;
     s = fs[f];
-    count = !prm[f].early;
     return true;
   }
   __device__ double mxv() const { return bad ? (double)INFINITY : mx; }
-  __device__ bool skip(int f) const { return !count && settled(&res[f], s.eps_abs); }
+  __device__ bool skip(int f) const {
+    return !count && prm[f].early && settled(&res[f], s.eps_abs);
+  }
   __device__ void put(double*, int f, int64_t off, double dec, float o) {
     if (count) {  // quantile search: the count of |dec - norm| <= eps_rel
       // normalised value recomputed exactly like core.normalize (core.py:179)
@@ -223,7 +237,7 @@ struct BaseProbeEpi {
   __device__ void finish(int f) { warp_flush(&res[f], cnt, mxv(), count); }
   // every lane computes; invalid lanes contribute nothing (no divergence)
   static constexpr bool kMasked = true, kProbe = true;
-  __device__ void put_masked(double dec, float o, bool valid) {
+  __device__ void put_masked(int, int64_t, double dec, float o, bool valid) {
     if (count) {
       double nv = fused::div_exact(__dsub_rn((double)o, s.vmin), s.range, s.range_inv);
       cnt += (valid && fabs(__dsub_rn(dec, nv)) <= s.eps_rel) ? 1 : 0;
@@ -237,8 +251,11 @@ struct BaseProbeEpi {
     if (count && t.count) atomicAdd(&res[f].count, t.count);
     atomicMax(&res[f].maxerr, t.maxerr);
   }
-  __device__ void finish_inc(int f, TileStat* t, volatile uint8_t* flag) {
-    tile_flush(&res[f], t, flag, cnt, mxv(), count);
+  __device__ void finish_inc(int f, TileStat* t, volatile uint8_t* flag, bool aborted) {
+    tile_flush(&res[f], t, flag, cnt, mxv(), count, aborted);
+  }
+  __device__ void report(int f) {
+    atomicMax(&res[f].maxerr, (unsigned long long)__double_as_longlong((double)INFINITY));
   }
 };
 
@@ -246,12 +263,17 @@ struct TruncPre {
   double base;
   float orig;
 };
+// masked truncation epilogue: only the original is prefetched (register
+// pressure); the base reconstruction is loaded at the put
 
 struct TruncProbeEpi {
   const double* base; const float* orig; const FieldScal* fs; const ProbeParam* prm;
   ProbeResult* res; int64_t n;
   double mx; FieldScal s;
   bool bad;  // masked path (see BaseProbeEpi)
+  static constexpr bool kAbort = true;
+  // the midpoint decode + base add need more registers: 3 CTAs/SM, no spills
+  static constexpr int kMinBlocks = EBCC_MINB_TRUNC;
   using Pre = TruncPre;
   __device__ Pre pre(int f, int64_t off) const {
     return {base[(int64_t)f * n + off], orig[(int64_t)f * n + off]};
@@ -275,21 +297,28 @@ struct TruncProbeEpi {
   }
   __device__ void finish(int f) { warp_flush(&res[f], 0, mxv(), false); }
   static constexpr bool kMasked = true, kProbe = true;
-  __device__ void put_masked(double v, const Pre& p, bool valid) {
-    const double rec = __dadd_rn(p.base, v);
+  __device__ Pre pre_masked(int f, int64_t off) const { return {0.0, orig[(int64_t)f * n + off]}; }
+  __device__ void put_masked(int f, int64_t off, double v, const Pre& p, bool valid) {
+    const double rec = __dadd_rn(base[(int64_t)f * n + off], v);
     bad |= valid && denorm_err(s, rec, p.orig) > s.eps_abs;
   }
   static constexpr bool kFinal = true;
   __device__ bool counting() const { return false; }
   __device__ void add_stored(int f, const TileStat& t) { atomicMax(&res[f].maxerr, t.maxerr); }
-  __device__ void finish_inc(int f, TileStat* t, volatile uint8_t* flag) {
-    tile_flush(&res[f], t, flag, 0, mxv(), false);
+  __device__ void finish_inc(int f, TileStat* t, volatile uint8_t* flag, bool aborted) {
+    tile_flush(&res[f], t, flag, 0, mxv(), false, aborted);
+  }
+  __device__ void report(int f) {
+    atomicMax(&res[f].maxerr, (unsigned long long)__double_as_longlong((double)INFINITY));
   }
 };
 
 struct ResidueEpi {
+  static constexpr bool kAbort = false;
+  static constexpr int kMinBlocks = EBCC_MINB;
   static constexpr bool kMasked = false, kProbe = false;
-  template <class P> __device__ void put_masked(double, const P&, bool) {}
+  template <class P> __device__ void put_masked(int, int64_t, double, const P&, bool) {}
+  __device__ auto pre_masked(int f, int64_t off) const { return pre(f, off); }
   const double* norm; double* base_dec; double* resid; const ProbeParam* prm; int64_t n;
   using Pre = double;
   __device__ Pre pre(int f, int64_t off) const { return norm[(int64_t)f * n + off]; }
@@ -301,11 +330,16 @@ struct ResidueEpi {
     resid[o] = __dsub_rn(nv, dec);  // nc.values - base_enc.decoded
   }
   __device__ void finish(int) {}
+  bool bad = false;  // (probe epilogues only)
+  __device__ void report(int) {}
 };
 
 struct StoreFieldEpi {
+  static constexpr bool kAbort = false;
+  static constexpr int kMinBlocks = EBCC_MINB;
   static constexpr bool kMasked = false, kProbe = false;
-  template <class P> __device__ void put_masked(double, const P&, bool) {}
+  template <class P> __device__ void put_masked(int, int64_t, double, const P&, bool) {}
+  __device__ auto pre_masked(int f, int64_t off) const { return pre(f, off); }
   double* out; const ProbeParam* prm; int64_t n;
   using Pre = fused::NoPre;
   __device__ Pre pre(int, int64_t) const { return {}; }
@@ -315,11 +349,16 @@ struct StoreFieldEpi {
     out[(int64_t)f * n + off] = v;
   }
   __device__ void finish(int) {}
+  bool bad = false;  // (probe epilogues only)
+  __device__ void report(int) {}
 };
 
 struct AddDenormEpi {
+  static constexpr bool kAbort = false;
+  static constexpr int kMinBlocks = EBCC_MINB;
   static constexpr bool kMasked = false, kProbe = false;
-  template <class P> __device__ void put_masked(double, const P&, bool) {}
+  template <class P> __device__ void put_masked(int, int64_t, double, const P&, bool) {}
+  __device__ auto pre_masked(int f, int64_t off) const { return pre(f, off); }
   const double* base; const FieldScal* fs; const ProbeParam* prm; float* out32; int64_t n;
   FieldScal s;
   using Pre = double;
@@ -336,6 +375,8 @@ struct AddDenormEpi {
     out32[o] = __double2float_rn(__dadd_rn(s.vmin, __dmul_rn(fld, s.range)));
   }
   __device__ void finish(int) {}
+  bool bad = false;  // (probe epilogues only)
+  __device__ void report(int) {}
 };
 
 int grid_for(int64_t n, int cap = 2048) {
@@ -481,10 +522,13 @@ void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, i
 
 void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                 int nfields, const double* norm, const float* orig, const FieldScal* fs,
-                ProbeResult* res, cudaStream_t st, const Inc* inc, bool xe) {
-  BaseProbeEpi e{norm, orig, fs, prm, res, g.n, 0, 0.0, FieldScal{}};
-  if (inc) fused::inverse_inc(m, prm, *inc, a, g, nfields, st, e, false, xe);
-  else fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false, xe);
+                ProbeResult* res, cudaStream_t st, const Inc* inc, bool xe, bool early) {
+  auto run = [&](auto e) {
+    if (inc) fused::inverse_inc(m, prm, *inc, a, g, nfields, st, e, false, xe);
+    else fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false, xe);
+  };
+  if (early) run(BaseProbeEpi<false>{norm, orig, fs, prm, res, g.n, 0, 0.0, FieldScal{}});
+  else run(BaseProbeEpi<true>{norm, orig, fs, prm, res, g.n, 0, 0.0, FieldScal{}});
 }
 
 void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,

@@ -136,7 +136,8 @@ void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, i
 // base probe: decode (lower bound) -> IDWT -> count & max error
 void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                 int nfields, const double* norm, const float* orig, const FieldScal* fs,
-                ProbeResult* res, cudaStream_t st, const Inc* inc = nullptr, bool xe = true);
+                ProbeResult* res, cudaStream_t st, const Inc* inc = nullptr, bool xe = true,
+                bool early = false);
 
 // residual probe: decode (midpoint) -> IDWT -> + base -> max error
 void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
