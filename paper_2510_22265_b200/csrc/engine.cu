@@ -115,6 +115,9 @@ bool is_pageable(const void* p) {
 }
 
 struct NeedBase { int64_t budget; };
+// truncation probes per chunk and step: the bisection's next midpoint plus
+// the two points one level further (one of which the next step needs)
+constexpr int kTruncSlots = 3;
 struct IngestFail {};
 struct NeedTrunc { int planes; int64_t t; };
 
@@ -149,6 +152,7 @@ struct ChunkSearch {
   // stream_len is non-decreasing).  -1 = unknown.
   int64_t p_lb = 0, p_ub = -1;     // pure-base payload bytes
   int64_t t_lb = 0, t_ub = -1;     // residual prefix bytes t
+  int64_t spec[2] = {-1, -1};      // speculative truncation offsets at the first miss
   bool pure_pruned = false, trunc_pruned = false;
 
   int64_t clamp_budget(int64_t b) const {
@@ -281,8 +285,22 @@ struct ChunkSearch {
     n_trunc_calls = 0;
     t_lb = 0;
     t_ub = -1;
-    if (err_at(0) <= eps_abs) return 0;
-    if (err_at(total) > eps_abs) return -1;
+    spec[0] = spec[1] = -1;
+    {
+      const bool before = missed;
+      const bool ok0 = err_at(0) <= eps_abs;
+      if (!before && missed) {  // 0, total and the first midpoint are all needed
+        spec[0] = total;
+        spec[1] = total / 2;
+      }
+      if (ok0) return 0;
+    }
+    {
+      const bool before = missed;
+      const bool ok = err_at(total) <= eps_abs;
+      if (!before && missed) spec[0] = total / 2;
+      if (!ok) return -1;
+    }
     // this pass holds the answer: it lies in the bracket (lo, hi]
     int64_t lo = 0, hi = total;
     while (hi - lo > 1) {
@@ -292,6 +310,8 @@ struct ChunkSearch {
       if (!before && missed) {
         t_lb = lo + 1;
         t_ub = hi;
+        spec[0] = mid - lo > 1 ? (lo + mid) / 2 : -1;
+        spec[1] = hi - mid > 1 ? (mid + hi) / 2 : -1;
       }
       if (ok) hi = mid;
       else lo = mid;
@@ -484,26 +504,28 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   w.fs = dalloc<FieldScal>(cap);
   // two parameter/result slots: pure-base probes and truncation probes
   w.tq_base = dalloc<uint8_t>((size_t)kTqBytes * cap);
-  w.tq_res = dalloc<uint8_t>((size_t)kTqBytes * cap);
-  w.prm = dalloc<ProbeParam>(2 * (size_t)cap);
-  w.res = dalloc<ProbeResult>(2 * (size_t)cap);
+  w.tq_res = dalloc<uint8_t>((size_t)kTqBytes * kTruncSlots * cap);
+  // parameter/result slots: base-stream probes, then kTruncSlots x truncation probes
+  w.prm = dalloc<ProbeParam>((1 + kTruncSlots) * (size_t)cap);
+  w.res = dalloc<ProbeResult>((1 + kTruncSlots) * (size_t)cap);
   w.limit = dalloc<uint64_t>(cap);
   w.active = dalloc<uint8_t>(cap);
   w.mm = dalloc<unsigned int>(4 * cap + 2);
   inc_capacity(g, &w.inc_tiles, &w.inc_tiles0);
   w.inc_lstride = g.levels > 1 ? (int64_t)g.lr[1] * g.cols : 1;
   for (int i = 0; i < 2; i++) {
-    w.Linc[i] = dalloc<double>((size_t)w.inc_lstride * cap);
+    const size_t np = (size_t)cap * (i ? kTruncSlots : 1);  // probes per step
+    w.Linc[i] = dalloc<double>((size_t)w.inc_lstride * np);
     w.lspn[i] = dalloc<uint32_t>(N);
-    w.iflags[i] = dalloc<uint8_t>((size_t)w.inc_tiles * cap);
-    w.its[i] = dalloc<TileStat>((size_t)w.inc_tiles0 * cap);
-    w.iplan[i] = dalloc<IncPlan>(cap);
-    w.istate[i] = dalloc<IncState>(cap);
-    CK(cudaMemset(w.iflags[i], kTileDirty, (size_t)w.inc_tiles * cap));
+    w.iflags[i] = dalloc<uint8_t>((size_t)w.inc_tiles * np);
+    w.its[i] = dalloc<TileStat>((size_t)w.inc_tiles0 * np);
+    w.iplan[i] = dalloc<IncPlan>(np);
+    w.istate[i] = dalloc<IncState>(np);
+    CK(cudaMemset(w.iflags[i], kTileDirty, (size_t)w.inc_tiles * np));
   }
   w.icomputed = dalloc<unsigned long long>(2 * kMaxLevels);
-  CK(cudaMallocHost(&w.h_prm, sizeof(ProbeParam) * 2 * cap));
-  CK(cudaMallocHost(&w.h_res, sizeof(ProbeResult) * 2 * cap));
+  CK(cudaMallocHost(&w.h_prm, sizeof(ProbeParam) * (1 + kTruncSlots) * cap));
+  CK(cudaMallocHost(&w.h_res, sizeof(ProbeResult) * (1 + kTruncSlots) * cap));
   build_tree_tables(g, w.tt, c->stream);
   w.has_tt = true;
 }
@@ -922,7 +944,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     I.klimit = (uint32_t)std::min<int64_t>(N / klim_div, 0xffffffffll);
     static const int dbg = getenv("EBCC_INC_LOG") ? atoi(getenv("EBCC_INC_LOG")) : 0;
     I.debug = dbg;
-    CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields, st));
+    CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields * (i ? kTruncSlots : 1), st));
   }
   CK(cudaMemsetAsync(w.icomputed, 0, sizeof(unsigned long long) * 2 * kMaxLevels, st));
   const Inc* inc_base = inc_ok ? &inc_s[0] : nullptr;
@@ -1091,17 +1113,41 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   };
   std::vector<int> pass(nfields, 0);
   std::vector<int> trunc_calls(nfields, 0);
-  std::vector<ProbeParam> tprm(nfields);
-  std::vector<ProbeResult> tres(nfields);
+  // speculative truncation probes (EBCC_SPEC=2|3: also probe the next
+  // bisection level's points) need one incremental state per slot; measured
+  // no faster on 37 x 721x1440 (the probe phase is throughput-bound), so off
+  static const int spec_env =
+      getenv("EBCC_SPEC") ? std::max(1, std::min(kTruncSlots, atoi(getenv("EBCC_SPEC")))) : 1;
+  const int TS = inc_res ? spec_env : 1;  // truncation probe slots in use
+  const int ntp = TS * nfields;           // truncation probes per step (probe v: chunk v % nfields)
+  std::vector<ProbeParam> tprm(ntp);
+  std::vector<ProbeResult> tres(ntp);
+  std::vector<int64_t> tslot_t(ntp, -1);
+  std::vector<int> tslot_pi(ntp, 0);
   ProbeParam* d_tprm = w.prm + w.cap;
   ProbeResult* d_tres = w.res + w.cap;
   ProbeParam* h_tprm = w.h_prm + w.cap;
   ProbeResult* h_tres = w.h_res + w.cap;
   auto trunc_requests = [&]() {
     bool any = false;
+    for (int v = 0; v < ntp; v++) tprm[v] = ProbeParam{};
+    auto set_probe = [&](int v, int f, int pi, int64_t t) {
+      int P = pi == 0 ? kBasePlanes : kDeepPlanes;
+      uint64_t T = pi == 0 ? T24[f] : T32[f];
+      uint64_t Bfull = (uint64_t)t * 8;
+      tprm[v].B = Bfull < T ? Bfull : T;
+      tprm[v].planes = P;
+      tprm[v].midpoint = 1;
+      tprm[v].n_last = rmo[f].n_max == kExpNone
+                           ? 0
+                           : n_last_of(rmo[f], &rpl[(size_t)f * kMaxPlaneRecs], P, Bfull, T);
+      tprm[v].active = 1;
+      tprm[v].early = early_ok();  // err_at(t) <= eps_abs is all the search asks
+      tslot_t[v] = t;
+      tslot_pi[v] = pi;
+    };
     for (int f = 0; f < nfields; f++) {
       ChunkSearch& s = cs[f];
-      tprm[f] = ProbeParam{};
       if (s.constant || s.trunc_planes || pass[f] > 1) continue;
       for (;;) {
         s.missed = false;
@@ -1120,17 +1166,14 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
           NeedTrunc nt{s.miss_planes, s.miss_key};
           s.tpending = nt.t;
           s.tpending_planes = nt.planes;
-          int P = nt.planes == 0 ? kBasePlanes : kDeepPlanes;
-          uint64_t T = nt.planes == 0 ? T24[f] : T32[f];
-          uint64_t Bfull = (uint64_t)nt.t * 8;
-          tprm[f].B = Bfull < T ? Bfull : T;
-          tprm[f].planes = P;
-          tprm[f].midpoint = 1;
-          tprm[f].n_last = rmo[f].n_max == kExpNone
-                               ? 0
-                               : n_last_of(rmo[f], &rpl[(size_t)f * kMaxPlaneRecs], P, Bfull, T);
-          tprm[f].active = 1;
-          tprm[f].early = early_ok();  // err_at(t) <= eps_abs is all the search asks
+          set_probe(f, f, nt.planes, nt.t);
+          // speculative slots: points the next step needs whichever way
+          // this probe answers (same planes variant)
+          for (int k = 0; k + 1 < TS && k < 2; k++) {
+            const int64_t t2 = s.spec[k];
+            if (t2 < 0 || t2 == nt.t || s.trunc[nt.planes].count(t2)) continue;
+            set_probe((k + 1) * nfields + f, f, nt.planes, t2);
+          }
           any = true;
           break;
         }
@@ -1139,24 +1182,24 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     return any;
   };
   auto enqueue_trunc = [&](cudaStream_t ts, double* a, double* b, bool eager) {
-    CK(cudaMemcpyAsync(d_tprm, h_tprm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, ts));
-    CK(cudaMemsetAsync(d_tres, 0, sizeof(ProbeResult) * nfields, ts));
+    CK(cudaMemcpyAsync(d_tprm, h_tprm, sizeof(ProbeParam) * ntp, cudaMemcpyHostToDevice, ts));
+    CK(cudaMemsetAsync(d_tres, 0, sizeof(ProbeResult) * ntp, ts));
     fused::g_level0_timer = eager ? &c->l0 : nullptr;
-    probe_trunc(mres, d_tprm, inc_res ? w.Linc[1] : a, b, g, nfields, w.base_dec, w.x32, w.fs,
-                d_tres, ts, inc_res, xe_res);
+    probe_trunc(mres, d_tprm, inc_res ? w.Linc[1] : a, b, g, ntp, w.base_dec, w.x32, w.fs,
+                d_tres, ts, inc_res, xe_res, nfields);
     fused::g_level0_timer = nullptr;
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(h_tres, d_tres, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, ts));
+    CK(cudaMemcpyAsync(h_tres, d_tres, sizeof(ProbeResult) * ntp, cudaMemcpyDeviceToHost, ts));
   };
   auto trunc_results = [&]() {
-    memcpy(tres.data(), h_tres, sizeof(ProbeResult) * nfields);
-    for (int f = 0; f < nfields; f++) {
-      if (!tprm[f].active) continue;
-      ChunkSearch& s = cs[f];
+    memcpy(tres.data(), h_tres, sizeof(ProbeResult) * ntp);
+    for (int v = 0; v < ntp; v++) {
+      if (!tprm[v].active) continue;
+      ChunkSearch& s = cs[v % nfields];
       double e;
-      uint64_t bitsv = tres[f].maxerr;
+      uint64_t bitsv = tres[v].maxerr;
       memcpy(&e, &bitsv, 8);
-      s.trunc[s.tpending_planes][s.tpending] = e;
+      s.trunc[tslot_pi[v]][tslot_t[v]] = e;
       tiles_probed += inc_s[1].ig.tiles0;
     }
   };
@@ -1192,10 +1235,10 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
           s.trunc_pruned = true;  // pure-base is no longer (ties go to pure-base)
           s.trunc_t = -1;
           pass[f] = 2;
-          tprm[f] = ProbeParam{};
+          for (int k = 0; k < TS; k++) tprm[k * nfields + f] = ProbeParam{};
         }
         anyp |= prm[f].active != 0;
-        anyt |= tprm[f].active != 0;
+        for (int k = 0; k < TS; k++) anyt |= tprm[k * nfields + f].active != 0;
       }
     }
     replay_ms += std::chrono::duration<double, std::milli>(SteadyClock::now() - h0).count();
@@ -1214,7 +1257,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     EventTimer t(c, &c->stats.ms_probe);
     bool timed = false;
     if (anyp) memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
-    if (anyt) memcpy(h_tprm, tprm.data(), sizeof(ProbeParam) * nfields);
+    if (anyt) memcpy(h_tprm, tprm.data(), sizeof(ProbeParam) * ntp);
     if (anyp && anyt) {
       joint_graph.run(st, [&](bool eager) {
         timed = eager;

@@ -211,9 +211,9 @@ struct BaseProbeEpi {
   using Pre = float;
   __device__ Pre pre(int f, int64_t off) const { return orig[(int64_t)f * n + off]; }
   __device__ Pre pre_masked(int f, int64_t off) const { return pre(f, off); }
-  __device__ bool begin(int f) {
+  __device__ bool begin(int v, int f) {  // probe v of chunk f
     cnt = 0; mx = 0.0; bad = false;
-    if (!prm[f].active) return false;
+    if (!prm[v].active) return false;
     s = fs[f];
     return true;
   }
@@ -278,9 +278,9 @@ struct TruncProbeEpi {
   __device__ Pre pre(int f, int64_t off) const {
     return {base[(int64_t)f * n + off], orig[(int64_t)f * n + off]};
   }
-  __device__ bool begin(int f) {
+  __device__ bool begin(int v, int f) {  // probe v of chunk f
     mx = 0.0; bad = false;
-    if (!prm[f].active) return false;
+    if (!prm[v].active) return false;
     s = fs[f];
     return true;
   }
@@ -322,7 +322,7 @@ struct ResidueEpi {
   const double* norm; double* base_dec; double* resid; const ProbeParam* prm; int64_t n;
   using Pre = double;
   __device__ Pre pre(int f, int64_t off) const { return norm[(int64_t)f * n + off]; }
-  __device__ bool begin(int f) { return prm[f].active != 0; }
+  __device__ bool begin(int v, int) { return prm[v].active != 0; }
   __device__ bool skip(int) const { return false; }
   __device__ void put(double*, int f, int64_t off, double dec, double nv) {
     int64_t o = (int64_t)f * n + off;
@@ -343,7 +343,7 @@ struct StoreFieldEpi {
   double* out; const ProbeParam* prm; int64_t n;
   using Pre = fused::NoPre;
   __device__ Pre pre(int, int64_t) const { return {}; }
-  __device__ bool begin(int f) { return prm[f].active != 0; }
+  __device__ bool begin(int v, int) { return prm[v].active != 0; }
   __device__ bool skip(int) const { return false; }
   __device__ void put(double*, int f, int64_t off, double v, const Pre&) {
     out[(int64_t)f * n + off] = v;
@@ -363,8 +363,8 @@ struct AddDenormEpi {
   FieldScal s;
   using Pre = double;
   __device__ Pre pre(int f, int64_t off) const { return base[(int64_t)f * n + off]; }
-  __device__ bool begin(int f) {
-    if (!prm[f].active) return false;
+  __device__ bool begin(int v, int f) {
+    if (!prm[v].active) return false;
     s = fs[f];
     return true;
   }
@@ -532,11 +532,13 @@ void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, cons
 }
 
 void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
-                 int nfields, const double* base_dec, const float* orig, const FieldScal* fs,
-                 ProbeResult* res, cudaStream_t st, const Inc* inc, bool xe) {
+                 int nprobes, const double* base_dec, const float* orig, const FieldScal* fs,
+                 ProbeResult* res, cudaStream_t st, const Inc* inc, bool xe, int nphys) {
+  // probe v reads chunk v % nphys; several probes per chunk need the
+  // incremental path (one LL buffer per probe)
   TruncProbeEpi e{base_dec, orig, fs, prm, res, g.n, 0.0, FieldScal{}};
-  if (inc) fused::inverse_inc(m, prm, *inc, a, g, nfields, st, e, true, xe);
-  else fused::inverse_fused(m, prm, a, b, g, nfields, st, e, true, xe);
+  if (inc) fused::inverse_inc(m, prm, *inc, a, g, nprobes, st, e, true, xe, nphys);
+  else fused::inverse_fused(m, prm, a, b, g, nprobes, st, e, true, xe);
 }
 
 // the level kernels' CTA tiling per level (fused::level_rows) and the

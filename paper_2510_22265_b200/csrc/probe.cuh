@@ -141,8 +141,9 @@ void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, cons
 
 // residual probe: decode (midpoint) -> IDWT -> + base -> max error
 void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
-                 int nfields, const double* base_dec, const float* orig, const FieldScal* fs,
-                 ProbeResult* res, cudaStream_t st, const Inc* inc = nullptr, bool xe = true);
+                 int nprobes, const double* base_dec, const float* orig, const FieldScal* fs,
+                 ProbeResult* res, cudaStream_t st, const Inc* inc = nullptr, bool xe = true,
+                 int nphys = -1);
 
 // some exponent n_max - p (p < 64 planes) outside the normal float64 range:
 // the level kernels' decode then keeps its scalbn path
