@@ -1005,7 +1005,8 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   auto enqueue_base = [&](bool eager, bool early) {
     CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
-    fused::g_level0_timer = eager ? &c->l0 : nullptr;
+    // roofline timing: the first base-search probe (every tile computed)
+    fused::g_level0_timer = eager && !early ? &c->l0 : nullptr;
     probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32, w.fs,
                w.res, st, inc_base, xe_base, early);
     fused::g_level0_timer = nullptr;
@@ -1184,7 +1185,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   auto enqueue_trunc = [&](cudaStream_t ts, double* a, double* b, bool eager) {
     CK(cudaMemcpyAsync(d_tprm, h_tprm, sizeof(ProbeParam) * ntp, cudaMemcpyHostToDevice, ts));
     CK(cudaMemsetAsync(d_tres, 0, sizeof(ProbeResult) * ntp, ts));
-    fused::g_level0_timer = eager ? &c->l0 : nullptr;
+    fused::g_level0_timer = nullptr;
     probe_trunc(mres, d_tprm, inc_res ? w.Linc[1] : a, b, g, ntp, w.base_dec, w.x32, w.fs,
                 d_tres, ts, inc_res, xe_res, nfields);
     fused::g_level0_timer = nullptr;
@@ -1282,7 +1283,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     c->stats.kernel_launches += (anyp + anyt) * g.levels;
     c->stats.probe_launches++;
     CK(cudaStreamSynchronize(st));
-    accumulate_level0(c, timed, nfields);
+    (void)timed;  // level-0 roofline timing comes from the first base-search step
     if (anyp) base_results();
     if (anyt) trunc_results();
     g_slow.mark(anyp && anyt ? "joint_step" : (anyp ? "pure_step" : "trunc_step"));
