@@ -433,6 +433,8 @@ struct ebcc_ctx {
   int unpack_cap = 0;
   uint8_t* d_stage = nullptr;
   int64_t stage_cap = 0;
+  uint8_t* h_pay = nullptr;       // decompress: page-locked copy of a pageable payload
+  int64_t h_pay_cap = 0;
   float* d_out = nullptr;
   int64_t out_cap = 0;
   uint8_t* d_cont = nullptr;      // container image (ebcc_fetch_container)
@@ -1431,6 +1433,7 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->d_out) cudaFree(c->d_out);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->h_arena) cudaFreeHost(c->h_arena);
+  if (c->h_pay) cudaFreeHost(c->h_pay);
   if (c->d_cont) cudaFree(c->d_cont);
   if (c->d_cmeta) cudaFree(c->d_cmeta);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -1953,7 +1956,22 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           c->d_stage = dalloc<uint8_t>(span);
           c->stage_cap = span;
         }
-        CK(cudaMemcpyAsync(c->d_stage, payload + lo, span,
+        const uint8_t* psrc = payload + lo;
+        if (!(flags & EBCC_INPUT_ON_DEVICE) && is_pageable(psrc)) {
+          // a pageable source would make the copy synchronous through the
+          // driver's small bounce buffers: stage it (thread team) into a
+          // page-locked block of this context instead
+          if (span > c->h_pay_cap) {
+            if (c->h_pay) CK(cudaFreeHost(c->h_pay));
+            c->h_pay = nullptr;
+            c->h_pay_cap = 0;
+            CK(cudaMallocHost(&c->h_pay, (size_t)span));
+            c->h_pay_cap = span;
+          }
+          parallel_memcpy(c->h_pay, psrc, (size_t)span);
+          psrc = c->h_pay;
+        }
+        CK(cudaMemcpyAsync(c->d_stage, psrc, span,
                            (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
                                                           : cudaMemcpyHostToDevice,
                            st));
