@@ -602,6 +602,56 @@ struct StepProf {
   double prep = 0, launch = 0, wait = 0, post = 0, timer = 0;
 };
 StepProf g_sp;
+// EBCC_TRACE=1: per-lane host timeline of one compress (step completions,
+// no extra synchronisation), printed when the call returns
+struct Trace {
+  bool on = false;
+  std::mutex mu;
+  std::chrono::steady_clock::time_point t0;
+  struct Ev { int lane; const char* what; int i; double ms; };
+  std::vector<Ev> ev;
+  Trace() { on = getenv("EBCC_TRACE") && getenv("EBCC_TRACE")[0] == '1'; }
+  void start() {
+    if (!on) return;
+    std::lock_guard<std::mutex> lk(mu);
+    ev.clear();
+    t0 = std::chrono::steady_clock::now();
+  }
+  void add(int lane, const char* what, int i) {
+    if (!on) return;
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::lock_guard<std::mutex> lk(mu);
+    ev.push_back({lane, what, i, ms});
+  }
+  void dump() {
+    if (!on) return;
+    std::lock_guard<std::mutex> lk(mu);
+    for (int lane = 0; lane < 8; lane++) {
+      std::string line;
+      const char* prev = nullptr;
+      int run = 0;
+      double first = 0, lastms = 0;
+      auto flush = [&]() {
+        if (!prev) return;
+        char b[96];
+        if (run > 1) snprintf(b, sizeof b, " %s x%d [%.2f..%.2f]", prev, run, first, lastms);
+        else snprintf(b, sizeof b, " %s@%.2f", prev, lastms);
+        line += b;
+      };
+      for (auto& e : ev) {
+        if (e.lane != lane) continue;
+        if (prev && strcmp(prev, e.what) == 0) { run++; lastms = e.ms; continue; }
+        flush();
+        prev = e.what; run = 1; first = lastms = e.ms;
+      }
+      flush();
+      if (!line.empty()) fprintf(stderr, "[ebcc trace lane %d]%s\n", lane, line.c_str());
+    }
+  }
+};
+Trace g_trace;
+thread_local int g_lane = 0;
+
 // EBCC_SLOWLOG=<ms>: report host intervals longer than that (tail-latency hunt)
 struct SlowLog {
   double thr = -1;
@@ -612,6 +662,7 @@ struct SlowLog {
   }
   bool on() const { return thr >= 0; }
   void mark(const char* what, int i = -1) {
+    g_trace.add(g_lane, what, i);
     if (thr < 0) return;
     auto now = std::chrono::steady_clock::now();
     double ms = std::chrono::duration<double, std::milli>(now - last).count();
@@ -1089,6 +1140,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   Meta mres = meta_of(w, true);
   bool resid_ready = false;
   auto collect_residual = [&]() {
+    g_trace.add(g_lane, "resid_ready", -1);
     CK(cudaStreamWaitEvent(st, c->ev_b, 0));
     encode_collect(c, nfields, true, active, rmo, rpl, st);
     float ms = 0;
@@ -1291,6 +1343,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     g_slow.mark(anyp && anyt ? "joint_step" : (anyp ? "pure_step" : "trunc_step"));
   }
   pc.mark("trunc_search");
+  g_trace.add(g_lane, "searches_done", -1);
   g_pc = nullptr;
   if (inc_ok) {
     unsigned long long comp[2 * kMaxLevels];
@@ -1681,6 +1734,8 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
     CK(cudaSetDevice(c->device));
     const int L = lanes_for(nfields);
     const int64_t n = (int64_t)rows * cols;
+    g_trace.start();
+    struct TraceDump { ~TraceDump() { g_trace.dump(); } } trace_dump;
     std::vector<int64_t> sizes;
     int status = EBCC_OK;
     cudaEvent_t t0 = c->oev0, t1 = c->oev1;
@@ -1710,6 +1765,7 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
       for (int k = 0; k < L; k++)
         th.emplace_back([&, k] {
           cudaSetDevice(c->device);
+          g_lane = k;
           lst[k] = compress_impl(ls[k], fields + lo[k] * n, lo[k + 1] - lo[k], rows, cols, eps_rel,
                                  q, r0, search_tol, flags, recs + lo[k], lsz[k], t0, 1.0 / L,
                                  &chain, k);
