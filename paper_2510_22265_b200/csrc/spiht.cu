@@ -660,9 +660,12 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
         mp_ent += cnt;
         mp_tiles += (cnt + CT - 1) / CT;
 #endif
-        // prepass: total children bits of significant type-A entries
+        // prepass: total children bits of significant type-A entries (the
+        // sign bits follow all of the wave's children bits).  A wave of one
+        // cluster tile gets it from the main pass's first scan instead.
         uint64_t TC = 0;
-        for (uint64_t base = 0; base < cnt; base += CT) {
+        const bool single = cnt <= CT;
+        for (uint64_t base = 0; !single && base < cnt; base += CT) {
           uint64_t local = 0;
           const uint64_t i0 = base + my0 + (uint64_t)threadIdx.x * MI;
 #pragma unroll
@@ -679,7 +682,7 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
         MPROF_MARK(w0 ? 2 : 3);
         const uint64_t segw = w0 ? lis_run : cnt;  // entry significance bits
         const uint64_t ch_seg0 = pos + segw;       // children significance bits
-        const uint64_t sg_seg0 = pos + segw + TC;  // their sign bits
+        uint64_t sg_seg0 = pos + segw + TC;        // their sign bits (single: after scan 1)
         uint64_t ch_off = 0, sig_off = 0, nxt_off = 0;
         for (uint64_t base = 0; base < cnt; base += CT) {
           uint64_t ent[MI];
@@ -750,6 +753,10 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
                                           ((uint64_t)nxts << 32) |
                                           (DECODE ? 0ull : ((uint64_t)nsig << 48)));
           const uint64_t ex1 = s1.ex, tot1 = s1.total;
+          if (single) {
+            TC = lane16(tot1, 1);
+            sg_seg0 = pos + segw + TC;
+          }
           uint64_t ex2, tot2, s2_before, s2_total;
           if (DECODE) {
             uint64_t cpos = ch_seg0 + ch_off + lane16(ex1, 1);
