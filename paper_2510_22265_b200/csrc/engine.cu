@@ -1923,6 +1923,8 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
   c->stats = ebcc_stats{};
   c->err.clear();
   arena_reset(c);  // the previous call ended synchronised
+  g_trace.start();
+  struct TraceDump { ~TraceDump() { g_trace.dump(); } } trace_dump;
   g_slow.mark("dec_enter");
   try {
     CK(cudaSetDevice(c->device));
@@ -2036,6 +2038,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           c->unpack_cap = (int)up.size() * 2;
           c->d_unpack = dalloc<UnpackPart>(c->unpack_cap);
         }
+        g_trace.add(0, "dec_payload_staged", -1);
         h2d_small(c, c->d_unpack, up.data(), sizeof(UnpackPart) * up.size(), st);
         unpack_parts(c->d_unpack, (int)up.size(), c->d_stage, st);
         c->stats.kernel_launches++;
@@ -2088,6 +2091,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         pack_meta(mb, w.packed, w.sprank, st);
         c->stats.kernel_launches += 4;
       }
+      g_trace.add(0, "dec_machines_issued", -1);
       bool res_joined = false;  // st has waited for the residual decoder
       bool xe_b = false, xe_r = false;  // stream exponents outside the normal range
       for (int i = 0; i < nb; i++) {
@@ -2162,6 +2166,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
                              sizeof(float) * g.n * (b - a), cudaMemcpyDeviceToHost, c->copy));
         }
       }
+      g_trace.add(0, "dec_idwt_issued", -1);
       if (any_res && !res_joined) CK(cudaStreamWaitEvent(st, c->ev_b, 0));
       if (G > 1) {
         CK(cudaEventRecord(c->ev_copy, c->copy));
@@ -2179,6 +2184,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
       }
       CK(cudaStreamSynchronize(st));
     }
+    g_trace.add(0, "dec_batches_done", -1);
     cudaEventRecord(t1, st);
     cudaEventSynchronize(t1);
     float ms = 0;
