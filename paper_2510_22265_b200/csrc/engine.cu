@@ -911,10 +911,14 @@ bool early_ok() {
 }
 
 // one compress batch of nfields (<= workspace capacity); x already in w.x32
+// in_groups > 0: the input arrives in that many field groups, group k
+// complete when in_ev[k] fires (host input copied group by group); each
+// group is normalised and transformed as soon as it lands
 int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0, double tol,
                    bool prune,
                    ebcc_chunk_rec* recs, int64_t out_base_off, std::vector<PackPart>& parts,
-                   std::vector<int64_t>& sizes) {
+                   std::vector<int64_t>& sizes, int in_groups = 0,
+                   const cudaEvent_t* in_ev = nullptr) {
   Workspace& w = c->ws;
   const Geo& g = w.g;
   cudaStream_t st = c->stream;
@@ -927,7 +931,25 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   // ---- ingest + normalise (core.normalize) ----
   CK(cudaGetLastError());
   g_slow.mark("enter_batch");
-  ingest_normalize(w.x32, N, nfields, w.norm, w.fs, w.mm, eps_rel, st);
+  const bool grouped = in_groups > 0;
+  if (!grouped) {
+    ingest_normalize(w.x32, N, nfields, w.norm, w.fs, w.mm, eps_rel, st);
+  } else {
+    // per group: normalise + forward DWT (the non-finite check is read after
+    // all groups; a failing input only costs the wasted transforms)
+    for (int k = 0; k < in_groups; k++) {
+      const int a = (int)((int64_t)nfields * k / in_groups);
+      const int b = (int)((int64_t)nfields * (k + 1) / in_groups);
+      if (b <= a) continue;
+      CK(cudaStreamWaitEvent(st, in_ev[k], 0));
+      ingest_normalize(w.x32 + (int64_t)a * N, N, b - a, w.norm + (int64_t)a * N, w.fs + a,
+                       w.mm + 4 * (int64_t)a, eps_rel, st);
+      CK(cudaMemcpyAsync(w.A + (int64_t)a * N, w.norm + (int64_t)a * N,
+                         sizeof(double) * N * (b - a), cudaMemcpyDeviceToDevice, st));
+      forward_dwt(w.A + (int64_t)a * N, w.B + (int64_t)a * N, N, b - a, g, st);
+      c->stats.kernel_launches += 2 * g.levels;
+    }
+  }
   CK(cudaGetLastError());
   pc.mark("ingest");
   c->stats.kernel_launches += 4;
@@ -955,10 +977,12 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   std::vector<PlaneRec> pl((size_t)kMaxPlaneRecs * nfields);
   {
     EventTimer t(c, &c->stats.ms_encode);
-    CK(cudaMemcpyAsync(w.A, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
-    forward_dwt(w.A, w.B, N, nfields, g, st);
-    CK(cudaGetLastError());
-    c->stats.kernel_launches += 2 * g.levels;
+    if (!grouped) {
+      CK(cudaMemcpyAsync(w.A, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
+      forward_dwt(w.A, w.B, N, nfields, g, st);
+      CK(cudaGetLastError());
+      c->stats.kernel_launches += 2 * g.levels;
+    }
     pc.mark("fwd_dwt");
     encode_pyramids(c, nfields, false, kBasePlanes, active, mo, pl);
   }
@@ -1598,16 +1622,43 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
       }
       CK(cudaGetLastError());
       const bool chained = chain && f0 == 0 && !(flags & EBCC_INPUT_ON_DEVICE);
+      // host input: copied in field groups on the copy stream, each group
+      // transformed as soon as it lands (compress_batch)
+      static const int in_groups_env =
+          getenv("EBCC_IN_GROUPS") ? std::max(1, atoi(getenv("EBCC_IN_GROUPS"))) : 4;
+      const int in_groups = (flags & EBCC_INPUT_ON_DEVICE) ? 0 : std::min(in_groups_env, nb);
+      cudaStream_t cst = in_groups ? c->copy : st;
+      if (in_groups && !c->copy) {
+        CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming));
+        cst = c->copy;
+      }
+      while ((int)c->ev_groups.size() < in_groups) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_groups.push_back(e);
+      }
+      if (in_groups) CK(cudaStreamWaitEvent(cst, c->cev0, 0));  // after this call's start
       if (chained && lane > 0) {
         while (chain->issued.load() < lane) std::this_thread::yield();
-        CK(cudaStreamWaitEvent(st, chain->done[lane - 1], 0));
+        CK(cudaStreamWaitEvent(cst, chain->done[lane - 1], 0));
       }
-      CK(cudaMemcpyAsync(c->ws.x32, src, in_bytes,
-                         (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
-                                                        : cudaMemcpyHostToDevice,
-                         st));
+      if (in_groups) {
+        for (int k = 0; k < in_groups; k++) {
+          const int64_t a = (int64_t)nb * k / in_groups, b = (int64_t)nb * (k + 1) / in_groups;
+          if (b > a)
+            CK(cudaMemcpyAsync(c->ws.x32 + a * g.n, src + a * g.n, sizeof(float) * g.n * (b - a),
+                               cudaMemcpyHostToDevice, cst));
+          CK(cudaEventRecord(c->ev_groups[k], cst));
+        }
+      } else {
+        CK(cudaMemcpyAsync(c->ws.x32, src, in_bytes,
+                           (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
+                                                          : cudaMemcpyHostToDevice,
+                           st));
+      }
       if (chained) {
-        CK(cudaEventRecord(chain->done[lane], st));
+        CK(cudaEventRecord(chain->done[lane], cst));
         chain->issued.store(lane + 1);
         chain_release.done = true;
       }
@@ -1618,7 +1669,7 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
       int s;
       try {
         s = compress_batch(c, nb, eps_rel, q, r0, search_tol, !(flags & EBCC_FULL_SEARCH),
-                           recs + f0, done, bparts, bsizes);
+                           recs + f0, done, bparts, bsizes, in_groups, c->ev_groups.data());
       } catch (IngestFail&) {
         c->err_index += f0 * g.n;
         return fail(c, EBCC_E_INGEST, "non-finite value in the input");

@@ -5,6 +5,7 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
@@ -12,7 +13,8 @@ from paper_2510_22265_b200 import _lib  # noqa: E402
 
 levels = int(sys.argv[1]) if len(sys.argv) > 1 else 37
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-host = bench.workload(0)[:levels].copy()
+base = bench.workload(0)
+host = np.concatenate([base] * ((levels + len(base) - 1) // len(base)))[:levels].copy()
 x = torch.from_numpy(host).cuda()
 pay = torch.empty(host.nbytes * 2, dtype=torch.uint8, device="cuda")
 out = torch.empty_like(x)
