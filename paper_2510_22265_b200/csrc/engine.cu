@@ -1137,8 +1137,15 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   // resid overwrites norm in place (nothing reads norm after this point)
   base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
   c->stats.kernel_launches += g.levels;
-  static const bool overlap = !(getenv("EBCC_OVERLAP") && getenv("EBCC_OVERLAP")[0] == '0');
-  cudaStream_t rs = overlap ? c->side : st;
+  // EBCC_OVERLAP: 0 (default) = residual encode on the lane's stream, then
+  // the pure and truncation searches; 1 = on the high-priority side stream
+  // with the first pure-base probes running beside it (measured slower, 32.3
+  // vs 31.3 ms, since the pure search got cheap: the probes slow the
+  // latency-bound machine on the critical path); 2 = on the side stream,
+  // the lane waits (31.5 ms)
+  static const int ovmode = getenv("EBCC_OVERLAP") ? atoi(getenv("EBCC_OVERLAP")) : 0;
+  const bool overlap = ovmode == 1;
+  cudaStream_t rs = ovmode == 0 ? st : c->side;
   CK(cudaEventRecord(c->ev_a, st));
   CK(cudaStreamWaitEvent(rs, c->ev_a, 0));
   CK(cudaEventRecord(c->ev_s0, rs));
@@ -1148,7 +1155,8 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   // off the critical path while overlapped: one CTA per field leaves
   // more SMs to the pure-search probes running beside it
   static const int rc = getenv("EBCC_RESID_CLUSTER") ? atoi(getenv("EBCC_RESID_CLUSTER")) : 2;
-  encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, active, rs, overlap ? rc : 0);
+  encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, active, rs,
+                overlap ? rc : machine_cluster_size(false, std::max(nfields, c->machine_fields)));
   CK(cudaEventRecord(c->ev_s1, rs));
   CK(cudaEventRecord(c->ev_b, rs));
   if (!overlap) pc.mark("residual_encode(serial)");
@@ -1283,6 +1291,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     }
   };
   bool pure_phase_marked = false;
+  if (!overlap) collect_residual();  // the searches start once the residual stream is there
   for (;;) {
     if (!resid_ready && cudaEventQuery(c->ev_b) == cudaSuccess) collect_residual();
     cudaGetLastError();  // a not-ready query is not an error
