@@ -36,7 +36,10 @@ namespace {
 #define EBCC_MT 512
 #endif
 constexpr int MT = EBCC_MT;      // machine threads
-constexpr int MI = 4;            // entries per thread per tile
+#ifndef EBCC_MI
+#define EBCC_MI 4
+#endif
+constexpr int MI = EBCC_MI;      // entries per thread per tile (16-bit scan lanes: MI*MT*4*4 < 2^16)
 constexpr int TILE = MT * MI;    // 2048
 constexpr int NW = MT / 32;
 constexpr int STAGE_BITS = TILE * 4 + 64;  // children segment can be 4x the tile
