@@ -291,6 +291,21 @@ __device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t& t
 
 __device__ __forceinline__ uint32_t lane16(uint64_t v, int k) { return (uint32_t)(v >> (16 * k)) & 0xffffu; }
 
+// physical bits of a stream word holding stream positions [a, b) of it
+// (MSB-first bytes in a little-endian word, bit_mask_in_word)
+__device__ __forceinline__ uint32_t seg_mask(int a, int b) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int B = 0; B < 4; B++) {
+    const int ja = min(max(a - 8 * B, 0), 8), jb = min(max(b - 8 * B, 0), 8);
+    m |= ((0xffu >> ja) & ~(0xffu >> jb) & 0xffu) << (8 * B);
+  }
+  return m;
+}
+#ifndef EBCC_LIP_PREFIX
+#define EBCC_LIP_PREFIX 1
+#endif
+
 // Cluster-wide exclusive scan: the CTAs of a cluster process consecutive
 // sub-tiles of one list, so each thread's prefix is its block prefix plus the
 // totals of the lower-ranked CTAs, exchanged through distributed shared
@@ -500,8 +515,76 @@ __global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, T
       nlsp += K;
       nlip -= K;
     }
-    // ---------------- LIP pass: a streaming stable partition -------------
-    if (DECODE) {
+    // ---------------- LIP pass (decoder) ---------------------------------
+    // The LIP's significance bits are one contiguous segment [pos, pos+nlip)
+    // (bits past `limit` read as 0).  An entry's rank among the significant
+    // ones is the number of set segment bits before its own: a per-word
+    // prefix (one cluster scan over the segment's words) plus a popcount in
+    // its word.  Survivors are compacted out of place (into the wave buffer,
+    // which then becomes the LIP); no per-tile cluster barrier.
+    if (DECODE && EBCC_LIP_PREFIX) {
+      uint64_t K = 0;
+      if (nlip) {
+        const uint64_t seg0 = pos, seg1 = min(pos + nlip, limit);
+        const uint64_t w0 = seg0 >> 5;
+        const uint64_t nw = seg1 > seg0 ? ((seg1 - 1) >> 5) - w0 + 1 : 0;
+        uint64_t* P = wav_b;  // exclusive prefix of set segment bits per word
+        auto segcount = [&](uint64_t w) -> uint32_t {
+          const uint64_t wb = (w0 + w) << 5;
+          const int a = seg0 > wb ? (int)(seg0 - wb) : 0;
+          const int b = seg1 < wb + 32 ? (int)(seg1 - wb) : 32;
+          return __popc(__ldg(bits + w0 + w) & seg_mask(a, b));
+        };
+        const uint64_t per = (nw + csize - 1) / csize;
+        const uint64_t wlo = min(nw, (uint64_t)crank * per), whi = min(nw, wlo + per);
+        const uint64_t tper = (whi - wlo + MT - 1) / MT;
+        const uint64_t tlo = min(whi, wlo + (uint64_t)threadIdx.x * tper);
+        const uint64_t thi = min(whi, tlo + tper);
+        uint64_t local = 0;
+        for (uint64_t w = tlo; w < thi; w++) local += segcount(w);
+        const ClusterScanOut cs = cscan(local);
+        K = cs.total;
+        uint64_t run = cs.ex;
+        for (uint64_t w = tlo; w < thi; w++) {
+          P[w] = run;
+          run += segcount(w);
+        }
+        csync();  // every CTA's prefixes visible
+        for (uint64_t i = (uint64_t)crank * MT + threadIdx.x; i < nlip; i += (uint64_t)MT * csize) {
+          const uint64_t e = lip[i];
+          const uint64_t q = pos + i;
+          bool sig = false;
+          uint64_t S = K;  // entries past `limit`: every set bit lies before them
+          if (q < seg1) {
+            const uint64_t wa = q >> 5;
+            const uint32_t word = __ldg(bits + wa);
+            const uint64_t wb = wa << 5;
+            const int a = seg0 > wb ? (int)(seg0 - wb) : 0;
+            S = P[wa - w0] + __popc(word & seg_mask(a, (int)(q - wb)));
+            sig = (word & bit_mask_in_word(q)) != 0;
+          }
+          if (sig) {
+            const uint64_t rank = nlsp + S, sp = pos + nlip + S;
+            const uint32_t c = (uint32_t)e;
+            lsp[rank] = c;
+            lsp_rank[c] = (uint32_t)rank;
+            if (sp < limit) {
+              sign_pos[c] = (uint32_t)sp;
+              pinfo[c] = (uint8_t)(p | (read_bit(bits, sp, limit) << 7));
+            } else {
+              pinfo[c] = (uint8_t)p;
+            }
+          } else {
+            wav_a[i - S] = e;
+          }
+        }
+      }
+      pos += nlip + K;
+      nlsp += K;
+      nlip -= K;
+      { uint64_t* t = lip; lip = wav_a; wav_a = t; }
+      csync();  // compacted LIP visible cluster-wide before the LIS appends
+    } else if (DECODE) {
       uint64_t K = 0;  // newly significant so far
       for (uint64_t base = 0; base < nlip; base += CT) {
         uint64_t ent[MI];
