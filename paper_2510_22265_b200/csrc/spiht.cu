@@ -1448,10 +1448,18 @@ void subtree_exponents(MachineBufs& mb, const Geo& g, const TreeTables& tt, cuda
 // live inside one GPC, so e.g. 37 fields x 4 CTAs do not all fit on 148 SMs).
 // Largest c <= 4 (the 16-bit scan lanes hold a 4-CTA tile) whose co-resident
 // cluster count covers the batch, from the occupancy calculator.
+// the largest cluster (<= kMaxCluster CTAs) for which every chunk's cluster
+// is resident at once: few large chunks get up to 7 CTAs each (the packed
+// 16-bit scan lanes hold a cluster tile's children count, <= 4*TILE*size)
+#ifndef EBCC_MAX_CLUSTER
+#define EBCC_MAX_CLUSTER 7
+#endif
+constexpr int kMaxCluster = EBCC_MAX_CLUSTER;
+static_assert(4 * TILE * kMaxCluster < 65536, "16-bit scan lanes");
 int machine_cluster_size(bool decode, int nfields) {
   if (const char* e = getenv("EBCC_MACHINE_CLUSTER")) {
     const int c = atoi(e);
-    return c < 1 ? 1 : (c > 4 ? 4 : c);
+    return c < 1 ? 1 : (c > kMaxCluster ? kMaxCluster : c);
   }
   static std::mutex mu;
   static std::unordered_map<int64_t, int> memo;
@@ -1464,7 +1472,7 @@ int machine_cluster_size(bool decode, int nfields) {
     if (it != memo.end()) return it->second;
   }
   int best = 1;
-  for (int c = 4; c >= 2; c--) {
+  for (int c = kMaxCluster; c >= 2; c--) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(nfields * c), 1, 1);
     cfg.blockDim = dim3(MT, 1, 1);
