@@ -195,6 +195,35 @@ def test_candidate_pruning_keeps_bytes(ebcc, eps):
     assert np.all(r_fast["n_trunc_probes"] <= r_full["n_trunc_probes"])
 
 
+def test_full_size_other_eps_vs_oracle_fixtures(ebcc):
+    """configs[1] levels at eps 0.1% and 10% (BASELINE.json's other targets):
+    containers equal the C oracle's (tests/golden/oracle_eps.json, made by
+    tools/oracle_fixture_eps.py), alone and inside one batched call of all
+    37 levels (incremental probes, candidate pruning and abortable probes
+    across many chunks and both lanes)."""
+    import hashlib
+    import json
+    import os
+    from paper_2510_22265_b200 import fields
+    from paper_2510_22265_b200.container import read_file
+    with open(os.path.join(os.path.dirname(__file__), "golden", "oracle_eps.json")) as fh:
+        cases = json.load(fh)
+    levels = fields.config2_levels()[0]
+    bad = []
+    for eps in sorted({c["eps"] for c in cases}):
+        whole, _, _ = read_file(ebcc.compress(levels[None], rel_error=eps))
+        for case in (c for c in cases if c["eps"] == eps):
+            a = levels[case["level"]]
+            assert gi.sha(a) == case["input_sha"], case["name"]
+            blob = ebcc.compress(a, rel_error=eps)
+            if hashlib.sha256(blob).hexdigest() != case["container_sha"]:
+                bad.append((case["name"], eps, "single", len(blob), case["container_len"]))
+            single, _, _ = read_file(blob)
+            if whole[case["level"]].payload != single[0].payload:
+                bad.append((case["name"], eps, "batched"))
+    assert not bad, bad
+
+
 def test_large_golden(ebcc, golden_large):
     bad = []
     for case in golden_large:
