@@ -228,11 +228,7 @@ struct BaseProbeEpi {
       cnt += fabs(__dsub_rn(dec, nv)) <= s.eps_rel;
     }
     double e = denorm_err(s, dec, o);
-#if EBCC_MAXSEL
-    mx = e > mx ? e : mx;  // e >= 0 and never NaN
-#else
     mx = fmax(e, mx);
-#endif
   }
   __device__ void finish(int f) { warp_flush(&res[f], cnt, mxv(), count); }
   // every lane computes; invalid lanes contribute nothing (no divergence)
@@ -289,11 +285,7 @@ struct TruncProbeEpi {
   __device__ void put(double*, int f, int64_t off, double v, const Pre& p) {
     double rec = __dadd_rn(p.base, v);  // base_field + dequantized
     double e = denorm_err(s, rec, p.orig);
-#if EBCC_MAXSEL
-    mx = e > mx ? e : mx;
-#else
     mx = fmax(e, mx);
-#endif
   }
   __device__ void finish(int f) { warp_flush(&res[f], 0, mxv(), false); }
   static constexpr bool kMasked = true, kProbe = true;
