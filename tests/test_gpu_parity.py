@@ -247,6 +247,7 @@ def test_full_size_config3_config4_vs_oracle_fixtures(ebcc):
     with open(os.path.join(os.path.dirname(__file__), "golden", "oracle_large.json")) as fh:
         cases = json.load(fh)
     bad = []
+    big = {}
     for case in cases:
         name = case["name"]
         if name.startswith("config4_var"):
@@ -258,7 +259,17 @@ def test_full_size_config3_config4_vs_oracle_fixtures(ebcc):
         blob = ebcc.compress(arr, case["eps"], case["q"])
         if hashlib.sha256(blob).hexdigest() != case["container_sha"]:
             bad.append((name, len(blob), case["container_len"]))
+        if name.startswith("config4_var"):
+            big[name] = (arr, blob)
     assert not bad, bad
+    # the configs[3] chunks in one call: several concurrent lanes and 7-CTA
+    # list-machine clusters; every chunk's payload equals its single-call one
+    from paper_2510_22265_b200.container import read_file
+    names = sorted(big)
+    whole, _, _ = read_file(ebcc.compress(np.stack([big[k][0] for k in names])))
+    for i, k in enumerate(names):
+        single, _, _ = read_file(big[k][1])
+        assert whole[i].payload == single[0].payload, k
 
 
 def test_random_fields_vs_oracle(ebcc, oracle):
