@@ -416,6 +416,10 @@ struct ebcc_ctx {
   std::string err;
   int64_t err_index = -1;   // flat element index of the last EBCC_E_INGEST
   Workspace ws;
+  // workspaces of other chunk shapes, kept for reuse (calls alternating
+  // between shapes - custom chunking, edge chunks - would otherwise free and
+  // reallocate several GB per call); most recently parked last
+  std::vector<Workspace> ws_cache;
   // pinned staging for pageable host buffers (copied by a thread team)
   uint8_t* h_stage = nullptr;
   // page-locked arena for the small host->device parameter copies of one
@@ -464,6 +468,25 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
   Workspace& w = c->ws;
   bool same_geo = w.g.rows == g.rows && w.g.cols == g.cols && w.g.levels == g.levels;
   if (same_geo && w.cap >= nfields) return;
+  if (!same_geo) {
+    for (size_t i = 0; i < c->ws_cache.size(); i++) {
+      Workspace& cw = c->ws_cache[i];
+      if (cw.g.rows == g.rows && cw.g.cols == g.cols && cw.g.levels == g.levels &&
+          cw.cap >= nfields) {
+        std::swap(c->ws, cw);  // the current one is parked in its place
+        return;
+      }
+    }
+    if (w.cap > 0) {  // park the current workspace, evicting the oldest
+      static const size_t kKeep = getenv("EBCC_WS_CACHE") ? (size_t)atoi(getenv("EBCC_WS_CACHE")) : 3;
+      c->ws_cache.push_back(w);
+      w = Workspace{};
+      while (c->ws_cache.size() > kKeep) {
+        c->ws_cache.front().release();
+        c->ws_cache.erase(c->ws_cache.begin());
+      }
+    }
+  }
   int cap = std::max(nfields, same_geo ? w.cap : 0);
   w.release();
   w.g = g;
@@ -1512,6 +1535,8 @@ void ebcc_destroy(ebcc_ctx* c) {
   c->lanes.clear();
   cudaSetDevice(c->device);
   c->ws.release();
+  for (Workspace& cw : c->ws_cache) cw.release();
+  c->ws_cache.clear();
   if (c->d_payload) cudaFree(c->d_payload);
   if (c->d_parts) cudaFree(c->d_parts);
   if (c->d_unpack) cudaFree(c->d_unpack);
@@ -1572,6 +1597,9 @@ int64_t batch_cap(ebcc_ctx* c, const Geo& g, int64_t nfields, double share) {
   const Workspace& w = c->ws;
   if (w.cap >= want && w.g.rows == g.rows && w.g.cols == g.cols && w.g.levels == g.levels)
     return want;
+  for (const Workspace& cw : c->ws_cache)
+    if (cw.cap >= want && cw.g.rows == g.rows && cw.g.cols == g.cols && cw.g.levels == g.levels)
+      return want;
   size_t freeb = 0, totalb = 0;
   CK(cudaMemGetInfo(&freeb, &totalb));
   const int64_t per_field = g.n * 176 + 4096;  // ~176 B per point per chunk in flight

@@ -112,33 +112,11 @@ def _compressed_from_records(chunks, recs, offs, payload, params):
 
 
 def _each_group(fn, groups: dict, ctx):
-    """fn over the same-shape chunk groups, in group order.  Several groups
-    (custom chunk shapes, edge chunks) run concurrently, one host thread and
-    library context each (ctypes releases the GIL, the library is reentrant
-    per context), so their latency-bound search phases overlap on the GPU
-    (37 levels in 256x512 chunks, four shapes: compress 333 -> 223 ms).  The
-    first group (in order) that raises decides the exception, as in a serial
-    loop."""
-    items = list(groups.items())
-    if ctx is not None or len(items) < 2:
-        return [fn(it) for it in items]
-    futs = [_group_pool().submit(fn, it) for it in items]
-    return [f.result() for f in futs]  # re-raises the first failing group's error
-
-
-_POOL = None
-_POOL_LOCK = __import__("threading").Lock()
-
-
-def _group_pool():
-    """Process-wide worker threads for shape groups: fixed threads, so their
-    per-thread library contexts (and device workspaces) are reused."""
-    global _POOL
-    with _POOL_LOCK:
-        if _POOL is None:
-            from concurrent.futures import ThreadPoolExecutor
-            _POOL = ThreadPoolExecutor(max_workers=4, thread_name_prefix="ebcc-group")
-        return _POOL
+    """fn over the same-shape chunk groups, in group order.  (Running the
+    groups concurrently, one worker thread and library context each, measured
+    slower once each context keeps a workspace per chunk shape: 199 vs 152 ms
+    for 37 levels in 256x512 chunks; the groups contend for the SMs.)"""
+    return [fn(it) for it in groups.items()]
 
 
 def compress_chunks(chunks: list, params: EbccParams, ctx=None) -> list:
@@ -400,14 +378,37 @@ def _validate_payload(data, off, blen, rlen, mode, rows, cols) -> int:
 
 
 def _records_to_grid_slow(dims, chunk_shape, recs, offs, data, ctx):
-    chunks = []
-    for i, origin in enumerate(tile_origins(dims, chunk_shape)):
-        tt, pp, hh, ww = block_shape_at(origin, dims, chunk_shape)
-        n = int(recs[i]["base_len"]) + int(recs[i]["resid_len"])
-        chunks.append(CompressedChunk(
-            mode=Mode(int(recs[i]["mode"])), epsilon_rel=float(recs[i]["eps"]),
-            q=float(recs[i]["q"]), vmin=float(recs[i]["vmin"]), vmax=float(recs[i]["vmax"]),
-            base_len=int(recs[i]["base_len"]), residual_len=int(recs[i]["resid_len"]),
-            payload=data[offs[i]: offs[i] + n], rows=tt * pp * hh, cols=ww,
-            block_shape=(tt, pp, hh, ww), origin=origin))
-    return decompress_grid(chunks, dims, ctx=ctx)
+    """Any chunking: chunks grouped by (rows, cols, levels), each group decoded
+    by one device call straight from the container bytes (records' offsets
+    index ``data``; no per-chunk payload copies), blocks scattered back in
+    tile order."""
+    origins = tile_origins(dims, chunk_shape)
+    buf = np.frombuffer(data, dtype=np.uint8)
+    mode = recs["mode"].astype(np.int64)
+    blen = recs["base_len"].astype(np.int64)
+    rlen = recs["resid_len"].astype(np.int64)
+    shapes = [block_shape_at(o, dims, chunk_shape) for o in origins]
+    groups: dict = {}
+    for i, (tt, pp, hh, ww) in enumerate(shapes):
+        rows, cols = tt * pp * hh, ww
+        lv = 0
+        if mode[i] != int(Mode.CONSTANT):
+            lv = _validate_payload(data, int(offs[i]), int(blen[i]), int(rlen[i]), int(mode[i]),
+                                   rows, cols)
+        groups.setdefault((rows, cols, lv or default_levels(rows, cols)), []).append(i)
+    out = np.empty(tuple(dims), dtype=np.float32)
+    for (rows, cols, lv), idx in groups.items():
+        idx = np.asarray(idx)
+        lrec = np.zeros(len(idx), dtype=_lib.REC_DTYPE)
+        lrec["mode"] = mode[idx]
+        lrec["vmin"] = recs["vmin"][idx].astype(np.float64)
+        lrec["vmax"] = recs["vmax"][idx].astype(np.float64)
+        lrec["base_len"] = blen[idx]
+        lrec["resid_len"] = rlen[idx]
+        res = decompress_batch(buf, np.ascontiguousarray(offs[idx], dtype=np.int64), lrec, rows,
+                               cols, lv, ctx=ctx)
+        for k, i in enumerate(idx):
+            t0, p0, h0, w0 = origins[i]
+            t, p, h, w = shapes[i]
+            out[t0: t0 + t, p0: p0 + p, h0: h0 + h, w0: w0 + w] = res[k].reshape(t, p, h, w)
+    return out
