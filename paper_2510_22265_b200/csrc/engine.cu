@@ -18,6 +18,8 @@
 // pure search, but the truncation search never touches the base memo, so
 // the order is observably identical, and running both base-memo searches
 // first lets the residual encode reuse the base coefficient metadata arrays.
+#include <omp.h>
+
 #include <algorithm>
 #include <atomic>
 #include <thread>
@@ -87,22 +89,20 @@ double py_floordiv(double vx, double wx) {
 // host memcpy split over a thread team (first-touch page faults of a fresh
 // destination are spread over the team too)
 void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-  unsigned hw = std::thread::hardware_concurrency();
-  int T = (int)std::min<unsigned>(hw ? hw : 4, 16);
-  if (bytes < (8u << 20) || T <= 1) {
+  // host staging copies (pageable <-> page-locked) of 10-150 MB: a persistent
+  // OpenMP team (spawning threads per call cost ~0.5 ms per 16 MB copy)
+  const int T = std::max(1, std::min(omp_get_max_threads(), 16));
+  if (bytes < (4u << 20) || T <= 1) {
     memcpy(dst, src, bytes);
     return;
   }
-  std::vector<std::thread> th;
   size_t step = (bytes + T - 1) / T;
   step = (step + 4095) & ~size_t(4095);
+#pragma omp parallel for num_threads(T) schedule(static)
   for (int t = 0; t < T; t++) {
-    size_t lo = (size_t)t * step;
-    if (lo >= bytes) break;
-    size_t n = std::min(step, bytes - lo);
-    th.emplace_back([=] { memcpy((char*)dst + lo, (const char*)src + lo, n); });
+    const size_t lo = (size_t)t * step;
+    if (lo < bytes) memcpy((char*)dst + lo, (const char*)src + lo, std::min(step, bytes - lo));
   }
-  for (auto& x : th) x.join();
 }
 
 bool is_pageable(const void* p) {
