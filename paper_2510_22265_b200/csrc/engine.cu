@@ -91,7 +91,7 @@ double py_floordiv(double vx, double wx) {
 void parallel_memcpy(void* dst, const void* src, size_t bytes) {
   // host staging copies (pageable <-> page-locked) of 10-150 MB: a persistent
   // OpenMP team (spawning threads per call cost ~0.5 ms per 16 MB copy)
-  const int T = std::max(1, std::min(omp_get_max_threads(), 16));
+  static const int T = (int)std::max(1u, std::min(std::thread::hardware_concurrency(), 16u));
   if (bytes < (4u << 20) || T <= 1) {
     memcpy(dst, src, bytes);
     return;
