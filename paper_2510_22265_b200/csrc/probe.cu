@@ -569,7 +569,8 @@ bool inc_geometry(const Geo& g, int nfields, Inc& inc) {
 void inc_capacity(const Geo& g, int64_t* tiles, int64_t* tiles0) {
   int64_t t = 0;
   for (int k = 0; k < g.levels; k++) {
-    const int th = fused::level_rows(g, k, 1);
+    // the shortest tiles of either grid-size regime (level_rows)
+    const int th = std::min(fused::level_rows(g, k, 1), fused::level_rows(g, k, fused::kSmallBatch + 1));
     int64_t n = (int64_t)((g.lc[k] + fused::TW - 1) / fused::TW) * ((g.lr[k] + th - 1) / th);
     if (k == 0) *tiles0 = n;
     t += n;
