@@ -1223,12 +1223,16 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   };
   std::vector<int> pass(nfields, 0);
   std::vector<int> trunc_calls(nfields, 0);
-  // speculative truncation probes (EBCC_SPEC=2|3: also probe the next
-  // bisection level's points) need one incremental state per slot; measured
-  // no faster on 37 x 721x1440 (the probe phase is throughput-bound), so off
+  // speculative truncation probes (also probe the next bisection level's
+  // points; EBCC_SPEC=1|2|3 forces the slot count) need one incremental state
+  // per slot; no faster on 37 x 721x1440 (the probe phase is throughput-bound)
   static const int spec_env =
-      getenv("EBCC_SPEC") ? std::max(1, std::min(kTruncSlots, atoi(getenv("EBCC_SPEC")))) : 1;
-  const int TS = inc_res ? spec_env : 1;  // truncation probe slots in use
+      getenv("EBCC_SPEC") ? std::max(1, std::min(kTruncSlots, atoi(getenv("EBCC_SPEC")))) : 0;
+  // default: speculate while a lane's chunks leave the GPU slack (measured on
+  // 721x1440 chunks: 1 chunk 8.4 -> 7.4 ms, 6 chunks 12.6 -> 11.9 ms; from
+  // 12 chunks on it costs more than it saves)
+  const int spec_auto = N * (int64_t)nfields <= (8ll << 20) ? kTruncSlots : 1;
+  const int TS = inc_res ? (spec_env ? spec_env : spec_auto) : 1;  // truncation probe slots in use
   const int ntp = TS * nfields;           // truncation probes per step (probe v: chunk v % nfields)
   std::vector<ProbeParam> tprm(ntp);
   std::vector<ProbeResult> tres(ntp);
