@@ -255,6 +255,8 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(e2e_steps):
         flush.zero_()
         torch.cuda.synchronize()
+        if world > 1:  # every rank's step starts together (max-over-ranks window)
+            torch.distributed.barrier()
         t0 = time.perf_counter()
         blob = ebcc.compress(pinned.numpy(), rel_error=EPS, q=Q)
         t1 = time.perf_counter()
