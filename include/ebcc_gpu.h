@@ -45,6 +45,10 @@ extern "C" {
                                     searches (no candidate pruning; same bytes,
                                     n_base_probes / n_trunc_probes equal the
                                     reference's probe counts)                 */
+#define EBCC_CONTAINER_BODY 8    /* ebcc_fetch_container: records + payloads
+                                    only (no 42-byte file header; header42 may
+                                    be NULL) - one rank's span of a container
+                                    assembled by several processes           */
 
 /* Chunk modes (pipeline.py:38-41). */
 #define EBCC_MODE_CONSTANT 0
@@ -104,6 +108,24 @@ int ebcc_fetch_payload(ebcc_ctx *ctx, uint8_t *payload, int64_t payload_cap, int
 int ebcc_fetch_container(ebcc_ctx *ctx, const uint8_t *header42, const uint8_t *records25,
                          int64_t nchunks, uint8_t *out, int64_t cap, int32_t flags,
                          int64_t *out_len);
+
+/* Host-side container indexing (container.py:82-145, pipeline.py:336-353),
+ * native so a 2,368-chunk container is indexed in microseconds:
+ *   ebcc_parse_records  walks the `count` records after the 42-byte header:
+ *                       copies each 25-byte record to records25 and the
+ *                       absolute payload offset to offsets.  EBCC_E_FORMAT
+ *                       with *err_offset and *err_aux = 1 truncated record,
+ *                       2 unknown mode, 3 truncated payload, 4 trailing bytes
+ *                       (the reference's FormatError offsets).
+ *   ebcc_check_streams  the stream-header checks of decompress_chunk for
+ *                       same-shape chunks; *levels = common level count;
+ *                       EBCC_E_FORMAT names the first bad chunk in *bad,
+ *                       EBCC_E_ARGUMENT a chunk of a different depth. */
+int ebcc_parse_records(const uint8_t *data, int64_t len, int64_t count, uint8_t *records25,
+                       int64_t *offsets, int64_t *err_offset, int32_t *err_aux);
+int ebcc_check_streams(const uint8_t *data, int64_t len, const uint8_t *records25,
+                       const int64_t *offsets, int64_t n, int32_t rows, int32_t cols,
+                       int32_t *levels, int64_t *bad);
 
 /* Page-locked host blocks for result arrays, from a per-process cache so that
  * repeated calls do not pay cudaHostAlloc.  Device->host copies into them run

@@ -802,10 +802,16 @@ int eo_compress_chunk(const float *values, int rows, int cols, double eps_rel, d
   int64_t n = (int64_t)rows * cols;
   /* core.normalize (core.py:161-180) */
   float fmin = values[0], fmax = values[0];
-  for (int64_t i = 1; i < n; i++) {
+  int pos_zero = 0;
+  for (int64_t i = 0; i < n; i++) {
     if (values[i] < fmin) fmin = values[i];
     if (values[i] > fmax) fmax = values[i];
+    if (values[i] == 0.0f && !signbit(values[i])) pos_zero = 1;
   }
+  /* tied signed zeros: numpy keeps one by its SIMD lane order (CPU-dependent);
+   * pinned here (and on the GPU) as "+0.0 preferred" */
+  if (fmin == 0.0f) fmin = pos_zero ? 0.0f : -0.0f;
+  if (fmax == 0.0f) fmax = pos_zero ? 0.0f : -0.0f;
   double vmin = fmin, vmax = fmax, vrange = vmax - vmin;
   res->vmin = vmin; res->vmax = vmax;
   if (vrange < 1e-30) { res->mode = 0; return EO_OK; }

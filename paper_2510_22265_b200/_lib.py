@@ -25,6 +25,7 @@ OK, E_ARGUMENT, E_FORMAT, E_RESIDUAL, E_CAPACITY, E_CUDA, E_NOMEM, E_INGEST = ra
 INPUT_ON_DEVICE = 1
 OUTPUT_ON_DEVICE = 2
 FULL_SEARCH = 4  # compress: every probe of the reference's searches (no candidate pruning)
+CONTAINER_BODY = 8  # fetch_container: records + payloads only (one rank's span)
 
 # the exported symbols include/ebcc_gpu.h declares (checked by the CPU tests)
 EXPORTS = ("ebcc_abi_version", "ebcc_create", "ebcc_destroy", "ebcc_set_stream",
@@ -32,7 +33,7 @@ EXPORTS = ("ebcc_abi_version", "ebcc_create", "ebcc_destroy", "ebcc_set_stream",
            "ebcc_get_stats", "ebcc_dwt", "ebcc_spiht_encode", "ebcc_spiht_decode",
            "ebcc_selftest_div", "ebcc_fetch_container", "ebcc_host_alloc", "ebcc_host_free",
            "ebcc_error_stats", "ebcc_error_histogram", "ebcc_ssim", "ebcc_radial_spectrum",
-           "ebcc_dev_probe_bench")
+           "ebcc_dev_probe_bench", "ebcc_parse_records", "ebcc_check_streams")
 
 
 class ChunkRec(ctypes.Structure):
@@ -97,6 +98,10 @@ def load(path: str = LIB_PATH):
                                            ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double)]
         L.ebcc_fetch_container.argtypes = [P, P, P, i64, P, i64, i32, ctypes.POINTER(i64)]
+        L.ebcc_parse_records.argtypes = [P, i64, i64, P, P, ctypes.POINTER(i64),
+                                         ctypes.POINTER(i32)]
+        L.ebcc_check_streams.argtypes = [P, i64, P, P, i64, i32, i32, ctypes.POINTER(i32),
+                                         ctypes.POINTER(i64)]
         L.ebcc_host_alloc.argtypes = [i64, ctypes.POINTER(P)]
         L.ebcc_host_free.argtypes = [P]
         L.ebcc_error_stats.argtypes = [P, P, P, i64, i64, i32, P]
@@ -246,6 +251,19 @@ class Context:
                                            ctypes.byref(got))
         self.raise_for(st, "ebcc_fetch_container")
         return out
+
+    def fetch_container_into(self, header: bytes | None, records: np.ndarray,
+                             payload_total: int, ptr: int, cap: int, flags: int = 0) -> int:
+        """Like :meth:`fetch_container`, into caller memory at ``ptr``;
+        ``flags`` may add CONTAINER_BODY (no header).  Returns the length."""
+        recs = np.ascontiguousarray(records)
+        n = len(recs)
+        got = ctypes.c_int64(0)
+        st = self.lib.ebcc_fetch_container(self.handle, header, recs.ctypes.data if n else None,
+                                           n, ctypes.c_void_p(ptr), int(cap), int(flags),
+                                           ctypes.byref(got))
+        self.raise_for(st, "ebcc_fetch_container")
+        return int(got.value)
 
     # -- decompress ----------------------------------------------------------
     def decompress(self, payload, offsets: np.ndarray, recs: np.ndarray, rows: int, cols: int,

@@ -99,6 +99,9 @@ def write_bytes(chunks, dims, chunk_shape) -> bytes:
 
 
 def _load(source) -> bytes:
+    import mmap
+    if isinstance(source, mmap.mmap):
+        return source  # a shared segment (distributed.decompress): indexed in place
     if isinstance(source, (bytes, bytearray, memoryview)):
         return bytes(source)
     if hasattr(source, "read"):
@@ -134,26 +137,40 @@ def parse(source):
     if count != expected:
         raise FormatError(f"chunk count {count} inconsistent with tiling ({expected})",
                           offset=42)
+    recs, offs = index_records(data, count)
+    return dims, chunk_shape, recs, offs, data
+
+
+_PARSE_ERRORS = {1: "truncated chunk record", 3: "truncated chunk payload"}
+
+
+def index_records(data, count: int):
+    """The record walk of read_file (container.py:82-145) in the native
+    library (``ebcc_parse_records``): RECORD_DTYPE records and the absolute
+    payload offset of each chunk; FormatError at the reference's offsets."""
+    import ctypes
+
+    from . import _lib
+    lib = _lib.load()
     recs = np.empty(count, dtype=RECORD_DTYPE)
     offs = np.empty(count, dtype=np.int64)
-    pos = HEADER.size
-    end = len(data)
-    for i in range(count):
-        if pos + RECORD.size > end:
-            raise FormatError("truncated chunk record", offset=pos)
-        rec = np.frombuffer(data, dtype=RECORD_DTYPE, count=1, offset=pos)[0]
-        if rec["mode"] > 2:
-            raise FormatError(f"unknown chunk mode {int(rec['mode'])}", offset=pos)
-        pos += RECORD.size
-        n = int(rec["base_len"]) + int(rec["resid_len"])
-        if pos + n > end:
-            raise FormatError("truncated chunk payload", offset=pos)
-        recs[i] = rec
-        offs[i] = pos
-        pos += n
-    if pos != end:
-        raise FormatError(f"{end - pos} trailing bytes after last chunk", offset=pos)
-    return dims, chunk_shape, recs, offs, data
+    view = np.frombuffer(data, dtype=np.uint8)
+    eoff = ctypes.c_int64(-1)
+    aux = ctypes.c_int32(0)
+    st = lib.ebcc_parse_records(view.ctypes.data if view.size else None, view.size, count,
+                                recs.ctypes.data if count else None,
+                                offs.ctypes.data if count else None, ctypes.byref(eoff),
+                                ctypes.byref(aux))
+    if st == _lib.OK:
+        return recs, offs
+    pos = int(eoff.value)
+    if st == _lib.E_FORMAT:
+        if aux.value == 2:
+            raise FormatError(f"unknown chunk mode {int(view[pos])}", offset=pos)
+        if aux.value == 4:
+            raise FormatError(f"{view.size - pos} trailing bytes after last chunk", offset=pos)
+        raise FormatError(_PARSE_ERRORS[aux.value], offset=pos)
+    raise FormatError("cannot index container records", offset=HEADER.size)
 
 
 def read_file(source):

@@ -19,6 +19,7 @@
 // the order is observably identical, and running both base-memo searches
 // first lets the residual encode reuse the base coefficient metadata arrays.
 #include <omp.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -61,14 +62,23 @@ struct CudaFail {
     if (e_ != cudaSuccess) throw CudaFail{e_, "engine.cu:" CK_STR(__LINE__) " " #x}; \
   } while (0)
 
+// workspace allocations add their size here (Workspace::bytes)
+thread_local int64_t* g_alloc_acc = nullptr;
+
 template <class T>
 T* dalloc(size_t count) {
   void* p = nullptr;
   if (count == 0) count = 1;
   cudaError_t e = cudaMalloc(&p, sizeof(T) * count);
   if (e != cudaSuccess) throw CudaFail{e, "cudaMalloc"};
+  if (g_alloc_acc) *g_alloc_acc += (int64_t)(sizeof(T) * count);
   return static_cast<T*>(p);
 }
+struct AllocScope {  // count the device allocations of this scope into `acc`
+  int64_t* prev;
+  explicit AllocScope(int64_t* acc) : prev(g_alloc_acc) { g_alloc_acc = acc; }
+  ~AllocScope() { g_alloc_acc = prev; }
+};
 
 // CPython float floor division (Objects/floatobject.c float_divmod), used by
 // base_codec.budget_for_ratio: int(raw // ratio) is NOT floor(raw / ratio).
@@ -324,6 +334,7 @@ struct ChunkSearch {
 struct Workspace {
   Geo g{};
   int cap = 0;  // fields
+  int64_t bytes = 0;  // device bytes held (allocations counted by AllocScope)
   float* x32 = nullptr;
   double *norm = nullptr, *A = nullptr, *B = nullptr, *base_dec = nullptr;
   int16_t *ec = nullptr, *ed = nullptr, *el = nullptr;
@@ -460,11 +471,22 @@ struct ebcc_ctx {
   std::vector<ebcc_ctx*> lanes;  // child contexts for concurrent sub-batches
   int machine_fields = 0;        // lanes: chunks whose machines run concurrently in total
   int last_batch = 0;            // chunks of the last compress batch (dev probe bench)
+  // batch plans (chunks per device batch), cached per call shape so that
+  // repeated calls neither query the free memory nor reallocate
+  struct Plan {
+    int rows = 0, cols = 0, levels = 0, lanes = 0;
+    int64_t nfields = -1, cap = 0;
+    bool matches(const Geo& g, int64_t nf, int l) const {
+      return rows == g.rows && cols == g.cols && levels == g.levels && nfields == nf && lanes == l;
+    }
+  } cplan, dplan;
 };
 
 namespace {
 
-void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
+// make c->ws a workspace of geometry g holding at least nfields chunks; a
+// new allocation takes max(nfields, want) chunks (want: the planned batch)
+void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields, int want = 0) {
   Workspace& w = c->ws;
   bool same_geo = w.g.rows == g.rows && w.g.cols == g.cols && w.g.levels == g.levels;
   if (same_geo && w.cap >= nfields) return;
@@ -487,10 +509,11 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields) {
       }
     }
   }
-  int cap = std::max(nfields, same_geo ? w.cap : 0);
+  int cap = std::max(std::max(nfields, want), same_geo ? w.cap : 0);
   w.release();
   w.g = g;
   w.cap = cap;
+  AllocScope acc(&w.bytes);
   const int64_t N = g.n * cap;
   w.x32 = dalloc<float>(N);
   w.norm = dalloc<double>(N);
@@ -576,6 +599,7 @@ MachineBufs machine_bufs(Workspace& w, int nfields, bool residual) {
 
 void ensure_dec2(Workspace& w) {
   if (w.dec2.mant) return;
+  AllocScope acc(&w.bytes);
   const size_t N = (size_t)w.g.n * w.cap;
   w.dec2.mant = dalloc<uint32_t>(N);
   w.dec2.sign_pos = dalloc<uint32_t>(N);
@@ -925,7 +949,8 @@ int64_t max_batch() {
 
 // chunks per batch: free-memory bound, queried only when the workspace does
 // not already cover the call (cudaMemGetInfo can stall for milliseconds)
-int64_t batch_cap(ebcc_ctx* c, const Geo& g, int64_t nfields, double share);
+int64_t plan_batch(ebcc_ctx* c, const Geo& g, int64_t want, int lanes, bool tree);
+int64_t balance(int64_t n, int64_t cap);
 
 // feasibility-only probes may skip settled CTAs (EBCC_EARLY=0 disables)
 bool early_ok() {
@@ -1595,20 +1620,63 @@ int ebcc_get_stats(const ebcc_ctx* c, ebcc_stats* out) {
 namespace {
 // compress nfields chunks on one context; the packed payload is left in
 // c->d_payload (c->payload_total bytes), per-chunk sizes in `sizes`
-int64_t batch_cap(ebcc_ctx* c, const Geo& g, int64_t nfields, double share) {
-  int64_t want = std::min<int64_t>(std::min<int64_t>(nfields, 4096), max_batch());
-  if (want < 1) want = 1;
-  const Workspace& w = c->ws;
-  if (w.cap >= want && w.g.rows == g.rows && w.g.cols == g.cols && w.g.levels == g.levels)
-    return want;
-  for (const Workspace& cw : c->ws_cache)
-    if (cw.cap >= want && cw.g.rows == g.rows && cw.g.cols == g.cols && cw.g.levels == g.levels)
-      return want;
-  size_t freeb = 0, totalb = 0;
-  CK(cudaMemGetInfo(&freeb, &totalb));
-  const int64_t per_field = g.n * 176 + 4096;  // ~176 B per point per chunk in flight
-  int64_t cap = (int64_t)((freeb * 0.6 * share) / per_field);
+// device bytes held by the workspaces of a context tree (the context and its
+// lanes); `caches` adds the parked workspaces of other chunk shapes
+int64_t tree_held(const ebcc_ctx* c, bool caches) {
+  int64_t b = c->ws.bytes;
+  if (caches)
+    for (const Workspace& w : c->ws_cache) b += w.bytes;
+  for (const ebcc_ctx* l : c->lanes) b += tree_held(l, caches);
+  return b;
+}
+void tree_drop_caches(ebcc_ctx* c) {
+  for (Workspace& w : c->ws_cache) w.release();
+  c->ws_cache.clear();
+  for (ebcc_ctx* l : c->lanes) tree_drop_caches(l);
+}
+// device bytes per chunk of a workspace of geometry g (measured from an
+// existing one, incl. the decompress decoder state; else ~262 B/pt), plus
+// the call's own payload / output buffers (~12 B/pt)
+int64_t per_field_bytes(const ebcc_ctx* c, const Geo& g) {
+  auto same = [&](const Workspace& w) {
+    return w.cap > 0 && w.g.rows == g.rows && w.g.cols == g.cols && w.g.levels == g.levels;
+  };
+  int64_t pf = g.n * 262 + (1 << 16);
+  auto take = [&](const Workspace& w) {
+    if (!same(w)) return;
+    int64_t b = w.bytes / w.cap + (w.dec2.mant ? 0 : g.n * 57);
+    pf = std::max<int64_t>(b, g.n * 64);
+  };
+  take(c->ws);
+  for (const ebcc_ctx* l : c->lanes) take(l->ws);
+  return pf + 12 * g.n;
+}
+// chunks per device batch for `lanes` concurrent sub-batches of up to `want`
+// chunks each: 85% of (free HBM + what this tree's workspaces hold) minus a
+// 1 GiB reserve, split evenly.  `tree` = every lane's workspace may be
+// reallocated (compress); otherwise only c->ws (decompress).
+int64_t plan_batch(ebcc_ctx* c, const Geo& g, int64_t want, int lanes, bool tree) {
+  want = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, 4096), max_batch()));
+  const int64_t pf = per_field_bytes(c, g);
+  auto cap_now = [&]() {
+    size_t freeb = 0, totalb = 0;
+    CK(cudaMemGetInfo(&freeb, &totalb));
+    const double avail = (double)freeb + (double)(tree ? tree_held(c, false) : c->ws.bytes) -
+                         (double)(1ll << 30);
+    return (int64_t)(avail * 0.85 / std::max(1, lanes) / (double)pf);
+  };
+  int64_t cap = cap_now();
+  if (cap < want && tree_held(c, true) > tree_held(c, false)) {
+    tree_drop_caches(c);  // parked workspaces of other shapes give way
+    cap = cap_now();
+  }
   return cap < 1 ? 1 : (cap > want ? want : cap);
+}
+// balanced batches: ceil(n / cap) batches of near-equal size
+int64_t balance(int64_t n, int64_t cap) {
+  if (n <= 0) return 1;
+  const int64_t nb = (n + cap - 1) / cap;
+  return (n + nb - 1) / nb;
 }
 
 // lanes: their input copies run one after another (lane k's copy starts
@@ -1622,7 +1690,7 @@ struct CopyChain {
 int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t rows, int32_t cols,
                   double eps_rel, double q, double r0, double search_tol, int32_t flags,
                   ebcc_chunk_rec* recs, std::vector<int64_t>& sizes, cudaEvent_t start_after,
-                  double mem_share, CopyChain* chain = nullptr, int lane = 0) {
+                  int64_t plan_cap, CopyChain* chain = nullptr, int lane = 0) {
   struct ChainRelease {  // a lane that fails before its copy must not stall the next
     CopyChain* ch; int k; bool done = false;
     ~ChainRelease() {
@@ -1640,7 +1708,7 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
     if (start_after) CK(cudaStreamWaitEvent(st, start_after, 0));
     int levels = clamp_levels(rows, cols, default_levels(rows, cols));
     Geo g = make_geo(rows, cols, levels);
-    const int64_t cap = batch_cap(c, g, nfields, mem_share);
+    const int64_t cap = balance(nfields, plan_cap);
     cudaEvent_t t0 = c->cev0, t1 = c->cev1;
     cudaEventRecord(t0, st);
     std::vector<PackPart> parts;
@@ -1649,7 +1717,7 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
     g_slow.mark("compress_setup");
     for (int64_t f0 = 0; f0 < nfields; f0 += cap) {
       int nb = (int)std::min<int64_t>(cap, nfields - f0);
-      ensure_workspace(c, g, nb);
+      ensure_workspace(c, g, nb, (int)cap);
       g_slow.mark("ensure_workspace");
       CK(cudaGetLastError());
       const float* src = fields + f0 * g.n;
@@ -1829,6 +1897,17 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
     CK(cudaSetDevice(c->device));
     const int L = lanes_for(nfields, (int64_t)rows * cols);
     const int64_t n = (int64_t)rows * cols;
+    {
+      const int levels = clamp_levels(rows, cols, default_levels(rows, cols));
+      const Geo g = make_geo(rows, cols, levels);
+      for (int k = 0; k < (L > 1 ? L : 0); k++) lane_ctx(c, k);  // the tree the plan covers
+      if (!c->cplan.matches(g, nfields, L)) {
+        c->cplan.cap = plan_batch(c, g, (nfields + L - 1) / L, L, true);
+        c->cplan.rows = g.rows; c->cplan.cols = g.cols; c->cplan.levels = g.levels;
+        c->cplan.nfields = nfields; c->cplan.lanes = L;
+      }
+    }
+    const int64_t plan_cap = c->cplan.cap;
     g_trace.start();
     struct TraceDump { ~TraceDump() { g_trace.dump(); } } trace_dump;
     std::vector<int64_t> sizes;
@@ -1838,7 +1917,7 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
     ebcc_stats total_stats{};
     if (L == 1) {
       status = compress_impl(c, fields, nfields, rows, cols, eps_rel, q, r0, search_tol, flags,
-                             recs, sizes, nullptr, 1.0);
+                             recs, sizes, nullptr, plan_cap);
       total_stats = c->stats;
       if (status != EBCC_OK && status != EBCC_E_RESIDUAL) return status;
     } else {
@@ -1862,7 +1941,7 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
           cudaSetDevice(c->device);
           g_lane = k;
           lst[k] = compress_impl(ls[k], fields + lo[k] * n, lo[k + 1] - lo[k], rows, cols, eps_rel,
-                                 q, r0, search_tol, flags, recs + lo[k], lsz[k], t0, 1.0 / L,
+                                 q, r0, search_tol, flags, recs + lo[k], lsz[k], t0, plan_cap,
                                  &chain, k);
         });
       for (auto& t : th) t.join();
@@ -1945,12 +2024,15 @@ int ebcc_fetch_payload(ebcc_ctx* c, uint8_t* payload, int64_t cap, int32_t flags
 
 int ebcc_fetch_container(ebcc_ctx* c, const uint8_t* header42, const uint8_t* records25,
                          int64_t n, uint8_t* out, int64_t cap, int32_t flags, int64_t* out_len) {
-  if (!c || !header42 || !out || n < 0 || (n && !records25)) return fail(c, EBCC_E_ARGUMENT, "bad arguments");
-  const int64_t total = 42 + 25 * n + c->payload_total;
+  const bool body = (flags & EBCC_CONTAINER_BODY) != 0;  // records + payloads only
+  if (!c || (!header42 && !body) || !out || n < 0 || (n && !records25))
+    return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  const int64_t hlen = body ? 0 : 42;
+  const int64_t total = hlen + 25 * n + c->payload_total;
   if (out_len) *out_len = total;
   if (cap < total) return fail(c, EBCC_E_CAPACITY, "container buffer too small");
   std::vector<ContainerPart> parts((size_t)n);
-  int64_t src = 0, dst = 42;
+  int64_t src = 0, dst = hlen;
   for (int64_t i = 0; i < n; i++) {
     uint32_t bl, rl;
     memcpy(&bl, records25 + 25 * i + 17, 4);
@@ -1981,7 +2063,7 @@ int ebcc_fetch_container(ebcc_ctx* c, const uint8_t* header42, const uint8_t* re
     }
     ContainerPart* d_parts = reinterpret_cast<ContainerPart*>(c->d_cmeta);
     uint8_t* d_recs = c->d_cmeta + sizeof(ContainerPart) * n;
-    CK(cudaMemcpyAsync(c->d_cont, header42, 42, cudaMemcpyHostToDevice, st));
+    if (!body) CK(cudaMemcpyAsync(c->d_cont, header42, 42, cudaMemcpyHostToDevice, st));
     if (n) {
       CK(cudaMemcpyAsync(d_parts, parts.data(), sizeof(ContainerPart) * n, cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(d_recs, records25, 25 * n, cudaMemcpyHostToDevice, st));
@@ -2027,11 +2109,27 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
     Geo g = make_geo(rows, cols, levels);
     cudaEvent_t t0 = c->cev0, t1 = c->cev1;
     cudaEventRecord(t0, st);
-    const int64_t cap = batch_cap(c, g, nfields, 1.0);
+    // decompress borrows lane 0's workspace (idle between compress calls)
+    // instead of holding a second one of its own
+    struct LaneWs {
+      ebcc_ctx* c;
+      explicit LaneWs(ebcc_ctx* c_) : c(c_) {
+        if (!c->lanes.empty()) std::swap(c->ws, c->lanes[0]->ws);
+      }
+      ~LaneWs() {
+        if (!c->lanes.empty()) std::swap(c->ws, c->lanes[0]->ws);
+      }
+    } lane_ws(c);
+    if (!c->dplan.matches(g, nfields, 1)) {
+      c->dplan.cap = plan_batch(c, g, nfields, 1, false);
+      c->dplan.rows = g.rows; c->dplan.cols = g.cols; c->dplan.levels = g.levels;
+      c->dplan.nfields = nfields; c->dplan.lanes = 1;
+    }
+    const int64_t cap = balance(nfields, c->dplan.cap);
     g_slow.mark("dec_meminfo");
     for (int64_t f0 = 0; f0 < nfields; f0 += cap) {
       int nb = (int)std::min<int64_t>(cap, nfields - f0);
-      ensure_workspace(c, g, nb);
+      ensure_workspace(c, g, nb, (int)cap);
       g_slow.mark("dec_workspace");
       Workspace& w = c->ws;
       // gather this batch's payload bytes into a staging buffer
@@ -2415,7 +2513,16 @@ std::mutex g_pin_mu;
 std::multimap<int64_t, void*> g_pin_free;
 std::unordered_map<void*, int64_t> g_pin_size;
 int64_t g_pin_cached = 0;
-constexpr int64_t kPinCacheMax = 8ll << 30;
+// freed page-locked blocks kept for reuse: up to a quarter of host RAM
+// (pinning a 9.8 GB result block costs seconds; reusing it nothing)
+int64_t pin_cache_max() {
+  static const int64_t m = [] {
+    const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
+    const int64_t ram = pages > 0 && psz > 0 ? (int64_t)pages * psz : (int64_t)32 << 30;
+    return std::max<int64_t>((int64_t)8 << 30, ram / 4);
+  }();
+  return m;
+}
 
 void pin_release_cached_locked() {
   for (auto& kv : g_pin_free) {
@@ -2461,7 +2568,7 @@ int ebcc_host_free(void* p) {
   if (it == g_pin_size.end()) return EBCC_E_ARGUMENT;
   g_pin_free.insert({it->second, p});
   g_pin_cached += it->second;
-  while (g_pin_cached > kPinCacheMax && !g_pin_free.empty()) {
+  while (g_pin_cached > pin_cache_max() && !g_pin_free.empty()) {
     auto v = g_pin_free.begin();  // smallest first
     g_pin_cached -= v->first;
     g_pin_size.erase(v->second);
@@ -2519,6 +2626,77 @@ int ebcc_dev_probe_bench(ebcc_ctx* c, double frac, int32_t iters, int32_t early,
     cudaGetLastError();
     return fail(c, EBCC_E_CUDA, std::string(e.what) + ": " + cudaGetErrorString(e.e));
   }
+}
+
+// container.read_file's record walk (container.py:82-145): records are
+// variable-length (25 B + payload), so the walk is sequential; a native loop
+// over 2,368 records takes microseconds (the Python loop: ~10 ms).
+int ebcc_parse_records(const uint8_t* data, int64_t len, int64_t count, uint8_t* records25,
+                       int64_t* offsets, int64_t* err_offset, int32_t* err_aux) {
+  if (!data || count < 0 || (count && (!records25 || !offsets)) || !err_offset || !err_aux)
+    return EBCC_E_ARGUMENT;
+  *err_offset = -1;
+  *err_aux = 0;
+  int64_t pos = 42;
+  for (int64_t i = 0; i < count; i++) {
+    if (pos + 25 > len) { *err_offset = pos; *err_aux = 1; return EBCC_E_FORMAT; }
+    const uint8_t mode = data[pos];
+    if (mode > 2) { *err_offset = pos; *err_aux = 2; return EBCC_E_FORMAT; }
+    memcpy(records25 + 25 * i, data + pos, 25);
+    uint32_t bl, rl;
+    memcpy(&bl, data + pos + 17, 4);
+    memcpy(&rl, data + pos + 21, 4);
+    pos += 25;
+    const int64_t n = (int64_t)bl + (int64_t)rl;
+    if (pos + n > len) { *err_offset = pos; *err_aux = 3; return EBCC_E_FORMAT; }
+    offsets[i] = pos;
+    pos += n;
+  }
+  if (pos != len) { *err_offset = pos; *err_aux = 4; return EBCC_E_FORMAT; }
+  return EBCC_OK;
+}
+
+// decompress_chunk's stream-header checks (pipeline.py:336-353,
+// spiht.parse_header spiht.py:67-78) for same-shape chunks: 'SP' magic,
+// positive dims equal to (rows, cols), levels >= 1 and <= 5, residual levels
+// equal to the base's.  *levels = the common level count (0 if every chunk is
+// constant); EBCC_E_FORMAT names the first bad chunk in *bad (its exact
+// reference message is produced by the caller); a chunk whose level count
+// differs from the first one's returns EBCC_E_ARGUMENT (mixed depths).
+int ebcc_check_streams(const uint8_t* data, int64_t len, const uint8_t* records25,
+                       const int64_t* offsets, int64_t n, int32_t rows, int32_t cols,
+                       int32_t* levels, int64_t* bad) {
+  if (!data || n < 0 || (n && (!records25 || !offsets)) || !levels || !bad) return EBCC_E_ARGUMENT;
+  *levels = 0;
+  *bad = -1;
+  auto hdr_ok = [&](int64_t off, int64_t ln, int* lv) {
+    if (ln < kHeader || off < 0 || off + ln > len) return false;
+    const uint8_t* h = data + off;
+    if (h[0] != 'S' || h[1] != 'P') return false;
+    uint32_t r, c;
+    memcpy(&r, h + 4, 4);
+    memcpy(&c, h + 8, 4);
+    if (r < 1 || c < 1 || h[3] < 1) return false;
+    if ((int64_t)r != rows || (int64_t)c != cols) return false;
+    *lv = h[3];
+    return true;
+  };
+  for (int64_t i = 0; i < n; i++) {
+    const uint8_t* rec = records25 + 25 * i;
+    const int mode = rec[0];
+    if (mode == EBCC_MODE_CONSTANT) continue;
+    uint32_t bl, rl;
+    memcpy(&bl, rec + 17, 4);
+    memcpy(&rl, rec + 21, 4);
+    int lv = 0, rlv = 0;
+    if (!hdr_ok(offsets[i], bl, &lv)) { *bad = i; return EBCC_E_FORMAT; }
+    if (mode == EBCC_MODE_TWO_LAYER && rl > 0 &&
+        (!hdr_ok(offsets[i] + bl, rl, &rlv) || rlv != lv)) { *bad = i; return EBCC_E_FORMAT; }
+    if (lv > 5) { *bad = i; return EBCC_E_FORMAT; }
+    if (*levels && lv != *levels) { *bad = i; return EBCC_E_ARGUMENT; }
+    *levels = lv;
+  }
+  return EBCC_OK;
 }
 
 int ebcc_selftest_div(ebcc_ctx* c, int64_t n, uint64_t seed, int64_t* mismatches) {

@@ -32,6 +32,15 @@ __device__ __forceinline__ float key_f32(unsigned int k) {
   return __uint_as_float(u);
 }
 
+// Signed zeros: numpy's float32 min/max keep one of several tied zeros by its
+// SIMD lane order, which differs between CPUs (and between positions of the
+// same data); this path pins "+0.0 preferred": the extremum is -0.0 only if
+// the field holds no +0.0 (max already behaves so in key order; for min the
+// two zero keys are swapped).  The oracle applies the same rule.
+__device__ __forceinline__ unsigned int zswap(unsigned int k) {
+  return k == 0x7fffffffu ? 0x80000000u : (k == 0x80000000u ? 0x7fffffffu : k);
+}
+
 __global__ void mm_init_kernel(unsigned int* mm, unsigned long long* first_bad, int nfields) {
   int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f < nfields) { mm[2 * f] = 0xffffffffu; mm[2 * f + 1] = 0u; first_bad[f] = ~0ull; }
@@ -48,7 +57,8 @@ __global__ void minmax_kernel(const float* __restrict__ x, int64_t n, unsigned i
     float v = xf[i];
     if (!isfinite(v)) bad = bad < (unsigned long long)i ? bad : (unsigned long long)i;
     unsigned int k = f32_key(v);
-    lo = k < lo ? k : lo;
+    const unsigned int km = zswap(k);
+    lo = km < lo ? km : lo;
     hi = k > hi ? k : hi;
   }
   if (bad != ~0ull) atomicMin(&first_bad[f], bad);  // core._check_finite, on device
@@ -68,7 +78,7 @@ __global__ void scalars_kernel(const unsigned int* mm, const unsigned long long*
                                int nfields, double eps_rel, FieldScal* fs) {
   int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nfields) return;
-  double vmin = (double)key_f32(mm[2 * f]), vmax = (double)key_f32(mm[2 * f + 1]);
+  double vmin = (double)key_f32(zswap(mm[2 * f])), vmax = (double)key_f32(mm[2 * f + 1]);
   double range = __dsub_rn(vmax, vmin);
   FieldScal s;
   s.vmin = vmin; s.vmax = vmax; s.range = range;

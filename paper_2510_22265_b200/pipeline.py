@@ -344,14 +344,9 @@ def records_to_grid(dims, chunk_shape, recs: np.ndarray, offs: np.ndarray, data:
         mode = recs["mode"].astype(np.int64)
         blen = recs["base_len"].astype(np.int64)
         rlen = recs["resid_len"].astype(np.int64)
-        nc = mode != 0
-        levels = 0
-        for i in np.flatnonzero(nc):
-            o = int(offs[i])
-            lv = _validate_payload(data, o, int(blen[i]), int(rlen[i]), int(mode[i]), h, w)
-            if levels and lv != levels:
-                return _records_to_grid_slow(dims, chunk_shape, recs, offs, data, ctx)
-            levels = lv
+        levels = _check_streams(buf, recs, offs, h, w)
+        if levels < 0:  # chunks of different depths
+            return _records_to_grid_slow(dims, chunk_shape, recs, offs, data, ctx)
         out = _lib.host_empty(dims, np.float32)
         lrec = np.zeros(len(recs), dtype=_lib.REC_DTYPE)
         lrec["mode"] = mode
@@ -363,6 +358,33 @@ def records_to_grid(dims, chunk_shape, recs: np.ndarray, offs: np.ndarray, data:
                          out=out.reshape(t * p, h, w), ctx=ctx)
         return out
     return _records_to_grid_slow(dims, chunk_shape, recs, offs, data, ctx)
+
+
+def _check_streams(buf: np.ndarray, recs: np.ndarray, offs: np.ndarray, rows: int,
+                   cols: int) -> int:
+    """Stream-header checks of every same-shape chunk in the native library
+    (``ebcc_check_streams``); returns the common level count (0: all
+    constant), -1 for mixed depths, and raises the reference's FormatError
+    for the first bad chunk."""
+    import ctypes
+    lib = _lib.load()
+    recs = np.ascontiguousarray(recs)
+    offs = np.ascontiguousarray(offs, dtype=np.int64)
+    lv = ctypes.c_int32(0)
+    bad = ctypes.c_int64(-1)
+    n = len(recs)
+    st = lib.ebcc_check_streams(buf.ctypes.data if buf.size else None, buf.size,
+                                recs.ctypes.data if n else None, offs.ctypes.data if n else None,
+                                n, rows, cols, ctypes.byref(lv), ctypes.byref(bad))
+    if st == _lib.OK:
+        return int(lv.value)
+    if st == _lib.E_ARGUMENT and bad.value >= 0:
+        return -1
+    i = int(bad.value)
+    # the exact reference message for that chunk
+    _validate_payload(buf, int(offs[i]), int(recs["base_len"][i]), int(recs["resid_len"][i]),
+                      int(recs["mode"][i]), rows, cols)
+    raise FormatError("bad stream header", offset=int(offs[i]))
 
 
 def _validate_payload(data, off, blen, rlen, mode, rows, cols) -> int:

@@ -3,8 +3,8 @@
 Chunks are independent (pipeline.py:358-367), so the data path
 has no collective: rank r compresses a contiguous block of chunks on its own
 GPU.  The one exchange is the final size all-gather (int64 per chunk) from
-which every rank derives its payload's offset in the container; the payload
-bytes are then gathered to rank 0, which writes the container (SURVEY.md
+which every rank derives its span of the container; every rank writes its
+records + payloads into one shared host segment (distributed.py; SURVEY.md
 §8(e)).  Over NVLink/NVSwitch the all-gather is a few KB; with the gloo
 backend the same code runs on CPU for the tests.
 """
@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .container import HEADER, RECORD, RECORD_DTYPE, assemble
+from .container import HEADER, RECORD
 
 
 def shard_bounds(nchunks: int, world: int, rank: int) -> tuple:
@@ -56,35 +56,20 @@ def container_offsets(all_sizes: np.ndarray) -> np.ndarray:
     return HEADER.size + starts
 
 
-def compress_sharded(grid, params, compress_records, group=None):
+def compress_sharded(grid, params, compress_records=None, group=None):
     """Compress a GridArray with its (default-chunked) slices split across the
-    ranks of ``group``.  ``compress_records(stack) -> (records[RECORD_DTYPE],
-    payload uint8, offsets)`` is the per-rank batch compressor (the GPU path
-    in production, the CPU oracle in tests).  Returns the container bytes on
-    rank 0 and None elsewhere."""
+    ranks of ``group``: :func:`distributed.compress_shard` on this rank's
+    block.  ``compress_records(stack) -> (records[RECORD_DTYPE], payload
+    uint8, offsets)`` replaces the device coder (the CPU oracle in the
+    multi-process tests); None = the GPU path.  Returns the container bytes
+    on rank 0 and None elsewhere."""
     import torch.distributed as dist
 
+    from .distributed import compress_shard
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     t, p, h, w = grid.dims
-    stack = grid.data.reshape(t * p, h, w)
-    n = stack.shape[0]
-    lo, hi = shard_bounds(n, world, rank)
-    recs, payload, offs = compress_records(stack[lo:hi])
-    local_sizes = (recs["base_len"].astype(np.int64) + recs["resid_len"].astype(np.int64))
-    exchange_sizes(local_sizes, n, group)  # every rank learns the layout
-    gathered = [None] * world if rank == 0 else None
-    dist.gather_object((recs.tobytes(), bytes(payload.tobytes()), offs.tolist()), gathered,
-                       dst=0, group=group)
-    if rank != 0:
-        return None
-    all_recs, parts, all_offs, base = [], [], [], 0
-    for rb, pb, ob in gathered:
-        r = np.frombuffer(rb, dtype=RECORD_DTYPE)
-        all_recs.append(r)
-        all_offs.extend(o + base for o in ob)
-        parts.append(pb)
-        base += len(pb)
-    records = np.concatenate(all_recs) if all_recs else np.zeros(0, RECORD_DTYPE)
-    payload = np.frombuffer(b"".join(parts), np.uint8)
-    return assemble(grid.dims, grid.chunk_shape, records, payload, np.asarray(all_offs, np.int64))
+    lo, hi = shard_bounds(t * p, world, rank)
+    stack = grid.data.reshape(t * p, h, w)[lo:hi]
+    return compress_shard(stack, grid.dims, params.epsilon_rel, params.q, group=group,
+                          coder=compress_records)
