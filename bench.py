@@ -54,6 +54,17 @@ WORKLOAD = ("configs[4]: 8 var x 37 levels x 8 steps = 2368 fields of 721x1440 f
             "(9.83 GB), eps_rel=1%")
 
 
+def workload(rank: int = 0, levels: int = 37) -> np.ndarray:
+    """configs[1]'s 37-level stack (developer tools in tools/ profile on it)."""
+    from paper_2510_22265_b200 import fields
+    out = np.empty((levels, ROWS, COLS), dtype=np.float32)
+    for lev in range(levels):
+        frac = lev / 36.0
+        out[lev] = fields.temperature_like(ROWS, COLS, seed=1000 + lev + 100 * rank,
+                                           mean=200.0 + 100.0 * frac, std=2.0 + 18.0 * frac)
+    return out
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as fh:

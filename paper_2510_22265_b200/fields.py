@@ -152,13 +152,35 @@ def config5_stack(ids, rows: int = GRID_025[0], cols: int = GRID_025[1],
     return np.frombuffer(buf, dtype=np.float32, count=n * rows * cols).reshape(shape)
 
 
+def vortex_like(rows: int, cols: int, seed: int) -> np.ndarray:
+    """Wind-speed-like field: the speed of a superposition of a few Gaussian
+    point vortices (random centres, radii, signed circulations) on a weak
+    k^-3 background; sharp cores and smooth far fields."""
+    gen = np.random.default_rng(seed)
+    y, x = np.mgrid[0:rows, 0:cols].astype(np.float64)
+    u = np.zeros((rows, cols))
+    v = np.zeros((rows, cols))
+    for _ in range(int(gen.integers(2, 6))):
+        y0, x0 = gen.uniform(0, rows), gen.uniform(0, cols)
+        rad = gen.uniform(0.05, 0.3) * max(rows, cols)
+        circ = gen.choice([-1.0, 1.0]) * gen.uniform(5.0, 30.0)
+        w = circ * np.exp(-((y - y0) ** 2 + (x - x0) ** 2) / (2.0 * rad * rad)) / rad
+        u -= w * (y - y0)
+        v += w * (x - x0)
+    speed = np.hypot(u, v) + 0.5 * power_law_grf(rows, cols, seed + 104729, 3.0)
+    return speed.astype(np.float32)
+
+
 def small_field(kind: str, rows: int, cols: int, seed: int) -> np.ndarray:
     """Small test fields: 'smooth', 'spiky' (isolated heavy-tailed outliers),
-    'precip' (intermittent), 'noise' (white) — float32."""
+    'precip' (intermittent), 'vortex' (point-vortex wind speed), 'noise'
+    (white) — float32."""
     if kind == "smooth":
         return temperature_like(rows, cols, seed=seed, mean=0.0, std=1.0)
     if kind == "precip":
         return precip_like(rows, cols, seed=seed)
+    if kind == "vortex":
+        return vortex_like(rows, cols, seed)
     if kind == "noise":
         return np.random.default_rng(seed).standard_normal((rows, cols)).astype(np.float32)
     if kind == "spiky":

@@ -1,4 +1,3 @@
 set -x
-timeout 300 python tools/host_io_probe.py > gpurun_out/r2_hostio.log 2>&1
-timeout 1200 python bench.py > gpurun_out/r2_bfull2.json 2> gpurun_out/r2_bfull2.err
-tail -n 5 gpurun_out/r2_bfull2.err
+timeout 600 python tools/prof_e2e_c5.py > gpurun_out/r2_e2e_pin.log 2>&1
+EBCC_HOSTPIN=0 TAG=nopin timeout 600 python tools/prof_e2e_c5.py > gpurun_out/r2_e2e_nopin.log 2>&1
