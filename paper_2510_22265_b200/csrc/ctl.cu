@@ -1,0 +1,587 @@
+// Device-resident feedback controller: the reference's searches as
+// per-chunk resumable state machines (see ctl.cuh).
+//
+// Each state machine is written as the reference's straight-line code with
+// every memo access a suspension point: CTL_GET(KEY, LABEL) looks the key up
+// and, if no probe has answered it yet, records LABEL, posts the probe and
+// returns; the next advance re-enters the switch at LABEL (a Duff's-device
+// coroutine; every variable that lives across a suspension is a CtlChunk
+// field).  One thread advances one chunk; a controller launch is a single
+// CTA that also sets the graph's conditional handles.
+#include <cstdio>
+
+#include "ctl.cuh"
+
+namespace ebcc {
+namespace {
+
+constexpr int kBasePlanes = 24, kDeepPlanes = 32;
+constexpr int kSuspend = 1, kDone = 0;
+
+// CPython float floor division (Objects/floatobject.c float_divmod), as
+// base_codec.budget_for_ratio uses it: int(raw // ratio) != floor(raw / ratio)
+__device__ double py_floordiv(double vx, double wx) {
+  const double mod = fmod(vx, wx);
+  double div = __ddiv_rn(__dsub_rn(vx, mod), wx);
+  if (mod != 0.0 && ((wx < 0) != (mod < 0))) div = __dsub_rn(div, 1.0);
+  double fl;
+  if (div != 0.0) {
+    fl = floor(div);
+    if (__dsub_rn(div, fl) > 0.5) fl = __dadd_rn(fl, 1.0);
+  } else {
+    fl = copysign(0.0, __ddiv_rn(vx, wx));
+  }
+  return fl;
+}
+
+__device__ __forceinline__ int64_t clamp_budget(const CtlChunk& s, int64_t b) {
+  if (b > s.raw) b = s.raw;
+  if (b < kHeader) b = kHeader;
+  return b;
+}
+// base_codec.budget_for_ratio (base_codec.py:34-38), then _ChunkCoder's clamp
+__device__ __forceinline__ int64_t ratio_budget(const CtlChunk& s, double ratio) {
+  int64_t b = (int64_t)py_floordiv((double)s.raw, ratio);
+  return clamp_budget(s, b > kHeader ? b : kHeader);
+}
+__device__ __forceinline__ int64_t stream_len(const CtlChunk& s, int64_t b) {
+  const int64_t full = kHeader + (int64_t)((s.T_base + 7) / 8);
+  return b < full ? b : full;
+}
+__device__ __forceinline__ int memo_find(const CtlChunk& s, int64_t b) {
+  for (int i = 0; i < s.nmemo; i++)
+    if (s.memo[i].budget == b) return i;
+  return -1;
+}
+__device__ __forceinline__ double q_of(const CtlChunk& s, int i) {
+  return __ddiv_rn((double)s.memo[i].count, (double)s.n);
+}
+__device__ __forceinline__ bool pure_ok_at(const CtlChunk& s, int i) {
+  return s.memo[i].maxerr <= s.eps_abs;
+}
+__device__ __forceinline__ int tmemo_find(const CtlChunk& s, int pi, int64_t t) {
+  for (int i = 0; i < s.ntmemo[pi]; i++)
+    if (s.tmemo[pi][i].t == t) return i;
+  return -1;
+}
+
+// ---- _search_base (pipeline.py:142-199) -------------------------------------
+// s.want_b / s.cur_b: the key and memo index of the access in progress
+#define CTL_GET_B(KEY, LABEL)                           \
+  s.want_b = (KEY);                                     \
+  case LABEL:                                           \
+    if ((s.cur_b = memo_find(s, s.want_b)) < 0) {       \
+      s.pc_b = LABEL;                                   \
+      return kSuspend;                                  \
+    }
+
+__device__ int adv_base(CtlChunk& s) {
+  switch (s.pc_b) {
+    case 0:
+      s.r_cap = fmax(1.0, __ddiv_rn((double)s.raw, (double)kHeader));
+      s.r0c = fmin(fmax(s.r0, 1.0), s.r_cap);
+      CTL_GET_B(ratio_budget(s, s.r0c), 1)
+      s.q_a0 = q_of(s, s.cur_b);
+      s.r_low = s.r_high = s.r0c;
+      s.have = s.q_a0 >= s.q;
+      s.q_a = s.q_a0;
+      while (s.q_a < s.q && s.r_low > 1.0) {
+        s.r_low = fmax(1.0, __ddiv_rn(s.r_low, 2.0));
+        CTL_GET_B(ratio_budget(s, s.r_low), 2)
+        s.q_a = q_of(s, s.cur_b);
+      }
+      if (s.q_a >= s.q) {
+        CTL_GET_B(ratio_budget(s, s.r_low), 3)
+        s.have = 1;
+      }
+      if (!s.have) {
+        CTL_GET_B(ratio_budget(s, 1.0), 4)
+        s.base_budget = s.memo[s.cur_b].budget;
+        s.done_b = 1;
+        s.pc_b = 99;
+        return kDone;
+      }
+      s.q_a = s.q_a0;
+      while (s.q_a > s.q && s.r_high < s.r_cap) {
+        s.r_high = fmin(s.r_cap, __dmul_rn(s.r_high, 2.0));
+        CTL_GET_B(ratio_budget(s, s.r_high), 5)
+        s.q_a = q_of(s, s.cur_b);
+      }
+      while (__dsub_rn(s.r_high, s.r_low) > s.tol) {
+        if (++s.guard > (1 << 20)) {  // the reference would spin forever here
+          s.status |= kCtlCapacity;
+          s.done_b = 1;
+          s.pc_b = 99;
+          return kDone;
+        }
+        s.r_mid = __dmul_rn(0.5, __dadd_rn(s.r_low, s.r_high));
+        CTL_GET_B(ratio_budget(s, s.r_mid), 6)
+        if (q_of(s, s.cur_b) < s.q) s.r_high = s.r_mid;
+        else s.r_low = s.r_mid;
+      }
+      // byte-exact refinement seeded from every budget cached so far
+      // (pipeline.py:193-198)
+      s.hi_b = -1;
+      s.lo_b = kHeader - 1;
+      for (int i = 0; i < s.nmemo; i++)
+        if (q_of(s, i) >= s.q && (s.hi_b < 0 || s.memo[i].budget < s.hi_b)) s.hi_b = s.memo[i].budget;
+      for (int i = 0; i < s.nmemo; i++)
+        if (q_of(s, i) < s.q && s.memo[i].budget < s.hi_b && s.memo[i].budget > s.lo_b)
+          s.lo_b = s.memo[i].budget;
+      // pipeline._bisect_min_feasible
+      while (s.hi_b - s.lo_b > 1) {
+        s.mid_b = (s.lo_b + s.hi_b) / 2;
+        CTL_GET_B(clamp_budget(s, s.mid_b), 7)
+        if (q_of(s, s.cur_b) >= s.q) s.hi_b = s.mid_b;
+        else s.lo_b = s.mid_b;
+      }
+      CTL_GET_B(clamp_budget(s, s.hi_b), 8)
+      s.base_budget = s.memo[s.cur_b].budget;
+      s.done_b = 1;
+      s.pc_b = 99;
+      return kDone;
+    default:
+      return kDone;
+  }
+}
+
+// ---- _search_pure (pipeline.py:215-236) ---------------------------------
+#define CTL_GET_P(KEY, LABEL)                           \
+  s.want_p = (KEY);                                     \
+  case LABEL:                                           \
+    if ((s.cur_p = memo_find(s, s.want_p)) < 0) {       \
+      s.pc_p = LABEL;                                   \
+      return kSuspend;                                  \
+    }
+
+__device__ int adv_pure(CtlChunk& s) {
+  switch (s.pc_p) {
+    case 0:
+      s.p_lb = kHeader;
+      s.p_ub = -1;
+      CTL_GET_P(clamp_budget(s, kHeader), 1)
+      if (pure_ok_at(s, s.cur_p)) {
+        s.pure_budget = s.memo[s.cur_p].budget;
+        s.done_p = 1;
+        s.pc_p = 99;
+        return kDone;
+      }
+      s.p_lb = kHeader + 1;
+      CTL_GET_P(clamp_budget(s, s.raw), 2)
+      if (!pure_ok_at(s, s.cur_p)) {
+        s.pure_budget = -1;
+        s.done_p = 1;
+        s.pc_p = 99;
+        return kDone;
+      }
+      s.lo_p = kHeader;
+      s.hi_p = s.raw;
+      // sorted(self._by_budget): every budget cached at this point
+      s.ncached = s.nmemo;
+      for (int i = 0; i < s.ncached; i++) {
+        const int64_t b = s.memo[i].budget;
+        int j = i;
+        while (j > 0 && s.cached[j - 1] > b) {
+          s.cached[j] = s.cached[j - 1];
+          j--;
+        }
+        s.cached[j] = b;
+      }
+      for (int i = 0; i < s.ncached; i++)
+        if (pure_ok_at(s, memo_find(s, s.cached[i])) && s.cached[i] < s.hi_p) s.hi_p = s.cached[i];
+      for (int i = 0; i < s.ncached; i++)
+        if (s.cached[i] < s.hi_p && !pure_ok_at(s, memo_find(s, s.cached[i])) &&
+            s.cached[i] > s.lo_p)
+          s.lo_p = s.cached[i];
+      while (s.hi_p - s.lo_p > 1) {
+        s.mid_p = (s.lo_p + s.hi_p) / 2;
+        s.p_lb = stream_len(s, s.lo_p + 1);  // the answer's bracket (candidate pruning)
+        s.p_ub = stream_len(s, s.hi_p);
+        CTL_GET_P(clamp_budget(s, s.mid_p), 3)
+        if (pure_ok_at(s, s.cur_p)) s.hi_p = s.mid_p;
+        else s.lo_p = s.mid_p;
+      }
+      CTL_GET_P(clamp_budget(s, s.hi_p), 4)
+      s.pure_budget = s.memo[s.cur_p].budget;
+      s.done_p = 1;
+      s.pc_p = 99;
+      return kDone;
+    default:
+      return kDone;
+  }
+}
+
+// ---- _truncation_search (pipeline.py:243-254), 24 then 32 planes ----------
+#define CTL_GET_T(KEY, LABEL)                                     \
+  s.want_t = (KEY);                                               \
+  case LABEL:                                                     \
+    if ((s.cur_t = tmemo_find(s, s.pass, s.want_t)) < 0) {        \
+      s.pc_t = LABEL;                                             \
+      return kSuspend;                                            \
+    }                                                             \
+    s.ntcalls++;
+
+__device__ __forceinline__ double terr(const CtlChunk& s) { return s.tmemo[s.pass][s.cur_t].err; }
+
+__device__ int adv_trunc(CtlChunk& s) {
+  switch (s.pc_t) {
+    case 0:
+      s.pass = 0;
+      while (s.pass < 2) {
+        s.total_t = (int64_t)(((s.pass ? s.T32 : s.T24) + 7) / 8);
+        s.t_lb = 0;
+        s.t_ub = -1;
+        s.spec[0] = s.total_t;      // a miss at err_at(0): 0, total and the
+        s.spec[1] = s.total_t / 2;  // first midpoint are all needed
+        CTL_GET_T(0, 1)
+        if (terr(s) <= s.eps_abs) {
+          s.trunc_t = 0;
+          s.trunc_planes = s.pass ? kDeepPlanes : kBasePlanes;
+          s.done_t = 1;
+          s.pc_t = 99;
+          return kDone;
+        }
+        s.spec[0] = s.total_t / 2;
+        s.spec[1] = -1;
+        CTL_GET_T(s.total_t, 2)
+        if (!(terr(s) <= s.eps_abs)) {  // this planes variant cannot reach the bound
+          s.pass++;
+          continue;
+        }
+        s.lo_t = 0;
+        s.hi_t = s.total_t;
+        while (s.hi_t - s.lo_t > 1) {
+          s.mid_t = (s.lo_t + s.hi_t) / 2;
+          s.t_lb = s.lo_t + 1;
+          s.t_ub = s.hi_t;
+          s.spec[0] = s.mid_t - s.lo_t > 1 ? (s.lo_t + s.mid_t) / 2 : -1;
+          s.spec[1] = s.hi_t - s.mid_t > 1 ? (s.mid_t + s.hi_t) / 2 : -1;
+          CTL_GET_T(s.mid_t, 3)
+          if (terr(s) <= s.eps_abs) s.hi_t = s.mid_t;
+          else s.lo_t = s.mid_t;
+        }
+        s.trunc_t = s.hi_t;
+        s.trunc_planes = s.pass ? kDeepPlanes : kBasePlanes;
+        s.done_t = 1;
+        s.pc_t = 99;
+        return kDone;
+      }
+      s.trunc_t = -1;
+      s.trunc_planes = 0;
+      s.done_t = 1;
+      s.pc_t = 99;
+      return kDone;
+    default:
+      return kDone;
+  }
+}
+
+// midpoint stopping plane of a decode of B bits of the `planes`-plane variant
+// (decode_with_plane, spiht.py:426-478, incl. zero-padded phantom planes)
+__device__ int n_last_of(const MachineOut& mo, const PlaneRec* pl, int planes, uint64_t B,
+                         uint64_t T) {
+  if (B == 0) return mo.n_max;
+  if (B <= T) {
+    int p = 0;
+    for (int k = 0; k < planes; k++)
+      if (pl[k].start < B) p = k;
+    return mo.n_max - p;
+  }
+  const uint64_t L = pl[planes - 1].lists_end;
+  int jmax;
+  if (L == 0) {
+    jmax = (kMaxDecodePlanes - 1) - planes;
+  } else {
+    const uint64_t j = (B - T + L - 1) / L - 1;
+    const uint64_t cap = (uint64_t)((kMaxDecodePlanes - 1) - planes);
+    jmax = (int)(j < cap ? j : cap);
+  }
+  return mo.n_max - (planes + jmax);
+}
+
+__device__ void memo_add(CtlChunk& s, int64_t b, const ProbeResult& r) {
+  if (memo_find(s, b) >= 0) return;
+  if (s.nmemo >= kCtlMemo) {
+    s.status |= kCtlCapacity;
+    return;
+  }
+  double e;
+  unsigned long long bits = r.maxerr;
+  memcpy(&e, &bits, 8);
+  s.memo[s.nmemo++] = CtlEntry{b, r.count, e};
+}
+__device__ void tmemo_add(CtlChunk& s, int pi, int64_t t, const ProbeResult& r) {
+  if (tmemo_find(s, pi, t) >= 0) return;
+  if (s.ntmemo[pi] >= kCtlTMemo) {
+    s.status |= kCtlCapacity;
+    return;
+  }
+  double e;
+  unsigned long long bits = r.maxerr;
+  memcpy(&e, &bits, 8);
+  s.tmemo[pi][s.ntmemo[pi]++] = CtlTEntry{t, e};
+}
+
+__device__ ProbeParam base_request(const CtlChunk& s, int64_t b, bool early) {
+  ProbeParam p{};
+  uint64_t B = (uint64_t)(stream_len(s, b) - kHeader) * 8;
+  if (B > s.T_base) B = s.T_base;
+  p.B = B;
+  p.planes = kBasePlanes;
+  p.active = 1;
+  p.early = early;
+  return p;
+}
+
+__device__ ProbeParam trunc_request(const CtlChunk& s, const CtlArgs& a, int f, int pi, int64_t t,
+                                    bool early) {
+  ProbeParam p{};
+  const int P = pi ? kDeepPlanes : kBasePlanes;
+  const uint64_t T = pi ? s.T32 : s.T24;
+  const uint64_t Bfull = (uint64_t)t * 8;
+  p.B = Bfull < T ? Bfull : T;
+  p.planes = P;
+  p.midpoint = 1;
+  const MachineOut mo = a.mo_res[f];
+  p.n_last = mo.n_max == kExpNone ? 0
+                                   : n_last_of(mo, a.pl_res + (int64_t)f * kMaxPlaneRecs, P, Bfull, T);
+  p.active = 1;
+  p.early = early;
+  return p;
+}
+
+// the controller is one CTA; `any` is or-reduced over it
+__device__ __forceinline__ bool block_any(bool v) { return __syncthreads_or(v) != 0; }
+
+__global__ void __launch_bounds__(1024) ctl_setup_kernel(CtlArgs a) {
+  const CtlParams P = *a.prm_in;
+  for (int f = threadIdx.x; f < a.nfields; f += blockDim.x) {
+    const FieldScal fs = a.fs[f];
+    const bool act = !fs.constant && fs.first_bad < 0;
+    a.active[f] = act;
+    MachineOut m{};
+    m.n_max = kExpNone;
+    a.mo_base[f] = m;
+    a.mo_res[f] = m;
+    CtlChunk& s = a.cs[f];
+    s.n = a.n;
+    s.raw = 4 * a.n;
+    s.q = P.q;
+    s.r0 = P.r0;
+    s.tol = P.tol;
+    s.eps_abs = fs.eps_abs;
+    s.T_base = s.T24 = s.T32 = 0;
+    s.active = act;
+    s.status = 0;
+    s.nmemo = 0;
+    s.pend = 0;
+    s.pend_budget = -1;
+    s.pc_b = s.pc_p = s.pc_t = 0;
+    s.guard = 0;
+    s.done_b = s.done_p = s.done_t = act ? 0 : 1;
+    s.base_budget = s.pure_budget = s.trunc_t = -1;
+    s.trunc_planes = 0;
+    s.ntcalls = 0;
+    s.pure_pruned = s.trunc_pruned = 0;
+    s.p_lb = kHeader;
+    s.p_ub = -1;
+    s.t_lb = 0;
+    s.t_ub = -1;
+    s.ntmemo[0] = s.ntmemo[1] = 0;
+    for (int k = 0; k < kCtlSlots; k++) s.tpend[k] = -1;
+    s.tpend_pi = 0;
+  }
+  if (threadIdx.x == 0) *a.stats = CtlStats{};
+}
+
+__global__ void __launch_bounds__(1024) ctl_base_kernel(CtlArgs a, int start, int set) {
+  bool any = false;
+  for (int f = threadIdx.x; f < a.nfields; f += blockDim.x) {
+    CtlChunk& s = a.cs[f];
+    ProbeParam p{};
+    if (s.active) {
+      if (start) {
+        s.T_base = a.mo_base[f].total_bits;
+        if (a.mo_base[f].overflow) s.status |= kCtlCapacity;
+      }
+      if (s.pend) {  // the probe that answered s.pend_budget
+        memo_add(s, s.pend_budget, a.res[f]);
+        s.pend = 0;
+      }
+      if (!s.done_b && !(s.status & kCtlCapacity) && adv_base(s) == kSuspend) {
+        s.pend = 1;
+        s.pend_budget = s.want_b;
+        p = base_request(s, s.want_b, false);
+        any = true;
+      }
+    }
+    a.res[f] = ProbeResult{};
+    a.prm[f] = p;
+  }
+  any = block_any(any);
+  if (threadIdx.x == 0) {
+    if (set & 1) cudaGraphSetConditional(a.h_loop, any ? 1u : 0u);
+    if (set & 2) cudaGraphSetConditional(a.h_pure, any ? 1u : 0u);
+    if (!start) a.stats->base_steps++;
+    if (any) a.stats->base_probes++;
+  }
+}
+
+__global__ void __launch_bounds__(1024) ctl_residue_kernel(CtlArgs a) {
+  for (int f = threadIdx.x; f < a.nfields; f += blockDim.x) {
+    const CtlChunk& s = a.cs[f];
+    ProbeParam p{};
+    if (s.active && s.base_budget >= 0) p = base_request(s, s.base_budget, false);
+    a.prm[f] = p;
+  }
+}
+
+__global__ void __launch_bounds__(1024) ctl_joint_kernel(CtlArgs a, int start, int set) {
+  const CtlParams P = *a.prm_in;
+  bool anyp = false, anyt = false;
+  const int nf = a.nfields;
+  if (start) {  // the residual stream's lengths; the searches start at the first step
+    for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+      CtlChunk& s = a.cs[f];
+      if (!s.active) continue;
+      const MachineOut mo = a.mo_res[f];
+      if (mo.overflow) s.status |= kCtlCapacity;
+      if (mo.n_max != kExpNone) {
+        s.T32 = mo.total_bits;
+        s.T24 = a.pl_res[(int64_t)f * kMaxPlaneRecs + kBasePlanes].start;
+      }
+      s.pend = 0;
+      for (int k = 0; k < kCtlSlots; k++) s.tpend[k] = -1;
+    }
+    return;
+  }
+  for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+    CtlChunk& s = a.cs[f];
+    ProbeParam pp{};
+    ProbeParam tp[kCtlSlots] = {};
+    if (s.active) {
+      if (s.pend) {
+        memo_add(s, s.pend_budget, a.res[f]);
+        s.pend = 0;
+      }
+      for (int k = 0; k < a.slots; k++)
+        if (s.tpend[k] >= 0) tmemo_add(s, s.tpend_pi, s.tpend[k], a.tres[k * nf + f]);
+      for (int k = 0; k < kCtlSlots; k++) s.tpend[k] = -1;
+      bool p_open = false, t_open = false;
+      if (!s.done_p && !(s.status & kCtlCapacity) && adv_pure(s) == kSuspend) {
+        s.pend = 1;
+        s.pend_budget = s.want_p;
+        pp = base_request(s, s.want_p, P.early != 0);
+        p_open = true;
+      }
+      if (!s.done_t && !(s.status & kCtlCapacity) && adv_trunc(s) == kSuspend) {
+        s.tpend_pi = s.pass;
+        s.tpend[0] = s.want_t;
+        tp[0] = trunc_request(s, a, f, s.pass, s.want_t, P.early != 0);
+        // speculative slots: points the next step needs whichever way this
+        // probe answers (same planes variant)
+        for (int k = 0; k + 1 < a.slots && k < 2; k++) {
+          const int64_t t2 = s.spec[k];
+          if (t2 < 0 || t2 == s.want_t || tmemo_find(s, s.pass, t2) >= 0) continue;
+          s.tpend[k + 1] = t2;
+          tp[k + 1] = trunc_request(s, a, f, s.pass, t2, P.early != 0);
+        }
+        t_open = true;
+      }
+      if (P.prune && (p_open || t_open)) {
+        // candidate pruning (pipeline.py:315-329 picks min((len, 0|1))): stop
+        // a search whose candidate can no longer win; same chosen candidate
+        const int64_t base_len = stream_len(s, s.base_budget);
+        int64_t two_ub = -1, pure_ub = -1;
+        if (s.trunc_planes) two_ub = base_len + kHeader + s.trunc_t;
+        else if (t_open && s.t_ub >= 0) two_ub = base_len + kHeader + s.t_ub;
+        if (s.done_p && s.pure_budget >= 0) pure_ub = stream_len(s, s.pure_budget);
+        else if (p_open && s.p_ub >= 0) pure_ub = s.p_ub;
+        const int64_t two_lb = base_len + kHeader + (t_open ? s.t_lb : 0);
+        if (p_open && two_ub >= 0 && s.p_lb > two_ub) {
+          s.done_p = 1;  // the two-layer candidate is strictly shorter
+          s.pure_budget = -1;
+          s.pure_pruned = 1;
+          s.pend = 0;
+          pp = ProbeParam{};
+          p_open = false;
+        } else if (t_open && pure_ub >= 0 && two_lb >= pure_ub) {
+          s.done_t = 1;  // pure-base is no longer (ties go to pure-base)
+          s.trunc_pruned = 1;
+          s.trunc_t = -1;
+          s.trunc_planes = 0;
+          for (int k = 0; k < kCtlSlots; k++) {
+            s.tpend[k] = -1;
+            tp[k] = ProbeParam{};
+          }
+          t_open = false;
+        }
+      }
+      anyp |= p_open;
+      anyt |= t_open;
+    }
+    a.prm[f] = pp;
+    a.res[f] = ProbeResult{};
+    for (int k = 0; k < a.slots; k++) {
+      a.tprm[k * nf + f] = tp[k];
+      a.tres[k * nf + f] = ProbeResult{};
+    }
+  }
+  anyp = block_any(anyp);
+  anyt = block_any(anyt);
+  if (threadIdx.x == 0) {
+    if (set & 1) cudaGraphSetConditional(a.h_loop, (anyp || anyt) ? 1u : 0u);
+    if (set & 2) cudaGraphSetConditional(a.h_pure, anyp ? 1u : 0u);
+    if (set & 4) cudaGraphSetConditional(a.h_trunc, anyt ? 1u : 0u);
+    a.stats->joint_steps++;
+    if (anyp) a.stats->pure_probes++;
+    if (anyt) a.stats->trunc_probes++;
+  }
+}
+
+__global__ void __launch_bounds__(1024) ctl_finalize_kernel(CtlArgs a) {
+  for (int f = threadIdx.x; f < a.nfields; f += blockDim.x) {
+    const CtlChunk& s = a.cs[f];
+    CtlOut o{};
+    o.status = s.status;
+    o.active = s.active;
+    o.base_budget = s.base_budget;
+    o.pure_budget = s.pure_budget;
+    o.trunc_t = s.trunc_t;
+    o.trunc_planes = s.trunc_planes;
+    o.n_base_probes = s.nmemo;
+    o.n_trunc_probes = s.ntcalls;
+    o.pure_pruned = s.pure_pruned;
+    o.trunc_pruned = s.trunc_pruned;
+    o.T_base = s.T_base;
+    o.T24 = s.T24;
+    o.T32 = s.T32;
+    a.out[f] = o;
+  }
+}
+
+inline int ctl_threads(int nfields) {
+  int t = 32;
+  while (t < nfields && t < 1024) t *= 2;
+  return t;
+}
+
+}  // namespace
+
+void ctl_setup(const CtlArgs& a, cudaStream_t st) {
+  ctl_setup_kernel<<<1, ctl_threads(a.nfields), 0, st>>>(a);
+}
+void ctl_base(const CtlArgs& a, bool start, int set, cudaStream_t st) {
+  ctl_base_kernel<<<1, ctl_threads(a.nfields), 0, st>>>(a, start ? 1 : 0, set);
+}
+void ctl_residue(const CtlArgs& a, cudaStream_t st) {
+  ctl_residue_kernel<<<1, ctl_threads(a.nfields), 0, st>>>(a);
+}
+void ctl_joint(const CtlArgs& a, bool start, int set, cudaStream_t st) {
+  ctl_joint_kernel<<<1, ctl_threads(a.nfields), 0, st>>>(a, start ? 1 : 0, set);
+}
+void ctl_finalize(const CtlArgs& a, cudaStream_t st) {
+  ctl_finalize_kernel<<<1, ctl_threads(a.nfields), 0, st>>>(a);
+}
+
+}  // namespace ebcc

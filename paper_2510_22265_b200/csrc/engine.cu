@@ -42,6 +42,7 @@
 #include "probe.cuh"
 #include "spiht.cuh"
 #include "ctx.cuh"
+#include "ctl.cuh"
 
 using namespace ebcc;
 
@@ -80,22 +81,6 @@ struct AllocScope {  // count the device allocations of this scope into `acc`
   explicit AllocScope(int64_t* acc) : prev(g_alloc_acc) { g_alloc_acc = acc; }
   ~AllocScope() { g_alloc_acc = prev; }
 };
-
-// CPython float floor division (Objects/floatobject.c float_divmod), used by
-// base_codec.budget_for_ratio: int(raw // ratio) is NOT floor(raw / ratio).
-double py_floordiv(double vx, double wx) {
-  double mod = std::fmod(vx, wx);
-  double div = (vx - mod) / wx;
-  if (mod != 0.0 && ((wx < 0) != (mod < 0))) div -= 1.0;
-  double fl;
-  if (div != 0.0) {
-    fl = std::floor(div);
-    if (div - fl > 0.5) fl += 1.0;
-  } else {
-    fl = std::copysign(0.0, vx / wx);
-  }
-  return fl;
-}
 
 // host memcpy split over a thread team (first-touch page faults of a fresh
 // destination are spread over the team too)
@@ -137,211 +122,10 @@ bool is_pageable(const void* p) {
   return a.type == cudaMemoryTypeUnregistered;
 }
 
-struct NeedBase { int64_t budget; };
 // truncation probes per chunk and step: the bisection's next midpoint plus
 // the two points one level further (one of which the next step needs)
-constexpr int kTruncSlots = 3;
+constexpr int kTruncSlots = kCtlSlots;
 struct IngestFail {};
-struct NeedTrunc { int planes; int64_t t; };
-
-// ---------------------------------------------------------------------------
-// per-chunk search state (a restatement of pipeline._ChunkCoder + searches)
-struct Entry {
-  int64_t budget, len;
-  uint64_t count;
-  double maxerr;
-};
-
-struct ChunkSearch {
-  int64_t n = 0, raw = 0;
-  double q = 0, r0 = 0, tol = 0, eps_abs = 0;
-  uint64_t T_base = 0;                 // bits of the full 24-plane base stream
-  std::vector<Entry> memo;             // insertion order = seq
-  std::unordered_map<int64_t, int> at; // budget -> memo index
-  size_t vsize = 0;                    // replay timeline position
-  std::unordered_map<int64_t, double> trunc[2];  // (24|32) t -> err
-
-  bool constant = false, failed = false, pure_done = false;
-  int phase = 0;                       // 0 base, 1 pure, 2 trunc, 3 done
-  int64_t pending = -1;                // budget of the base-memo probe in flight
-  int64_t tpending = -1;               // offset of the truncation probe in flight
-  int tpending_planes = 0;
-  int64_t base_budget = -1, pure_budget = -1;
-  int64_t trunc_t = -1;
-  int trunc_planes = 0;
-  int n_trunc_calls = 0;
-  // Candidate pruning: bounds on the two candidates' sizes at the first
-  // replay miss (the bisections keep the answer inside their bracket and
-  // stream_len is non-decreasing).  -1 = unknown.
-  int64_t p_lb = 0, p_ub = -1;     // pure-base payload bytes
-  int64_t t_lb = 0, t_ub = -1;     // residual prefix bytes t
-  int64_t spec[2] = {-1, -1};      // speculative truncation offsets at the first miss
-  bool pure_pruned = false, trunc_pruned = false;
-
-  int64_t clamp_budget(int64_t b) const {
-    if (b > raw) b = raw;
-    if (b < kHeader) b = kHeader;
-    return b;
-  }
-  int64_t stream_len(int64_t b) const {
-    int64_t full = kHeader + (int64_t)((T_base + 7) / 8);
-    return b < full ? b : full;
-  }
-  // Replay miss handling: the first memo miss of a replay is the probe to
-  // run next.  Instead of unwinding (an exception per chunk per step), the
-  // replay continues on a dummy infeasible answer (q = 0, error = inf), which
-  // drives every loop of the searches to termination; its result is ignored.
-  bool missed = false;
-  int64_t miss_key = -1;
-  int miss_planes = 0;
-  Entry dummy{};
-
-  // _ChunkCoder.at_budget with the replay timeline
-  const Entry& at_budget(int64_t b) {
-    b = clamp_budget(b);
-    auto it = at.find(b);
-    if (it == at.end()) {
-      if (!missed) { missed = true; miss_key = b; }
-      dummy = Entry{b, 0, 0, INFINITY};
-      return dummy;
-    }
-    size_t seq = (size_t)it->second;
-    if (seq == vsize) vsize++;
-    return memo[seq];
-  }
-  double q_of(const Entry& e) const { return (double)e.count / (double)n; }
-  int64_t budget_for_ratio(double ratio) const {
-    double raw_f = (double)raw;
-    int64_t b = (int64_t)py_floordiv(raw_f, ratio);
-    return b > kHeader ? b : kHeader;
-  }
-  const Entry& at_ratio(double ratio) { return at_budget(budget_for_ratio(ratio)); }
-  bool pure_ok(int64_t b) { return at_budget(b).maxerr <= eps_abs; }
-
-  // pipeline._bisect_min_feasible
-  template <class F>
-  static int64_t bisect(int64_t lo, int64_t hi, F feasible) {
-    while (hi - lo > 1) {
-      int64_t mid = (lo + hi) / 2;
-      if (feasible(mid)) hi = mid;
-      else lo = mid;
-    }
-    return hi;
-  }
-
-  // pipeline._search_base (pipeline.py:142-199) -> chosen budget
-  int64_t search_base() {
-    vsize = 0;
-    double r_cap = std::max(1.0, (double)raw / (double)kHeader);
-    double r0c = std::min(std::max(r0, 1.0), r_cap);
-    double q_a0 = q_of(at_ratio(r0c));
-    double r_low = r0c, r_high = r0c;
-    bool have = q_a0 >= q;
-    double q_a = q_a0;
-    while (q_a < q && r_low > 1.0) {
-      r_low = std::max(1.0, r_low / 2.0);
-      q_a = q_of(at_ratio(r_low));
-    }
-    if (q_a >= q) { at_ratio(r_low); have = true; }
-    if (!have) return at_ratio(1.0).budget;
-    q_a = q_a0;
-    while (q_a > q && r_high < r_cap) {
-      r_high = std::min(r_cap, r_high * 2.0);
-      q_a = q_of(at_ratio(r_high));
-    }
-    while (r_high - r_low > tol) {
-      double r_mid = 0.5 * (r_low + r_high);
-      if (q_of(at_ratio(r_mid)) < q) r_high = r_mid;
-      else r_low = r_mid;
-    }
-    int64_t hi = -1, lo = kHeader - 1;
-    for (size_t i = 0; i < vsize; i++)
-      if (q_of(memo[i]) >= q && (hi < 0 || memo[i].budget < hi)) hi = memo[i].budget;
-    for (size_t i = 0; i < vsize; i++)
-      if (q_of(memo[i]) < q && memo[i].budget < hi) lo = std::max(lo, memo[i].budget);
-    int64_t best = bisect(lo, hi, [&](int64_t b) { return q_of(at_budget(b)) >= q; });
-    return at_budget(best).budget;
-  }
-
-  // pipeline._search_pure (pipeline.py:215-236) -> budget or -1
-  int64_t search_pure(size_t base_entries) {
-    vsize = base_entries;
-    p_lb = kHeader;
-    p_ub = -1;
-    if (pure_ok(kHeader)) return at_budget(kHeader).budget;
-    if (!missed) p_lb = kHeader + 1;
-    if (!pure_ok(raw)) return -1;
-    int64_t lo = kHeader, hi = raw;
-    std::vector<int64_t> cached;
-    for (size_t i = 0; i < vsize; i++) cached.push_back(memo[i].budget);
-    std::sort(cached.begin(), cached.end());
-    for (int64_t b : cached)
-      if (pure_ok(b)) hi = std::min(hi, b);
-    for (int64_t b : cached)
-      if (b < hi && !pure_ok(b)) lo = std::max(lo, b);
-    // _bisect_min_feasible, noting the bracket (lo, hi] at the first miss
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) / 2;
-      const bool before = missed;
-      const bool ok = pure_ok(mid);
-      if (!before && missed) {
-        p_lb = stream_len(lo + 1);
-        p_ub = stream_len(hi);
-      }
-      if (ok) hi = mid;
-      else lo = mid;
-    }
-    return at_budget(hi).budget;
-  }
-
-  // pipeline._truncation_search for one planes variant -> t or -1
-  int64_t search_trunc(int pi, int64_t total) {
-    auto err_at = [&](int64_t t) -> double {
-      auto it = trunc[pi].find(t);
-      if (it == trunc[pi].end()) {
-        if (!missed) { missed = true; miss_key = t; miss_planes = pi; }
-        return INFINITY;
-      }
-      n_trunc_calls++;
-      return it->second;
-    };
-    n_trunc_calls = 0;
-    t_lb = 0;
-    t_ub = -1;
-    spec[0] = spec[1] = -1;
-    {
-      const bool before = missed;
-      const bool ok0 = err_at(0) <= eps_abs;
-      if (!before && missed) {  // 0, total and the first midpoint are all needed
-        spec[0] = total;
-        spec[1] = total / 2;
-      }
-      if (ok0) return 0;
-    }
-    {
-      const bool before = missed;
-      const bool ok = err_at(total) <= eps_abs;
-      if (!before && missed) spec[0] = total / 2;
-      if (!ok) return -1;
-    }
-    // this pass holds the answer: it lies in the bracket (lo, hi]
-    int64_t lo = 0, hi = total;
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) / 2;
-      const bool before = missed;
-      const bool ok = err_at(mid) <= eps_abs;
-      if (!before && missed) {
-        t_lb = lo + 1;
-        t_ub = hi;
-        spec[0] = mid - lo > 1 ? (lo + mid) / 2 : -1;
-        spec[1] = hi - mid > 1 ? (mid + hi) / 2 : -1;
-      }
-      if (ok) hi = mid;
-      else lo = mid;
-    }
-    return hi;
-  }
-};
 
 // ---------------------------------------------------------------------------
 struct Workspace {
@@ -398,8 +182,33 @@ struct Workspace {
   ProbeResult* h_res = nullptr;
   TreeTables tt{};
   bool has_tt = false;
+  // device controller (ctl.cuh): per-chunk search state, results, params
+  CtlChunk* ctl = nullptr;
+  CtlOut* ctl_out = nullptr;
+  CtlParams* ctl_prm = nullptr;
+  CtlStats* ctl_stats = nullptr;
+  CtlOut* h_ctl_out = nullptr;     // pinned mirrors read once per batch
+  FieldScal* h_fs = nullptr;
+  CtlStats* h_ctl_stats = nullptr;
+  CtlParams* h_ctl_prm = nullptr;
+  MachineOut* h_mo = nullptr;      // base then residual machine outputs (2 x cap)
+  // instantiated search graphs of this workspace, by batch shape
+  struct SearchGraph {
+    cudaGraphExec_t exec = nullptr;
+    int nf = -1, slots = 0, prune = -1, early = -1, inc = -1, cluster = -1;
+  };
+  std::vector<SearchGraph> graphs;
 
   void release() {
+    for (SearchGraph& sg : graphs)
+      if (sg.exec) cudaGraphExecDestroy(sg.exec);
+    graphs.clear();
+    void* cp[] = {ctl, ctl_out, ctl_prm, ctl_stats};
+    for (void* p : cp)
+      if (p) cudaFree(p);
+    void* hp[] = {h_ctl_out, h_fs, h_ctl_stats, h_ctl_prm, h_mo};
+    for (void* p : hp)
+      if (p) cudaFreeHost(p);
     void* ptrs[] = {x32, norm, A, B, base_dec, ec, ed, el, mant, sign_pos, lsp_rank, pinfo, hrel,
                     packed, ninfo,
                     packed2, sprank, sprank2, A2, B2,
@@ -481,6 +290,8 @@ struct ebcc_ctx {
   cudaEvent_t cev0 = nullptr, cev1 = nullptr;    // per-call timing (batch loop)
   cudaEvent_t oev0 = nullptr, oev1 = nullptr;    // per-call timing (ebcc_compress)
   cudaEvent_t tm_a = nullptr, tm_b = nullptr;
+  cudaStream_t cap[5] = {};      // graph capture streams (created on first use)
+  cudaEvent_t tev[2] = {};       // base-encode timing
   cudaStream_t join = nullptr;   // caller's default stream the library stream follows
   cudaEvent_t ev_join = nullptr;
   std::vector<ebcc_ctx*> lanes;  // child contexts for concurrent sub-batches
@@ -498,6 +309,12 @@ struct ebcc_ctx {
 };
 
 namespace {
+
+// graph capture streams of a context (created on first use)
+cudaStream_t cap_stream(ebcc_ctx* c, int k) {
+  if (!c->cap[k]) CK(cudaStreamCreateWithFlags(&c->cap[k], cudaStreamNonBlocking));
+  return c->cap[k];
+}
 
 // make c->ws a workspace of geometry g holding at least nfields chunks; a
 // new allocation takes max(nfields, want) chunks (want: the planned batch)
@@ -589,6 +406,15 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields, int want = 0) {
   w.icomputed = dalloc<unsigned long long>(2 * kMaxLevels);
   CK(cudaMallocHost(&w.h_prm, sizeof(ProbeParam) * (1 + kTruncSlots) * cap));
   CK(cudaMallocHost(&w.h_res, sizeof(ProbeResult) * (1 + kTruncSlots) * cap));
+  w.ctl = dalloc<CtlChunk>(cap);
+  w.ctl_out = dalloc<CtlOut>(cap);
+  w.ctl_prm = dalloc<CtlParams>(1);
+  w.ctl_stats = dalloc<CtlStats>(1);
+  CK(cudaMallocHost(&w.h_ctl_out, sizeof(CtlOut) * cap));
+  CK(cudaMallocHost(&w.h_fs, sizeof(FieldScal) * cap));
+  CK(cudaMallocHost(&w.h_ctl_stats, sizeof(CtlStats)));
+  CK(cudaMallocHost(&w.h_ctl_prm, sizeof(CtlParams)));
+  CK(cudaMallocHost(&w.h_mo, sizeof(MachineOut) * 2 * cap));
   build_tree_tables(g, w.tt, c->stream);
   w.has_tt = true;
 }
@@ -742,17 +568,21 @@ void h2d_small(ebcc_ctx* c, void* dst, const void* src, size_t n, cudaStream_t s
 
 // encode the pyramids in `coef` (all fields): exponents, machine (which
 // skips all-zero pyramids itself), refinement, packed metadata.  Async on st.
+// active == nullptr: the machine outputs and active flags were set on the
+// device (ctl_setup) - nothing is copied from the host (graph-capturable)
 void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const double* coef,
-                   bool packed_residual, const std::vector<uint8_t>& active, cudaStream_t st,
+                   bool packed_residual, const std::vector<uint8_t>* active, cudaStream_t st,
                    int cluster = 0) {
   Workspace& w = c->ws;
   CK(cudaGetLastError());  // surface anything deferred from before this encode
   MachineBufs mb = machine_bufs(w, nfields, residual);
-  std::vector<MachineOut> init(nfields);
-  for (auto& m : init) { m = MachineOut{}; m.n_max = kExpNone; }
-  h2d_small(c, mb.out, init.data(), sizeof(MachineOut) * nfields, st);
+  if (active) {
+    std::vector<MachineOut> init(nfields);
+    for (auto& m : init) { m = MachineOut{}; m.n_max = kExpNone; }
+    h2d_small(c, mb.out, init.data(), sizeof(MachineOut) * nfields, st);
+    h2d_small(c, w.active, active->data(), nfields, st);
+  }
   CK(cudaMemsetAsync(mb.bits, 0, sizeof(uint32_t) * mb.bit_stride * nfields, st));
-  h2d_small(c, w.active, active.data(), nfields, st);
   coef_prepare(coef, w.g.n, mb, w.g, st);
   CK(cudaGetLastError());
   subtree_exponents(mb, w.g, w.tt, st);
@@ -789,30 +619,10 @@ void encode_pyramids(ebcc_ctx* c, int nfields, bool residual, int planes,
   CK(cudaEventRecord(c->ev_a, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_a, 0));
   const int cluster = machine_cluster_size(false, std::max(nfields, c->machine_fields));
-  encode_launch(c, nfields, residual, planes, c->ws.A, residual, active, c->side, cluster);
+  encode_launch(c, nfields, residual, planes, c->ws.A, residual, &active, c->side, cluster);
   CK(cudaEventRecord(c->ev_b, c->side));
   CK(cudaStreamWaitEvent(c->stream, c->ev_b, 0));
   encode_collect(c, nfields, residual, active, mo, pl, c->stream);
-}
-
-// midpoint stopping plane of a decode of B bits of the `planes`-plane variant
-// (decode_with_plane, spiht.py:426-478, incl. zero-padded phantom planes)
-int n_last_of(const MachineOut& mo, const PlaneRec* pl, int planes, uint64_t B, uint64_t T) {
-  if (B == 0) return mo.n_max;
-  if (B <= T) {
-    int p = 0;
-    for (int k = 0; k < planes; k++)
-      if (pl[k].start < B) p = k;
-    return mo.n_max - p;
-  }
-  uint64_t L = pl[planes - 1].lists_end;
-  int jmax;
-  if (L == 0) jmax = (kMaxDecodePlanes - 1) - planes;
-  else {
-    uint64_t j = (B - T + L - 1) / L - 1;  // last j with T + j*L < B
-    jmax = (int)std::min<uint64_t>(j, (uint64_t)((kMaxDecodePlanes - 1) - planes));
-  }
-  return mo.n_max - (planes + jmax);
 }
 
 void put_header(uint8_t* h, int n_max, int levels, int rows, int cols) {
@@ -912,49 +722,6 @@ uint8_t* host_stage(ebcc_ctx* c, int64_t bytes) {
   return c->h_stage;
 }
 
-// One feedback-probe step (H2D params, reset results, the level kernels, D2H
-// results) replayed as a CUDA graph: the first step of each kind runs
-// eagerly (it also sets kernel attributes), the second is captured, later
-// steps only launch the graph.
-struct StepGraph {
-  cudaGraphExec_t exec = nullptr;
-  int eager = 0;
-  ~StepGraph() {
-    if (exec) cudaGraphExecDestroy(exec);
-  }
-  template <class F>
-  void run(cudaStream_t st, F enqueue) {
-    static const bool off = getenv("EBCC_GRAPHS") && getenv("EBCC_GRAPHS")[0] == '0';
-    if (off || eager < 1) {
-      enqueue(true);
-      eager++;
-      return;
-    }
-    if (!exec) {
-      cudaGraph_t gr = nullptr;
-      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      enqueue(false);
-      CK(cudaStreamEndCapture(st, &gr));
-      CK(cudaGraphInstantiate(&exec, gr, 0));
-      cudaGraphDestroy(gr);
-    }
-    CK(cudaGraphLaunch(exec, st));
-  }
-};
-
-// level-0 kernel timing: only eager (uncaptured) steps record the events
-void accumulate_level0(ebcc_ctx* c, bool timed, int nfields) {
-  if (!timed) return;
-  float ms = 0;
-  if (cudaEventElapsedTime(&ms, c->l0.a, c->l0.b) == cudaSuccess) {
-    c->stats.ms_probe_kernel += ms;
-    c->stats.probe_kernel_count++;
-    c->stats.probe_kernel_fields += nfields;
-  } else {
-    cudaGetLastError();
-  }
-}
-
 // chunks per device batch: bounded by free HBM (and EBCC_MAX_BATCH, which the
 // tests use to exercise the multi-batch path)
 int64_t max_batch() {
@@ -973,10 +740,66 @@ bool early_ok() {
   return on;
 }
 
-// one compress batch of nfields (<= workspace capacity); x already in w.x32
+// Add a conditional node (WHILE / IF on handle h) at the current capture
+// point of `st` and capture its body from `bst` (a stream not capturing).
+template <class F>
+void add_conditional(cudaStream_t st, cudaStream_t bst, cudaGraphConditionalHandle h,
+                     cudaGraphConditionalNodeType type, F fill) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t gr = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &gr, &deps, &nd));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = type;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, gr, deps, nd, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  CK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+  CK(cudaStreamBeginCaptureToGraph(bst, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  fill(body, bst);
+  cudaGraph_t out = nullptr;
+  CK(cudaStreamEndCapture(bst, &out));
+}
+
+CtlArgs ctl_args(Workspace& w, int nfields, int slots) {
+  CtlArgs a{};
+  a.cs = w.ctl;
+  a.out = w.ctl_out;
+  a.prm_in = w.ctl_prm;
+  a.stats = w.ctl_stats;
+  a.fs = w.fs;
+  a.mo_base = w.mo_base;
+  a.mo_res = w.mo_res;
+  a.pl_res = w.pl_res;
+  a.active = w.active;
+  a.prm = w.prm;
+  a.res = w.res;
+  a.tprm = w.prm + w.cap;
+  a.tres = w.res + w.cap;
+  a.nfields = nfields;
+  a.slots = slots;
+  a.n = w.g.n;
+  return a;
+}
+
+// One compress batch of nfields (<= workspace capacity); x already in w.x32.
 // in_groups > 0: the input arrives in that many field groups, group k
 // complete when in_ev[k] fires (host input copied group by group); each
-// group is normalised and transformed as soon as it lands
+// group is normalised and transformed as soon as it lands.
+//
+// Eagerly enqueued: ingest + normalise, forward DWT, controller setup and
+// the base encode.  Then ONE launch of the batch's search graph: the base
+// quantile search (a conditional WHILE loop: controller step -> batched
+// probe), the residue and the residual DWT + 32-plane encode, the joint
+// pure-base + truncation searches (a WHILE loop whose two probe branches are
+// IF nodes), and the copies of the candidate-choice inputs to the host.  The
+// controller (ctl.cu) advances every chunk's search on the device and sets
+// the loop conditions; the host synchronises once, after the graph, to pack
+// the chosen prefixes.
 int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0, double tol,
                    bool prune,
                    ebcc_chunk_rec* recs, int64_t out_base_off, std::vector<PackPart>& parts,
@@ -986,20 +809,19 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   const Geo& g = w.g;
   cudaStream_t st = c->stream;
   const int64_t N = g.n;
-
-  PhaseClock pc(st);
-  g_pc = pc.on ? &pc : nullptr;
-  double replay_ms = 0;
   c->last_batch = nfields;
-  // ---- ingest + normalise (core.normalize) ----
+  // ---- ingest + normalise (core.normalize) + forward DWT ----
   CK(cudaGetLastError());
   g_slow.mark("enter_batch");
   const bool grouped = in_groups > 0;
   if (!grouped) {
     ingest_normalize(w.x32, N, nfields, w.norm, w.fs, w.mm, eps_rel, st);
+    CK(cudaMemcpyAsync(w.A, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
+    forward_dwt(w.A, w.B, N, nfields, g, st);
+    c->stats.kernel_launches += 4 + 2 * g.levels;
   } else {
     // per group: normalise + forward DWT (the non-finite check is read after
-    // all groups; a failing input only costs the wasted transforms)
+    // the searches; a failing input only costs the wasted work)
     for (int k = 0; k < in_groups; k++) {
       const int a = (int)((int64_t)nfields * k / in_groups);
       const int b = (int)((int64_t)nfields * (k + 1) / in_groups);
@@ -1010,63 +832,19 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       CK(cudaMemcpyAsync(w.A + (int64_t)a * N, w.norm + (int64_t)a * N,
                          sizeof(double) * N * (b - a), cudaMemcpyDeviceToDevice, st));
       forward_dwt(w.A + (int64_t)a * N, w.B + (int64_t)a * N, N, b - a, g, st);
-      c->stats.kernel_launches += 2 * g.levels;
+      c->stats.kernel_launches += 4 + 2 * g.levels;
     }
   }
   CK(cudaGetLastError());
-  pc.mark("ingest");
-  c->stats.kernel_launches += 4;
-  std::vector<FieldScal> fs(nfields);
-  CK(cudaMemcpyAsync(fs.data(), w.fs, sizeof(FieldScal) * nfields, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
 
-  for (int f = 0; f < nfields; f++)
-    if (fs[f].first_bad >= 0) {
-      c->err_index = (int64_t)f * N + fs[f].first_bad;
-      throw IngestFail{};
-    }
-  std::vector<ChunkSearch> cs(nfields);
-  std::vector<uint8_t> active(nfields);
-  for (int f = 0; f < nfields; f++) {
-    ChunkSearch& s = cs[f];
-    s.n = N; s.raw = N * 4; s.q = q; s.r0 = r0; s.tol = tol; s.eps_abs = fs[f].eps_abs;
-    s.constant = fs[f].constant != 0;
-    active[f] = !s.constant;
-    if (s.constant) s.phase = 3;
-  }
-
-  // ---- base pyramid + full 24-plane encode (once; every budget is a prefix) ----
-  std::vector<MachineOut> mo(nfields);
-  std::vector<PlaneRec> pl((size_t)kMaxPlaneRecs * nfields);
-  {
-    EventTimer t(c, &c->stats.ms_encode);
-    if (!grouped) {
-      CK(cudaMemcpyAsync(w.A, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
-      forward_dwt(w.A, w.B, N, nfields, g, st);
-      CK(cudaGetLastError());
-      c->stats.kernel_launches += 2 * g.levels;
-    }
-    pc.mark("fwd_dwt");
-    encode_pyramids(c, nfields, false, kBasePlanes, active, mo, pl);
-  }
-  pc.mark("base_tail");
-  g_slow.mark("base_encode");
-  for (int f = 0; f < nfields; f++) cs[f].T_base = active[f] ? mo[f].total_bits : 0;
-  std::vector<int> base_nmax(nfields);
-  bool xe_base = false, xe_res = false;  // exponents outside the normal range (rare)
-  for (int f = 0; f < nfields; f++) {
-    base_nmax[f] = mo[f].n_max;
-    if (active[f] && mo[f].n_max != kExpNone) xe_base |= exps_extreme(mo[f].n_max);
-  }
-
-  std::vector<ProbeParam> prm(nfields);
-  std::vector<ProbeResult> res(nfields);
-  Meta mbase = meta_of(w, false);
-  StepGraph base_graph, pure_graph, trunc_graph, joint_graph;
-
-  // incremental probes: one state per stream, invalid at the batch start
+  // ---- controller setup + base encode (eager, no host round trip) ----
   static const bool inc_env = !(getenv("EBCC_INC") && getenv("EBCC_INC")[0] == '0');
   static const int klim_div = getenv("EBCC_INC_KDIV") ? std::max(1, atoi(getenv("EBCC_INC_KDIV"))) : 16;
+  // speculative truncation probes (the next bisection level's two points
+  // beside each midpoint) while a lane's chunks leave the GPU slack
+  // (EBCC_SPEC=1|2|3 forces the slot count)
+  static const int spec_env =
+      getenv("EBCC_SPEC") ? std::max(1, std::min(kTruncSlots, atoi(getenv("EBCC_SPEC")))) : 0;
   Inc inc_s[2];
   bool inc_ok = inc_env;
   for (int i = 0; i < 2; i++) {
@@ -1084,403 +862,187 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     I.klimit = (uint32_t)std::min<int64_t>(N / klim_div, 0xffffffffll);
     static const int dbg = getenv("EBCC_INC_LOG") ? atoi(getenv("EBCC_INC_LOG")) : 0;
     I.debug = dbg;
-    CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields * (i ? kTruncSlots : 1), st));
   }
-  CK(cudaMemsetAsync(w.icomputed, 0, sizeof(unsigned long long) * 2 * kMaxLevels, st));
   const Inc* inc_base = inc_ok ? &inc_s[0] : nullptr;
   const Inc* inc_res = inc_ok ? &inc_s[1] : nullptr;
-  int64_t tiles_probed = 0;  // level-0 tiles the probes cover (instrumentation)
-
-  // ---- base quantile search ----
-  // fill the pure-search requests (phase 1) or base-search requests (phase 0)
-  std::vector<size_t> base_entries(nfields, 0);
-  auto base_requests = [&](int phase) {
-    bool any = false;
-    for (int f = 0; f < nfields; f++) {
-      ChunkSearch& s = cs[f];
-      prm[f] = ProbeParam{};
-      if (s.constant) continue;
-      if (phase == 1 && s.pure_done) continue;
-      s.missed = false;
-      int64_t r = phase == 0 ? s.search_base() : s.search_pure(base_entries[f]);
-      if (!s.missed) {
-        if (phase == 0) {
-          s.base_budget = r;
-        } else {
-          s.pure_budget = r;
-          s.pure_done = true;
-        }
-      } else {
-        s.pending = s.miss_key;
-        int64_t len = s.stream_len(s.miss_key);
-        uint64_t B = (uint64_t)(len - kHeader) * 8;
-        if (B > s.T_base) B = s.T_base;
-        prm[f].B = B;
-        prm[f].planes = kBasePlanes;
-        prm[f].active = 1;
-        prm[f].early = phase == 1 && early_ok();  // the pure search only asks max_err <= eps_abs
-        any = true;
-      }
-    }
-    return any;
-  };
-  auto base_results = [&]() {
-    memcpy(res.data(), w.h_res, sizeof(ProbeResult) * nfields);
-    for (int f = 0; f < nfields; f++) {
-      if (!prm[f].active) continue;
-      ChunkSearch& s = cs[f];
-      const int64_t b = s.pending;  // the budget this probe answered
-      Entry e;
-      e.budget = b;
-      e.len = s.stream_len(b);
-      e.count = res[f].count;
-      uint64_t bitsv = res[f].maxerr;
-      memcpy(&e.maxerr, &bitsv, 8);
-      s.at[b] = (int)s.memo.size();
-      s.memo.push_back(e);
-      tiles_probed += inc_s[0].ig.tiles0;
-    }
-  };
-  // early: the pure-base search's feasibility probes (no quantile count)
-  auto enqueue_base = [&](bool eager, bool early) {
-    CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(w.res, 0, sizeof(ProbeResult) * nfields, st));
-    // roofline timing: the first base-search probe (every tile computed)
-    fused::g_level0_timer = eager && !early ? &c->l0 : nullptr;
-    probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32, w.fs,
-               w.res, st, inc_base, xe_base, early);
-    fused::g_level0_timer = nullptr;
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(ProbeResult) * nfields, cudaMemcpyDeviceToHost, st));
-  };
-  for (;;) {
-    auto h0 = SteadyClock::now();
-    const bool any = base_requests(0);
-    replay_ms += std::chrono::duration<double, std::milli>(SteadyClock::now() - h0).count();
-    if (!any) break;
-    auto tp0 = SteadyClock::now();
-    g_sp.prep += std::chrono::duration<double, std::micro>(tp0 - h0).count();
-    g_sp.n++;
-    EventTimer t(c, &c->stats.ms_probe);
-    memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
-    bool timed = false;
-    base_graph.run(st, [&](bool eager) {
-      timed = eager;
-      enqueue_base(eager, false);
-    });
-    c->stats.kernel_launches += g.levels;
-    c->stats.probe_launches++;
-    auto tp1 = SteadyClock::now();
-    g_sp.launch += std::chrono::duration<double, std::micro>(tp1 - tp0).count();
-    CK(cudaStreamSynchronize(st));
-    auto tp2 = SteadyClock::now();
-    g_sp.wait += std::chrono::duration<double, std::micro>(tp2 - tp1).count();
-    accumulate_level0(c, timed, nfields);
-    base_results();
-    g_sp.post += us_since(tp2);
-    g_slow.mark("base_step", (int)g_sp.n);
-  }
-  for (int f = 0; f < nfields; f++) base_entries[f] = cs[f].memo.size();
-  pc.mark("base_search");
-
-  // ---- residue = norm - base decode at the chosen budget (main stream),
-  // then the residual DWT + 32-plane encode on the high-priority side
-  // stream, overlapped with the first pure-base probes below (which only
-  // read the base memo and the base metadata) ----
-  for (int f = 0; f < nfields; f++) {
-    prm[f] = ProbeParam{};
-    if (cs[f].constant) continue;
-    int64_t len = cs[f].stream_len(cs[f].base_budget);
-    uint64_t B = (uint64_t)(len - kHeader) * 8;
-    if (B > cs[f].T_base) B = cs[f].T_base;
-    prm[f].B = B; prm[f].planes = kBasePlanes; prm[f].active = 1;
-  }
-  memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
-  CK(cudaMemcpyAsync(w.prm, w.h_prm, sizeof(ProbeParam) * nfields, cudaMemcpyHostToDevice, st));
-  // resid overwrites norm in place (nothing reads norm after this point)
-  base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
-  c->stats.kernel_launches += g.levels;
-  // EBCC_OVERLAP: 0 (default) = residual encode on the lane's stream, then
-  // the pure and truncation searches; 1 = on the high-priority side stream
-  // with the first pure-base probes running beside it (measured slower, 32.3
-  // vs 31.3 ms, since the pure search got cheap: the probes slow the
-  // latency-bound machine on the critical path); 2 = on the side stream,
-  // the lane waits (31.5 ms)
-  static const int ovmode = getenv("EBCC_OVERLAP") ? atoi(getenv("EBCC_OVERLAP")) : 0;
-  const bool overlap = ovmode == 1;
-  cudaStream_t rs = ovmode == 0 ? st : c->side;
-  CK(cudaEventRecord(c->ev_a, st));
-  CK(cudaStreamWaitEvent(rs, c->ev_a, 0));
-  CK(cudaEventRecord(c->ev_s0, rs));
-  CK(cudaMemcpyAsync(w.A2, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, rs));
-  forward_dwt(w.A2, w.B2, N, nfields, g, rs);
-  c->stats.kernel_launches += 2 * g.levels;
-  // off the critical path while overlapped: one CTA per field leaves
-  // more SMs to the pure-search probes running beside it
-  static const int rc = getenv("EBCC_RESID_CLUSTER") ? atoi(getenv("EBCC_RESID_CLUSTER")) : 2;
-  encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, active, rs,
-                overlap ? rc : machine_cluster_size(false, std::max(nfields, c->machine_fields)));
-  CK(cudaEventRecord(c->ev_s1, rs));
-  CK(cudaEventRecord(c->ev_b, rs));
-  if (!overlap) pc.mark("residual_encode(serial)");
-
-  // ---- pure-base search and truncation search (24 planes, then 32),
-  // interleaved: they are independent given the base search, so once the
-  // residual stream has landed every step probes both kinds of candidates
-  // as two concurrent graph branches (pure on `st`, truncation on `side`,
-  // with their own parameter/result slots and scratch pyramids) ----
-  std::vector<MachineOut> rmo(nfields);
-  std::vector<PlaneRec> rpl((size_t)kMaxPlaneRecs * nfields);
-  std::vector<uint64_t> T24(nfields, 0), T32(nfields, 0);
-  Meta mres = meta_of(w, true);
-  bool resid_ready = false;
-  auto collect_residual = [&]() {
-    g_trace.add(g_lane, "resid_ready", -1);
-    CK(cudaStreamWaitEvent(st, c->ev_b, 0));
-    encode_collect(c, nfields, true, active, rmo, rpl, st);
-    float ms = 0;
-    if (cudaEventElapsedTime(&ms, c->ev_s0, c->ev_s1) == cudaSuccess) c->stats.ms_encode += ms;
-    for (int f = 0; f < nfields; f++) {
-      if (!active[f] || rmo[f].n_max == kExpNone) continue;
-      const PlaneRec* p = &rpl[(size_t)f * kMaxPlaneRecs];
-      T32[f] = rmo[f].total_bits;
-      T24[f] = p[kBasePlanes].start;
-      xe_res |= exps_extreme(rmo[f].n_max);
-    }
-    resid_ready = true;
-    if (pc.on) {
-      float e = 0;
-      cudaEventElapsedTime(&e, c->ev_s0, c->ev_s1);
-      char b[96];
-      snprintf(b, sizeof b, " resid_ready_after_steps=%lld resid_encode_gpu=%.2fms",
-               (long long)c->stats.probe_launches, e);
-      pc.log += b;
-    }
-  };
-  auto total_bytes = [&](int f, int pi) -> int64_t {
-    uint64_t T = pi == 0 ? T24[f] : T32[f];
-    return (int64_t)((T + 7) / 8);
-  };
-  std::vector<int> pass(nfields, 0);
-  std::vector<int> trunc_calls(nfields, 0);
-  // speculative truncation probes (also probe the next bisection level's
-  // points; EBCC_SPEC=1|2|3 forces the slot count) need one incremental state
-  // per slot; no faster on 37 x 721x1440 (the probe phase is throughput-bound)
-  static const int spec_env =
-      getenv("EBCC_SPEC") ? std::max(1, std::min(kTruncSlots, atoi(getenv("EBCC_SPEC")))) : 0;
-  // default: speculate while a lane's chunks leave the GPU slack (measured on
-  // 721x1440 chunks: 1 chunk 8.4 -> 7.4 ms, 6 chunks 12.6 -> 11.9 ms; from
-  // 12 chunks on it costs more than it saves)
   const int spec_auto = N * (int64_t)nfields <= (8ll << 20) ? kTruncSlots : 1;
-  const int TS = inc_res ? (spec_env ? spec_env : spec_auto) : 1;  // truncation probe slots in use
-  const int ntp = TS * nfields;           // truncation probes per step (probe v: chunk v % nfields)
-  std::vector<ProbeParam> tprm(ntp);
-  std::vector<ProbeResult> tres(ntp);
-  std::vector<int64_t> tslot_t(ntp, -1);
-  std::vector<int> tslot_pi(ntp, 0);
-  ProbeParam* d_tprm = w.prm + w.cap;
-  ProbeResult* d_tres = w.res + w.cap;
-  ProbeParam* h_tprm = w.h_prm + w.cap;
-  ProbeResult* h_tres = w.h_res + w.cap;
-  auto trunc_requests = [&]() {
-    bool any = false;
-    for (int v = 0; v < ntp; v++) tprm[v] = ProbeParam{};
-    auto set_probe = [&](int v, int f, int pi, int64_t t) {
-      int P = pi == 0 ? kBasePlanes : kDeepPlanes;
-      uint64_t T = pi == 0 ? T24[f] : T32[f];
-      uint64_t Bfull = (uint64_t)t * 8;
-      tprm[v].B = Bfull < T ? Bfull : T;
-      tprm[v].planes = P;
-      tprm[v].midpoint = 1;
-      tprm[v].n_last = rmo[f].n_max == kExpNone
-                           ? 0
-                           : n_last_of(rmo[f], &rpl[(size_t)f * kMaxPlaneRecs], P, Bfull, T);
-      tprm[v].active = 1;
-      tprm[v].early = early_ok();  // err_at(t) <= eps_abs is all the search asks
-      tslot_t[v] = t;
-      tslot_pi[v] = pi;
+  const int TS = inc_res ? (spec_env ? spec_env : spec_auto) : 1;  // truncation probe slots
+  const int ntp = TS * nfields;
+  *w.h_ctl_prm = CtlParams{q, r0, tol, prune ? 1 : 0, early_ok() ? 1 : 0, TS, 0};
+  CK(cudaMemcpyAsync(w.ctl_prm, w.h_ctl_prm, sizeof(CtlParams), cudaMemcpyHostToDevice, st));
+  const CtlArgs a0 = ctl_args(w, nfields, TS);
+  ctl_setup(a0, st);
+  const int cluster = machine_cluster_size(false, std::max(nfields, c->machine_fields));
+  // on the high-priority stream: the list machine needs whole SMs, and with
+  // concurrent work (lanes) it must win them as they drain
+  CK(cudaEventRecord(c->ev_a, st));
+  CK(cudaStreamWaitEvent(c->side, c->ev_a, 0));
+  CK(cudaEventRecord(c->tev[0], c->side));
+  encode_launch(c, nfields, false, kBasePlanes, w.A, false, nullptr, c->side, cluster);
+  CK(cudaEventRecord(c->tev[1], c->side));
+  CK(cudaEventRecord(c->ev_b, c->side));
+  CK(cudaStreamWaitEvent(st, c->ev_b, 0));
+  c->stats.kernel_launches += 2;
+  g_slow.mark("base_encode_issued");
+
+  // ---- the search graph (built once per batch shape of this workspace) ----
+  const int early = early_ok() ? 1 : 0;
+  Workspace::SearchGraph* sg = nullptr;
+  for (Workspace::SearchGraph& x : w.graphs)
+    if (x.nf == nfields && x.slots == TS && x.prune == (int)prune && x.early == early &&
+        x.inc == (int)inc_ok && x.cluster == cluster)
+      sg = &x;
+  if (!sg) {
+    Meta mbase = meta_of(w, false), mres = meta_of(w, true);
+    cudaStream_t s0 = cap_stream(c, 0), s1 = cap_stream(c, 1), s2 = cap_stream(c, 2),
+                 s3 = cap_stream(c, 3), s4 = cap_stream(c, 4);
+    CK(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal));
+    cudaStreamCaptureStatus cst;
+    cudaGraph_t top = nullptr;
+    CK(cudaStreamGetCaptureInfo(s0, &cst, nullptr, &top, nullptr, nullptr));
+    // incremental-probe state is invalid at the batch start
+    for (int i = 0; i < 2; i++)
+      CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields * (i ? kTruncSlots : 1), s0));
+    CK(cudaMemsetAsync(w.icomputed, 0, sizeof(unsigned long long) * 2 * kMaxLevels, s0));
+    auto base_probe = [&](cudaStream_t ps, bool early_p) {
+      probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32,
+                 w.fs, w.res, ps, inc_base, false, early_p);
     };
-    for (int f = 0; f < nfields; f++) {
-      ChunkSearch& s = cs[f];
-      if (s.constant || s.trunc_planes || pass[f] > 1) continue;
-      for (;;) {
-        s.missed = false;
-        int64_t t = s.search_trunc(pass[f], total_bytes(f, pass[f]));
-        if (!s.missed) {
-          if (t >= 0) {
-            s.trunc_t = t;
-            s.trunc_planes = pass[f] == 0 ? kBasePlanes : kDeepPlanes;
-            trunc_calls[f] += s.n_trunc_calls;
-            break;
-          }
-          trunc_calls[f] += s.n_trunc_calls;
-          pass[f]++;
-          if (pass[f] > 1) break;
-        } else {
-          NeedTrunc nt{s.miss_planes, s.miss_key};
-          s.tpending = nt.t;
-          s.tpending_planes = nt.planes;
-          set_probe(f, f, nt.planes, nt.t);
-          // speculative slots: points the next step needs whichever way
-          // this probe answers (same planes variant)
-          for (int k = 0; k + 1 < TS && k < 2; k++) {
-            const int64_t t2 = s.spec[k];
-            if (t2 < 0 || t2 == nt.t || s.trunc[nt.planes].count(t2)) continue;
-            set_probe((k + 1) * nfields + f, f, nt.planes, t2);
-          }
-          any = true;
-          break;
-        }
-      }
-    }
-    return any;
-  };
-  auto enqueue_trunc = [&](cudaStream_t ts, double* a, double* b, bool eager) {
-    CK(cudaMemcpyAsync(d_tprm, h_tprm, sizeof(ProbeParam) * ntp, cudaMemcpyHostToDevice, ts));
-    CK(cudaMemsetAsync(d_tres, 0, sizeof(ProbeResult) * ntp, ts));
+    // base quantile search: start (T_base, first requests), the first probe
+    // (its level-0 kernel timed for the roofline), then the loop
+    CtlArgs ab = a0;
+    ctl_base(ab, true, 0, s0);
+    fused::g_level0_timer = &c->l0;
+    base_probe(s0, false);
     fused::g_level0_timer = nullptr;
-    probe_trunc(mres, d_tprm, inc_res ? w.Linc[1] : a, b, g, ntp, w.base_dec, w.x32, w.fs,
-                d_tres, ts, inc_res, xe_res, nfields);
-    fused::g_level0_timer = nullptr;
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(h_tres, d_tres, sizeof(ProbeResult) * ntp, cudaMemcpyDeviceToHost, ts));
-  };
-  auto trunc_results = [&]() {
-    memcpy(tres.data(), h_tres, sizeof(ProbeResult) * ntp);
-    for (int v = 0; v < ntp; v++) {
-      if (!tprm[v].active) continue;
-      ChunkSearch& s = cs[v % nfields];
-      double e;
-      uint64_t bitsv = tres[v].maxerr;
-      memcpy(&e, &bitsv, 8);
-      s.trunc[tslot_pi[v]][tslot_t[v]] = e;
-      tiles_probed += inc_s[1].ig.tiles0;
-    }
-  };
-  bool pure_phase_marked = false;
-  if (!overlap) collect_residual();  // the searches start once the residual stream is there
-  for (;;) {
-    if (!resid_ready && cudaEventQuery(c->ev_b) == cudaSuccess) collect_residual();
-    cudaGetLastError();  // a not-ready query is not an error
-    auto h0 = SteadyClock::now();
-    bool anyp = base_requests(1);
-    bool anyt = resid_ready && trunc_requests();
-    if (prune && (anyp || anyt)) {
-      // candidate pruning (pipeline.py:315-329 picks min((len, 0|1))): stop
-      // a search whose candidate can no longer win; the chosen candidate and
-      // so the container bytes are unchanged
-      anyp = anyt = false;
-      for (int f = 0; f < nfields; f++) {
-        ChunkSearch& s = cs[f];
-        if (s.constant) continue;
-        const int64_t base_len = s.stream_len(s.base_budget);
-        const bool p_open = prm[f].active != 0, t_open = tprm[f].active != 0;
-        int64_t two_ub = -1, pure_ub = -1;
-        if (s.trunc_planes) two_ub = base_len + kHeader + s.trunc_t;
-        else if (t_open && s.t_ub >= 0) two_ub = base_len + kHeader + s.t_ub;
-        if (s.pure_done && s.pure_budget >= 0) pure_ub = s.stream_len(s.pure_budget);
-        else if (p_open && s.p_ub >= 0) pure_ub = s.p_ub;
-        const int64_t two_lb = base_len + kHeader + (t_open ? s.t_lb : 0);
-        if (p_open && two_ub >= 0 && s.p_lb > two_ub) {
-          s.pure_done = true;  // the two-layer candidate is strictly shorter
-          s.pure_budget = -1;
-          s.pure_pruned = true;
-          prm[f] = ProbeParam{};
-        } else if (t_open && pure_ub >= 0 && two_lb >= pure_ub) {
-          s.trunc_pruned = true;  // pure-base is no longer (ties go to pure-base)
-          s.trunc_t = -1;
-          pass[f] = 2;
-          for (int k = 0; k < TS; k++) tprm[k * nfields + f] = ProbeParam{};
-        }
-        anyp |= prm[f].active != 0;
-        for (int k = 0; k < TS; k++) anyt |= tprm[k * nfields + f].active != 0;
-      }
-    }
-    replay_ms += std::chrono::duration<double, std::milli>(SteadyClock::now() - h0).count();
-    if (!anyp && !pure_phase_marked) {
-      pc.mark("pure_search");
-      pure_phase_marked = true;
-    }
-    if (!anyp && !anyt) {
-      if (!resid_ready) {
-        collect_residual();
-        pc.mark("residual_encode");
-        continue;
-      }
-      break;
-    }
-    EventTimer t(c, &c->stats.ms_probe);
-    bool timed = false;
-    if (anyp) memcpy(w.h_prm, prm.data(), sizeof(ProbeParam) * nfields);
-    if (anyt) memcpy(h_tprm, tprm.data(), sizeof(ProbeParam) * ntp);
-    if (anyp && anyt) {
-      joint_graph.run(st, [&](bool eager) {
-        timed = eager;
-        CK(cudaEventRecord(c->ev_f0, st));
-        CK(cudaStreamWaitEvent(c->side, c->ev_f0, 0));
-        enqueue_trunc(c->side, w.A2, w.B2, false);
-        enqueue_base(eager, true);
-        CK(cudaEventRecord(c->ev_f1, c->side));
-        CK(cudaStreamWaitEvent(st, c->ev_f1, 0));
+    cudaGraphConditionalHandle hb;
+    CK(cudaGraphConditionalHandleCreate(&hb, top, 1, cudaGraphCondAssignDefault));
+    add_conditional(s0, s1, hb, cudaGraphCondTypeWhile, [&](cudaGraph_t body, cudaStream_t bs) {
+      cudaGraphConditionalHandle hp;
+      CK(cudaGraphConditionalHandleCreate(&hp, body, 0, 0));
+      CtlArgs al = a0;
+      al.h_loop = hb;
+      al.h_pure = hp;
+      ctl_base(al, false, 3, bs);
+      add_conditional(bs, s3, hp, cudaGraphCondTypeIf,
+                      [&](cudaGraph_t, cudaStream_t is) { base_probe(is, false); });
+    });
+    // residue = norm - base decode at the chosen budget; residual DWT +
+    // 32-plane encode (the 24-plane variant is its prefix)
+    ctl_residue(a0, s0);
+    base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, s0);
+    CK(cudaMemcpyAsync(w.A2, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, s0));
+    forward_dwt(w.A2, w.B2, N, nfields, g, s0);
+    CK(cudaEventRecord(c->ev_s0, s0));
+    encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, nullptr, s0, cluster);
+    CK(cudaEventRecord(c->ev_s1, s0));
+    // pure-base search and truncation search (24 planes, then 32): each step
+    // probes both kinds of candidates as two concurrent IF branches
+    ctl_joint(a0, true, 0, s0);
+    cudaGraphConditionalHandle hj;
+    CK(cudaGraphConditionalHandleCreate(&hj, top, 1, cudaGraphCondAssignDefault));
+    add_conditional(s0, s1, hj, cudaGraphCondTypeWhile, [&](cudaGraph_t body, cudaStream_t bs) {
+      cudaGraphConditionalHandle hp, ht;
+      CK(cudaGraphConditionalHandleCreate(&hp, body, 0, 0));
+      CK(cudaGraphConditionalHandleCreate(&ht, body, 0, 0));
+      CtlArgs al = a0;
+      al.h_loop = hj;
+      al.h_pure = hp;
+      al.h_trunc = ht;
+      ctl_joint(al, false, 7, bs);
+      CK(cudaEventRecord(c->ev_f0, bs));
+      CK(cudaStreamWaitEvent(s2, c->ev_f0, 0));
+      add_conditional(s2, s4, ht, cudaGraphCondTypeIf, [&](cudaGraph_t, cudaStream_t is) {
+        probe_trunc(mres, w.prm + w.cap, inc_res ? w.Linc[1] : w.A2, w.B2, g, ntp, w.base_dec,
+                    w.x32, w.fs, w.res + w.cap, is, inc_res, false, nfields);
       });
-    } else if (anyp) {
-      pure_graph.run(st, [&](bool eager) {
-        timed = eager;
-        enqueue_base(eager, true);
-      });
-    } else {
-      trunc_graph.run(st, [&](bool eager) {
-        timed = eager;
-        enqueue_trunc(st, w.A, w.B, eager);
-      });
-    }
-    c->stats.kernel_launches += (anyp + anyt) * g.levels;
-    c->stats.probe_launches++;
-    CK(cudaStreamSynchronize(st));
-    (void)timed;  // level-0 roofline timing comes from the first base-search step
-    if (anyp) base_results();
-    if (anyt) trunc_results();
-    g_slow.mark(anyp && anyt ? "joint_step" : (anyp ? "pure_step" : "trunc_step"));
+      add_conditional(bs, s3, hp, cudaGraphCondTypeIf,
+                      [&](cudaGraph_t, cudaStream_t is) { base_probe(is, true); });
+      CK(cudaEventRecord(c->ev_f1, s2));
+      CK(cudaStreamWaitEvent(bs, c->ev_f1, 0));
+    });
+    ctl_finalize(a0, s0);
+    CK(cudaMemcpyAsync(w.h_ctl_out, w.ctl_out, sizeof(CtlOut) * nfields, cudaMemcpyDeviceToHost, s0));
+    CK(cudaMemcpyAsync(w.h_fs, w.fs, sizeof(FieldScal) * nfields, cudaMemcpyDeviceToHost, s0));
+    CK(cudaMemcpyAsync(w.h_mo, w.mo_base, sizeof(MachineOut) * nfields, cudaMemcpyDeviceToHost, s0));
+    CK(cudaMemcpyAsync(w.h_mo + w.cap, w.mo_res, sizeof(MachineOut) * nfields,
+                       cudaMemcpyDeviceToHost, s0));
+    CK(cudaMemcpyAsync(w.h_ctl_stats, w.ctl_stats, sizeof(CtlStats), cudaMemcpyDeviceToHost, s0));
+    cudaGraph_t gr = nullptr;
+    CK(cudaStreamEndCapture(s0, &gr));
+    Workspace::SearchGraph ng;
+    ng.nf = nfields; ng.slots = TS; ng.prune = prune; ng.early = early; ng.inc = inc_ok;
+    ng.cluster = cluster;
+    CK(cudaGraphInstantiate(&ng.exec, gr, 0));
+    cudaGraphDestroy(gr);
+    w.graphs.push_back(ng);
+    sg = &w.graphs.back();
+    g_slow.mark("graph_built");
   }
-  pc.mark("trunc_search");
+  CK(cudaGraphLaunch(sg->exec, st));
+  CK(cudaStreamSynchronize(st));
+  g_slow.mark("searches_done");
   g_trace.add(g_lane, "searches_done", -1);
-  g_pc = nullptr;
-  if (inc_ok) {
-    unsigned long long comp[2 * kMaxLevels];
-    CK(cudaMemcpy(comp, w.icomputed, sizeof comp, cudaMemcpyDeviceToHost));
-    c->stats.tiles_computed += (int64_t)(comp[0] + comp[kMaxLevels]);
-    c->stats.tiles_probed += tiles_probed;
+
+  // ---- instrumentation ----
+  {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, c->tev[0], c->tev[1]) == cudaSuccess) c->stats.ms_encode += ms;
+    if (cudaEventElapsedTime(&ms, c->ev_s0, c->ev_s1) == cudaSuccess) c->stats.ms_encode += ms;
+    if (cudaEventElapsedTime(&ms, c->l0.a, c->l0.b) == cudaSuccess) {
+      c->stats.ms_probe_kernel += ms;
+      c->stats.probe_kernel_count++;
+      c->stats.probe_kernel_fields += nfields;
+    }
+    cudaGetLastError();
+    const CtlStats cs = *w.h_ctl_stats;
+    c->stats.probe_launches += 1 + (int64_t)(cs.base_steps + cs.joint_steps);
+    c->stats.kernel_launches += 4 + (int64_t)(cs.base_steps + cs.joint_steps) +
+                                (int64_t)(1 + cs.base_probes + cs.pure_probes + cs.trunc_probes) *
+                                    (g.levels + 1) +
+                                2 * g.levels + 10 + g.levels;
   }
-  if (pc.on) {
-    char b[64];
-    snprintf(b, sizeof b, " (host replay %.2fms)", replay_ms);
-    pc.log += b;
-  }
-  // ---- candidate choice (pipeline.py:315-329) + payload parts ----
+
+  // ---- ingest errors, then candidate choice (pipeline.py:315-329) + parts ----
+  const FieldScal* fs = w.h_fs;
+  for (int f = 0; f < nfields; f++)
+    if (fs[f].first_bad >= 0) {
+      c->err_index = (int64_t)f * N + fs[f].first_bad;
+      throw IngestFail{};
+    }
   int status = EBCC_OK;
+  const MachineOut* bmo = w.h_mo;
+  const MachineOut* rmo = w.h_mo + w.cap;
+  int64_t probed = 0;
   for (int f = 0; f < nfields; f++) {
     ebcc_chunk_rec& r = recs[f];
-    ChunkSearch& s = cs[f];
+    const CtlOut& o = w.h_ctl_out[f];
     memset(&r, 0, sizeof(r));
     r.vmin = fs[f].vmin;
     r.vmax = fs[f].vmax;
-    r.n_base_probes = (int32_t)s.memo.size();
-    r.n_trunc_probes = trunc_calls[f];
-    if (s.constant) {
+    r.n_base_probes = o.n_base_probes;
+    r.n_trunc_probes = o.n_trunc_probes;
+    probed += o.n_base_probes + o.n_trunc_probes;
+    if (fs[f].constant) {
       r.mode = EBCC_MODE_CONSTANT;
       sizes.push_back(0);
       continue;
     }
-    int64_t pure_len = s.pure_budget >= 0 ? s.stream_len(s.pure_budget) : -1;
-    int64_t base_len = s.stream_len(s.base_budget);
-    int64_t two_len = s.trunc_t >= 0 ? base_len + kHeader + s.trunc_t : -1;
+    if (o.status & kCtlCapacity)
+      throw CudaFail{cudaErrorMemoryAllocation, "search state capacity (memo / list / loop guard)"};
+    const int64_t full = kHeader + (int64_t)((o.T_base + 7) / 8);
+    auto stream_len = [&](int64_t b) { return b < full ? b : full; };
+    const int64_t pure_len = o.pure_budget >= 0 ? stream_len(o.pure_budget) : -1;
+    const int64_t base_len = stream_len(o.base_budget);
+    const int64_t two_len = o.trunc_t >= 0 ? base_len + kHeader + o.trunc_t : -1;
     if (pure_len < 0 && two_len < 0) {
       r.status = EBCC_E_RESIDUAL;
       status = EBCC_E_RESIDUAL;
       sizes.push_back(0);
       continue;
     }
-    if (base_nmax[f] < -128 || base_nmax[f] > 127 ||
+    const int base_nmax = bmo[f].n_max;
+    if (base_nmax < -128 || base_nmax > 127 ||
         (rmo[f].n_max != kExpNone && (rmo[f].n_max < -128 || rmo[f].n_max > 127)))
       throw CudaFail{cudaErrorInvalidValue, "stream exponent out of int8 range"};
     int64_t off = out_base_off;
@@ -1488,7 +1050,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     PackPart bp{};
     bp.src = w.bits_base + (int64_t)f * w.words_base;
     bp.bit_limit = ~0ull;
-    put_header(bp.hdr, base_nmax[f], g.levels, g.rows, g.cols);
+    put_header(bp.hdr, base_nmax, g.levels, g.rows, g.cols);
     if (pure_len >= 0 && (two_len < 0 || pure_len <= two_len)) {
       r.mode = EBCC_MODE_PURE_BASE;
       r.base_len = pure_len;
@@ -1500,21 +1062,27 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     } else {
       r.mode = EBCC_MODE_TWO_LAYER;
       r.base_len = base_len;
-      r.resid_len = kHeader + s.trunc_t;
-      r.resid_planes = s.trunc_planes;
+      r.resid_len = kHeader + o.trunc_t;
+      r.resid_planes = o.trunc_planes;
       bp.dst_off = (uint64_t)off;
       bp.nbytes = (uint64_t)base_len;
       parts.push_back(bp);
       PackPart rp{};
       rp.src = w.bits_res + (int64_t)f * w.words_res;
       rp.dst_off = (uint64_t)(off + base_len);
-      rp.nbytes = (uint64_t)(kHeader + s.trunc_t);
-      rp.bit_limit = s.trunc_planes == kBasePlanes ? T24[f] : T32[f];
-      int rn = rmo[f].n_max == kExpNone ? kZeroSentinel : rmo[f].n_max;
+      rp.nbytes = (uint64_t)(kHeader + o.trunc_t);
+      rp.bit_limit = o.trunc_planes == kBasePlanes ? o.T24 : o.T32;
+      const int rn = rmo[f].n_max == kExpNone ? kZeroSentinel : rmo[f].n_max;
       put_header(rp.hdr, rn, g.levels, g.rows, g.cols);
       parts.push_back(rp);
       sizes.push_back(two_len);
     }
+  }
+  if (inc_ok) {
+    unsigned long long comp[2 * kMaxLevels];
+    CK(cudaMemcpy(comp, w.icomputed, sizeof comp, cudaMemcpyDeviceToHost));
+    c->stats.tiles_computed += (int64_t)(comp[0] + comp[kMaxLevels]);
+    c->stats.tiles_probed += probed * inc_s[0].ig.tiles0;
   }
   return status;
 }
@@ -1577,6 +1145,8 @@ int ebcc_create(int32_t device, ebcc_ctx** out) {
     cudaEventCreate(&c->ev_s1);
     cudaEventCreate(&c->tm_a);
     cudaEventCreate(&c->tm_b);
+    cudaEventCreate(&c->tev[0]);
+    cudaEventCreate(&c->tev[1]);
   }
   c->own_stream = true;
   *out = c;
@@ -1621,6 +1191,10 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->tm_a) cudaEventDestroy(c->tm_a);
   if (c->tm_b) cudaEventDestroy(c->tm_b);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  for (cudaEvent_t e : c->tev)
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : c->cap)
+    if (s) cudaStreamDestroy(s);
   delete c;
 }
 

@@ -373,7 +373,10 @@ __device__ __forceinline__ void stage_flush(Stage& s, uint64_t seg_start, uint64
 // the machine.  Encoder: significance from the entries' relative exponents;
 // decoder: significance read from the stream at the scan-assigned offset.
 template <bool DECODE>
-__global__ void __launch_bounds__(MT, 1) machine_kernel(MachineBufs mb, Geo g, TreeTables tt,
+#ifndef EBCC_MACH_MINB
+#define EBCC_MACH_MINB 1
+#endif
+__global__ void __launch_bounds__(MT, EBCC_MACH_MINB) machine_kernel(MachineBufs mb, Geo g, TreeTables tt,
                                                         int planes) {
   cg::cluster_group cl = cg::this_cluster();
   const int csize = (int)cl.num_blocks();

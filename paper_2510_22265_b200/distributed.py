@@ -273,6 +273,7 @@ def decompress(buf, group=None) -> np.ndarray | None:
                     local[idx] = decompress_batch(seg.view, loffs[idx], r, h, w, lv)
     except EbccError as exc:
         err = exc
+    local = None  # drop the views of the shared segments before unmapping
     _raise_first(_gather_errors(err, group))
     dist.barrier(group)
     seg.close()
