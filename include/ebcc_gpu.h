@@ -132,6 +132,8 @@ int ebcc_check_streams(const uint8_t *data, int64_t len, const uint8_t *records2
  * at full PCIe/C2C speed without a staging hop. */
 int ebcc_host_alloc(int64_t bytes, void **out);
 int ebcc_host_free(void *ptr);
+/* Release every freed block the cache holds. */
+void ebcc_host_cache_trim(void);
 
 /* Decompress `nfields` same-shape chunks.  recs[i].mode/vmin/vmax/base_len/
  * resid_len come from the container; chunk i's payload starts at

@@ -33,7 +33,8 @@ EXPORTS = ("ebcc_abi_version", "ebcc_create", "ebcc_destroy", "ebcc_set_stream",
            "ebcc_get_stats", "ebcc_dwt", "ebcc_spiht_encode", "ebcc_spiht_decode",
            "ebcc_selftest_div", "ebcc_fetch_container", "ebcc_host_alloc", "ebcc_host_free",
            "ebcc_error_stats", "ebcc_error_histogram", "ebcc_ssim", "ebcc_radial_spectrum",
-           "ebcc_dev_probe_bench", "ebcc_parse_records", "ebcc_check_streams")
+           "ebcc_dev_probe_bench", "ebcc_parse_records", "ebcc_check_streams",
+           "ebcc_host_cache_trim")
 
 
 class ChunkRec(ctypes.Structure):
@@ -104,6 +105,8 @@ def load(path: str = LIB_PATH):
                                          ctypes.POINTER(i64)]
         L.ebcc_host_alloc.argtypes = [i64, ctypes.POINTER(P)]
         L.ebcc_host_free.argtypes = [P]
+        L.ebcc_host_cache_trim.argtypes = []
+        L.ebcc_host_cache_trim.restype = None
         L.ebcc_error_stats.argtypes = [P, P, P, i64, i64, i32, P]
         L.ebcc_error_histogram.argtypes = [P, P, P, i64, i64, i32, P, i32, P]
         L.ebcc_ssim.argtypes = [P, P, P, i64, i32, i32, i32, P]
@@ -325,18 +328,31 @@ class Context:
         return int(bad.value)
 
 
-_contexts: dict = {}
-_ctx_lock = threading.Lock()
+_tls = threading.local()
 
 
 def context(device: int | None = None) -> Context:
-    """Per-(thread, device) shared context."""
+    """Per-(thread, device) shared context.  Held in thread-local storage:
+    when the thread exits, its contexts (and their device workspaces) are
+    destroyed, so thread pools do not accumulate workspaces."""
     if device is None:
         device = int(os.environ.get("EBCC_DEVICE", "0"))
-    key = (threading.get_ident(), device)
-    with _ctx_lock:
-        ctx = _contexts.get(key)
-        if ctx is None:
-            ctx = Context(device)
-            _contexts[key] = ctx
-        return ctx
+    ctxs = getattr(_tls, "contexts", None)
+    if ctxs is None:
+        ctxs = _tls.contexts = {}
+    ctx = ctxs.get(device)
+    if ctx is None:
+        ctx = ctxs[device] = Context(device)
+    return ctx
+
+
+def trim(device: int | None = None) -> None:
+    """Release this thread's context for ``device`` (all devices if None):
+    its device workspaces, graphs and staging buffers; the next call
+    allocates anew.  Also drops the library's cache of freed page-locked
+    result blocks."""
+    ctxs = getattr(_tls, "contexts", {}) or {}
+    for d in list(ctxs):
+        if device is None or d == device:
+            ctxs.pop(d).close()
+    load().ebcc_host_cache_trim()

@@ -325,10 +325,18 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields, int want = 0) {
   if (!same_geo) {
     for (size_t i = 0; i < c->ws_cache.size(); i++) {
       Workspace& cw = c->ws_cache[i];
-      if (cw.g.rows == g.rows && cw.g.cols == g.cols && cw.g.levels == g.levels &&
-          cw.cap >= nfields) {
-        std::swap(c->ws, cw);  // the current one is parked in its place
-        return;
+      if (cw.g.rows == g.rows && cw.g.cols == g.cols && cw.g.levels == g.levels) {
+        if (cw.cap >= nfields) {
+          // reuse it; the current one is parked as the most recently used
+          Workspace found = cw;
+          c->ws_cache.erase(c->ws_cache.begin() + i);
+          if (w.cap > 0) c->ws_cache.push_back(w);
+          w = found;
+          return;
+        }
+        cw.release();  // too small for this call: never keep two of a shape
+        c->ws_cache.erase(c->ws_cache.begin() + i);
+        break;
       }
     }
     if (w.cap > 0) {  // park the current workspace, evicting the oldest
@@ -2195,6 +2203,11 @@ int ebcc_host_alloc(int64_t bytes, void** out) {
   g_pin_size[p] = bytes;
   *out = p;
   return EBCC_OK;
+}
+
+void ebcc_host_cache_trim(void) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  pin_release_cached_locked();
 }
 
 int ebcc_host_free(void* p) {

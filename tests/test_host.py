@@ -212,3 +212,20 @@ def test_sharded_container_equals_single_process(tmp_path):
     dims, cs, recs, offs, _ = parse(got)
     sizes = recs["base_len"].astype(np.int64) + recs["resid_len"]
     np.testing.assert_array_equal(container_offsets(sizes) + 25, offs)
+
+
+def test_ingest_error_precedes_shape_errors():
+    """The reference scans for non-finite values before it validates the
+    shape or the chunk shape (core.py:94-105): a 5-D array or a bad
+    chunk_shape holding a NaN raises IngestError, not ArgumentError."""
+    from paper_2510_22265_b200.core import grid_from_array
+    from paper_2510_22265_b200.errors import ArgumentError, IngestError
+    a = np.ones((2, 1, 1, 3, 4), np.float32)
+    a[1, 0, 0, 2, 3] = np.nan
+    for check in (True, False):
+        with pytest.raises(IngestError):
+            grid_from_array(a, check_finite=check)
+        with pytest.raises(IngestError):
+            grid_from_array(a[1], chunk_shape=(1, 0, 1, 1), check_finite=check)
+    with pytest.raises(ArgumentError):
+        grid_from_array(np.ones((2, 1, 1, 3, 4), np.float32), check_finite=False)
