@@ -900,7 +900,65 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     if (x.nf == nfields && x.slots == TS && x.prune == (int)prune && x.early == early &&
         x.inc == (int)inc_ok && x.cluster == cluster)
       sg = &x;
-  if (!sg) {
+  // EBCC_GRAPHS=0: the same sequence issued eagerly, the loop conditions read
+  // back by the host after every controller step (profiling only: ncu does
+  // not descend into conditional graph nodes)
+  static const bool graphs = !(getenv("EBCC_GRAPHS") && getenv("EBCC_GRAPHS")[0] == '0');
+  if (!graphs) {
+    Meta mbase = meta_of(w, false), mres = meta_of(w, true);
+    for (int i = 0; i < 2; i++)
+      CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields * (i ? kTruncSlots : 1), st));
+    CK(cudaMemsetAsync(w.icomputed, 0, sizeof(unsigned long long) * 2 * kMaxLevels, st));
+    auto base_probe = [&](bool early_p) {
+      probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32,
+                 w.fs, w.res, st, inc_base, false, early_p);
+    };
+    auto stats_now = [&]() {
+      CK(cudaMemcpyAsync(w.h_ctl_stats, w.ctl_stats, sizeof(CtlStats), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      return *w.h_ctl_stats;
+    };
+    ctl_base(a0, true, 0, st);
+    fused::g_level0_timer = &c->l0;
+    base_probe(false);
+    fused::g_level0_timer = nullptr;
+    unsigned long long seen = stats_now().base_probes;
+    for (;;) {
+      ctl_base(a0, false, 0, st);
+      const CtlStats cs = stats_now();
+      if (cs.base_probes == seen) break;
+      seen = cs.base_probes;
+      base_probe(false);
+    }
+    ctl_residue(a0, st);
+    base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
+    CK(cudaMemcpyAsync(w.A2, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
+    forward_dwt(w.A2, w.B2, N, nfields, g, st);
+    CK(cudaEventRecord(c->ev_s0, st));
+    encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, nullptr, st, cluster);
+    CK(cudaEventRecord(c->ev_s1, st));
+    ctl_joint(a0, true, 0, st);
+    CtlStats prev = stats_now();
+    for (;;) {
+      ctl_joint(a0, false, 0, st);
+      const CtlStats cs = stats_now();
+      const bool anyp = cs.pure_probes != prev.pure_probes;
+      const bool anyt = cs.trunc_probes != prev.trunc_probes;
+      prev = cs;
+      if (!anyp && !anyt) break;
+      if (anyt)
+        probe_trunc(mres, w.prm + w.cap, inc_res ? w.Linc[1] : w.A2, w.B2, g, ntp, w.base_dec,
+                    w.x32, w.fs, w.res + w.cap, st, inc_res, false, nfields);
+      if (anyp) base_probe(true);
+    }
+    ctl_finalize(a0, st);
+    CK(cudaMemcpyAsync(w.h_ctl_out, w.ctl_out, sizeof(CtlOut) * nfields, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(w.h_fs, w.fs, sizeof(FieldScal) * nfields, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(w.h_mo, w.mo_base, sizeof(MachineOut) * nfields, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(w.h_mo + w.cap, w.mo_res, sizeof(MachineOut) * nfields,
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(w.h_ctl_stats, w.ctl_stats, sizeof(CtlStats), cudaMemcpyDeviceToHost, st));
+  } else if (!sg) {
     Meta mbase = meta_of(w, false), mres = meta_of(w, true);
     cudaStream_t s0 = cap_stream(c, 0), s1 = cap_stream(c, 1), s2 = cap_stream(c, 2),
                  s3 = cap_stream(c, 3), s4 = cap_stream(c, 4);
@@ -987,7 +1045,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     sg = &w.graphs.back();
     g_slow.mark("graph_built");
   }
-  CK(cudaGraphLaunch(sg->exec, st));
+  if (graphs) CK(cudaGraphLaunch(sg->exec, st));
   CK(cudaStreamSynchronize(st));
   g_slow.mark("searches_done");
   g_trace.add(g_lane, "searches_done", -1);
