@@ -299,7 +299,10 @@ __device__ int n_last_of(const MachineOut& mo, const PlaneRec* pl, int planes, u
   return mo.n_max - (planes + jmax);
 }
 
-__device__ void memo_add(CtlChunk& s, int64_t b, const ProbeResult& r) {
+// counted: a base-search probe (its count field holds violations; a probe
+// that stopped early reported more than vlim of them, so the count stored
+// here is below the threshold exactly when the full count would be)
+__device__ void memo_add(CtlChunk& s, int64_t b, const ProbeResult& r, bool counted) {
   if (memo_find(s, b) >= 0) return;
   if (s.nmemo >= kCtlMemo) {
     s.status |= kCtlCapacity;
@@ -308,7 +311,9 @@ __device__ void memo_add(CtlChunk& s, int64_t b, const ProbeResult& r) {
   double e;
   unsigned long long bits = r.maxerr;
   memcpy(&e, &bits, 8);
-  s.memo[s.nmemo++] = CtlEntry{b, r.count, e};
+  const unsigned long long v = r.count;
+  const unsigned long long hits = !counted ? 0ull : (v >= (unsigned long long)s.n ? 0ull : (unsigned long long)s.n - v);
+  s.memo[s.nmemo++] = CtlEntry{b, hits, e};
 }
 __device__ void tmemo_add(CtlChunk& s, int pi, int64_t t, const ProbeResult& r) {
   if (tmemo_find(s, pi, t) >= 0) return;
@@ -330,7 +335,20 @@ __device__ ProbeParam base_request(const CtlChunk& s, int64_t b, bool early) {
   p.planes = kBasePlanes;
   p.active = 1;
   p.early = early;
+  p.vlim = s.vlim;
   return p;
+}
+
+// smallest count c with c / n >= q (the reference's float64 compare), as the
+// number of violations a count probe may see: n - c (-1: none reaches q)
+__device__ int32_t violation_limit(int64_t n, double q) {
+  const double dn = (double)n;
+  int64_t c = (int64_t)floor(__dmul_rn(q, dn));
+  if (c < 0) c = 0;
+  if (c > n) c = n;
+  while (c > 0 && __ddiv_rn((double)(c - 1), dn) >= q) c--;
+  while (c <= n && __ddiv_rn((double)c, dn) < q) c++;
+  return (int32_t)(n - c);
 }
 
 __device__ ProbeParam trunc_request(const CtlChunk& s, const CtlArgs& a, int f, int pi, int64_t t,
@@ -370,6 +388,7 @@ __global__ void __launch_bounds__(1024) ctl_setup_kernel(CtlArgs a) {
     s.r0 = P.r0;
     s.tol = P.tol;
     s.eps_abs = fs.eps_abs;
+    s.vlim = violation_limit(a.n, P.q);
     s.T_base = s.T24 = s.T32 = 0;
     s.active = act;
     s.status = 0;
@@ -395,6 +414,7 @@ __global__ void __launch_bounds__(1024) ctl_setup_kernel(CtlArgs a) {
 }
 
 __global__ void __launch_bounds__(1024) ctl_base_kernel(CtlArgs a, int start, int set) {
+  const bool early = a.prm_in->early != 0;
   bool any = false;
   for (int f = threadIdx.x; f < a.nfields; f += blockDim.x) {
     CtlChunk& s = a.cs[f];
@@ -405,13 +425,13 @@ __global__ void __launch_bounds__(1024) ctl_base_kernel(CtlArgs a, int start, in
         if (a.mo_base[f].overflow) s.status |= kCtlCapacity;
       }
       if (s.pend) {  // the probe that answered s.pend_budget
-        memo_add(s, s.pend_budget, a.res[f]);
+        memo_add(s, s.pend_budget, a.res[f], true);
         s.pend = 0;
       }
       if (!s.done_b && !(s.status & kCtlCapacity) && adv_base(s) == kSuspend) {
         s.pend = 1;
         s.pend_budget = s.want_b;
-        p = base_request(s, s.want_b, false);
+        p = base_request(s, s.want_b, early);
         any = true;
       }
     }
@@ -461,7 +481,7 @@ __global__ void __launch_bounds__(1024) ctl_joint_kernel(CtlArgs a, int start, i
     ProbeParam tp[kCtlSlots] = {};
     if (s.active) {
       if (s.pend) {
-        memo_add(s, s.pend_budget, a.res[f]);
+        memo_add(s, s.pend_budget, a.res[f], false);
         s.pend = 0;
       }
       for (int k = 0; k < a.slots; k++)

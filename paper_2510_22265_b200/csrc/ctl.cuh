@@ -48,6 +48,7 @@ struct CtlChunk {
   uint64_t T_base, T24, T32;
   int32_t active;        // not constant, finite input
   int32_t status;
+  int32_t vlim, pad_v;   // violations a count probe may see and still reach q
   // --- base memo (shared by the base and the pure-base searches) ---
   int32_t nmemo, pend;   // pend: memo budget of the probe in flight (-1 none)
   int64_t pend_budget;

@@ -92,6 +92,11 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
     memcpy(dst, src, bytes);
     return;
   }
+  {  // a fresh destination (a new bytes object) faults in 2 MiB pages
+    const uintptr_t a = ((uintptr_t)dst + (2u << 20) - 1) & ~(uintptr_t)((2u << 20) - 1);
+    const uintptr_t b = ((uintptr_t)dst + bytes) & ~(uintptr_t)((2u << 20) - 1);
+    if (b > a) madvise((void*)a, b - a, MADV_HUGEPAGE);
+  }
   size_t step = (bytes + T - 1) / T;
   step = (step + 4095) & ~size_t(4095);
 #pragma omp parallel for num_threads(T) schedule(static)
@@ -274,6 +279,21 @@ struct ebcc_ctx {
   int64_t h_pay_cap = 0;
   float* d_out = nullptr;
   int64_t out_cap = 0;
+  // double buffers of the batch pipelines: compress stages batch i+1's
+  // pageable input while batch i computes; decompress alternates its device
+  // output and payload staging so batch i's device->host copy overlaps batch
+  // i+1's decoders (ev_buf[k]: the last copy out of / into buffer k is done)
+  uint8_t* h_stage2 = nullptr;
+  int64_t h_stage2_cap = 0;
+  uint8_t* h_pay2 = nullptr;
+  int64_t h_pay2_cap = 0;
+  float* d_out2 = nullptr;
+  int64_t out2_cap = 0;
+  cudaEvent_t ev_obuf[2] = {};
+  cudaEvent_t ev_pbuf[2] = {};
+  float* d_in2 = nullptr;         // compress: the next batch's input (device)
+  int64_t in2_cap = 0;
+  cudaEvent_t ev_in2 = nullptr, ev_in2_used = nullptr;
   uint8_t* d_cont = nullptr;      // container image (ebcc_fetch_container)
   int64_t cont_cap = 0;
   uint8_t* d_cmeta = nullptr;     // its records + parts
@@ -717,6 +737,29 @@ void h2d_small(ebcc_ctx* c, void* dst, const void* src, size_t n, cudaStream_t s
   memcpy(c->h_arena + at, src, n);
   CK(cudaMemcpyAsync(dst, c->h_arena + at, n, cudaMemcpyHostToDevice, st));
   c->arena_used = at + n;
+}
+
+// a page-locked block of at least `bytes` held in (p, cap)
+uint8_t* pinned_block(uint8_t*& p, int64_t& cap, int64_t bytes) {
+  if (bytes > cap) {
+    if (p) CK(cudaFreeHost(p));
+    p = nullptr;
+    cap = 0;
+    CK(cudaMallocHost(&p, (size_t)bytes));
+    cap = bytes;
+  }
+  return p;
+}
+template <class T>
+T* device_block(T*& p, int64_t& cap, int64_t count) {
+  if (count > cap) {
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+    p = dalloc<T>((size_t)count);
+    cap = count;
+  }
+  return p;
 }
 
 uint8_t* host_stage(ebcc_ctx* c, int64_t bytes) {
@@ -1236,6 +1279,14 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->h_arena) cudaFreeHost(c->h_arena);
   if (c->h_pay) cudaFreeHost(c->h_pay);
+  if (c->h_stage2) cudaFreeHost(c->h_stage2);
+  if (c->h_pay2) cudaFreeHost(c->h_pay2);
+  if (c->d_out2) cudaFree(c->d_out2);
+  if (c->d_in2) cudaFree(c->d_in2);
+  for (cudaEvent_t e : {c->ev_in2, c->ev_in2_used})
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ev_obuf[0], c->ev_obuf[1], c->ev_pbuf[0], c->ev_pbuf[1]})
+    if (e) cudaEventDestroy(e);
   if (c->d_cont) cudaFree(c->d_cont);
   if (c->d_cmeta) cudaFree(c->d_cmeta);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -1331,7 +1382,7 @@ int64_t per_field_bytes(const ebcc_ctx* c, const Geo& g) {
   };
   take(c->ws);
   for (const ebcc_ctx* l : c->lanes) take(l->ws);
-  return pf + 12 * g.n;
+  return pf + 20 * g.n;  // + payload, two output / input buffers
 }
 // chunks per device batch for `lanes` concurrent sub-batches of up to `want`
 // chunks each: 85% of (free HBM + what this tree's workspaces hold) minus a
@@ -1397,6 +1448,29 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
     sizes.clear();
     int status = EBCC_OK;
     g_slow.mark("compress_setup");
+    // host input, several batches: while batch i computes, a helper thread
+    // stages batch i+1 (pageable input: into the other page-locked block) and
+    // uploads it on the copy stream into a second device buffer; batch i+1
+    // then starts with a device-to-device copy instead of waiting for PCIe
+    const bool host_in = !(flags & EBCC_INPUT_ON_DEVICE);
+    struct Prefetch {
+      std::thread t;
+      int64_t f0 = -1;
+      cudaError_t err = cudaSuccess;
+      ~Prefetch() { if (t.joinable()) t.join(); }
+    } pf;
+    int stage_k = 0;
+    auto stage_buf = [&](int k, int64_t bytes) {
+      return k ? pinned_block(c->h_stage2, c->h_stage2_cap, bytes) : host_stage(c, bytes);
+    };
+    if (host_in && cap < nfields) {
+      if (!c->copy) {
+        CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming));
+      }
+      for (cudaEvent_t* e : {&c->ev_in2, &c->ev_in2_used})
+        if (!*e) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
     for (int64_t f0 = 0; f0 < nfields; f0 += cap) {
       int nb = (int)std::min<int64_t>(cap, nfields - f0);
       ensure_workspace(c, g, nb, (int)cap);
@@ -1404,12 +1478,23 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
       CK(cudaGetLastError());
       const float* src = fields + f0 * g.n;
       const size_t in_bytes = sizeof(float) * g.n * nb;
-      if (!(flags & EBCC_INPUT_ON_DEVICE) && is_pageable(src)) {
+      const bool prefetched = pf.f0 == f0;
+      if (prefetched) {
+        pf.t.join();
+        pf.f0 = -1;
+        if (pf.err != cudaSuccess) throw CudaFail{pf.err, "input prefetch"};
+        CK(cudaStreamWaitEvent(st, c->ev_in2, 0));
+        CK(cudaMemcpyAsync(c->ws.x32, c->d_in2, in_bytes, cudaMemcpyDeviceToDevice, st));
+        CK(cudaEventRecord(c->ev_in2_used, st));
+        g_trace.add(g_lane, "in_prefetched", (int)f0);
+      } else if (host_in && is_pageable(src)) {
         CK(cudaGetLastError());
-        uint8_t* stg = host_stage(c, (int64_t)in_bytes);
+        uint8_t* stg = stage_buf(stage_k, (int64_t)in_bytes);
         CK(cudaGetLastError());
         parallel_memcpy(stg, src, in_bytes);
         src = reinterpret_cast<const float*>(stg);
+        stage_k ^= 1;
+        g_trace.add(g_lane, "in_staged", (int)f0);
       }
       CK(cudaGetLastError());
       const bool chained = chain && f0 == 0 && !(flags & EBCC_INPUT_ON_DEVICE);
@@ -1417,7 +1502,7 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
       // transformed as soon as it lands (compress_batch)
       static const int in_groups_env =
           getenv("EBCC_IN_GROUPS") ? std::max(1, atoi(getenv("EBCC_IN_GROUPS"))) : 4;
-      const int in_groups = (flags & EBCC_INPUT_ON_DEVICE) ? 0 : std::min(in_groups_env, nb);
+      const int in_groups = (!host_in || prefetched) ? 0 : std::min(in_groups_env, nb);
       cudaStream_t cst = in_groups ? c->copy : st;
       if (in_groups && !c->copy) {
         CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
@@ -1442,7 +1527,7 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
                                cudaMemcpyHostToDevice, cst));
           CK(cudaEventRecord(c->ev_groups[k], cst));
         }
-      } else {
+      } else if (!prefetched) {
         CK(cudaMemcpyAsync(c->ws.x32, src, in_bytes,
                            (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
                                                           : cudaMemcpyHostToDevice,
@@ -1452,6 +1537,38 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
         CK(cudaEventRecord(chain->done[lane], cst));
         chain->issued.store(lane + 1);
         chain_release.done = true;
+      }
+      // next batch: stage + upload behind this batch's compute
+      const int64_t f1 = f0 + cap;
+      if (host_in && f1 < nfields) {
+        const int64_t nb1 = std::min<int64_t>(cap, nfields - f1);
+        const size_t nbytes = sizeof(float) * g.n * nb1;
+        const float* nsrc = fields + f1 * g.n;
+        uint8_t* nstg = nullptr;
+        if (is_pageable(nsrc)) {
+          nstg = stage_buf(stage_k, (int64_t)nbytes);
+          stage_k ^= 1;
+        }
+        float* dst = device_block(c->d_in2, c->in2_cap, g.n * cap);
+        // the upload may overwrite d_in2 once this batch's copy out of it ran
+        if (prefetched) CK(cudaStreamWaitEvent(c->copy, c->ev_in2_used, 0));
+        const int dev = c->device;
+        cudaStream_t cp = c->copy;
+        cudaEvent_t done_ev = c->ev_in2;
+        Prefetch* pp = &pf;
+        pf.err = cudaSuccess;
+        pf.t = std::thread([=] {
+          const float* s = nsrc;
+          if (nstg) {
+            parallel_memcpy(nstg, nsrc, nbytes);
+            s = reinterpret_cast<const float*>(nstg);
+          }
+          cudaError_t e = cudaSetDevice(dev);
+          if (e == cudaSuccess) e = cudaMemcpyAsync(dst, s, nbytes, cudaMemcpyHostToDevice, cp);
+          if (e == cudaSuccess) e = cudaEventRecord(done_ev, cp);
+          pp->err = e;
+        });
+        pf.f0 = f1;
       }
       std::vector<PackPart> bparts;
       int64_t done = 0;
@@ -1493,6 +1610,7 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
       }
       sizes.insert(sizes.end(), bsizes.begin(), bsizes.end());
       g_slow.mark("batch_pack");
+      g_trace.add(g_lane, "packed", (int)f0);
     }
     int64_t total = 0;
     for (int64_t f = 0; f < nfields; f++) total += sizes[f];
@@ -1757,10 +1875,28 @@ int ebcc_fetch_container(ebcc_ctx* c, const uint8_t* header42, const uint8_t* re
     if (flags & EBCC_OUTPUT_ON_DEVICE) {
       CK(cudaMemcpyAsync(out, c->d_cont, total, cudaMemcpyDeviceToDevice, st));
     } else if (is_pageable(out)) {
-      uint8_t* stg = host_stage(c, total);
-      CK(cudaMemcpyAsync(stg, c->d_cont, total, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      parallel_memcpy(out, stg, (size_t)total);
+      // pageable destination (a fresh bytes object): device->host copies of
+      // 64 MiB pieces into two page-locked blocks, each piece copied on by the
+      // thread team while the next one crosses PCIe
+      constexpr int64_t kPiece = 64ll << 20;
+      uint8_t* blk[2] = {host_stage(c, std::min(total, kPiece)),
+                         total > kPiece ? pinned_block(c->h_stage2, c->h_stage2_cap, kPiece)
+                                        : nullptr};
+      for (int k = 0; k < 2; k++)
+        if (!c->ev_pbuf[k]) CK(cudaEventCreateWithFlags(&c->ev_pbuf[k], cudaEventDisableTiming));
+      const int64_t pieces = (total + kPiece - 1) / kPiece;
+      auto issue = [&](int64_t i) {
+        const int64_t o = i * kPiece, len = std::min(kPiece, total - o);
+        CK(cudaMemcpyAsync(blk[i & 1], c->d_cont + o, len, cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(c->ev_pbuf[i & 1], st));
+      };
+      issue(0);
+      for (int64_t i = 0; i < pieces; i++) {
+        if (i + 1 < pieces) issue(i + 1);
+        CK(cudaEventSynchronize(c->ev_pbuf[i & 1]));
+        const int64_t o = i * kPiece, len = std::min(kPiece, total - o);
+        parallel_memcpy(out + o, blk[i & 1], (size_t)len);
+      }
     } else {
       CK(cudaMemcpyAsync(out, c->d_cont, total, cudaMemcpyDeviceToHost, st));
     }
@@ -1812,7 +1948,15 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
     }
     const int64_t cap = balance(nfields, c->dplan.cap);
     g_slow.mark("dec_meminfo");
-    for (int64_t f0 = 0; f0 < nfields; f0 += cap) {
+    for (int k = 0; k < 2; k++) {
+      if (!c->ev_obuf[k]) CK(cudaEventCreateWithFlags(&c->ev_obuf[k], cudaEventDisableTiming));
+      if (!c->ev_pbuf[k]) CK(cudaEventCreateWithFlags(&c->ev_pbuf[k], cudaEventDisableTiming));
+    }
+    // batch b uses output / payload staging buffers b & 1 (double buffers:
+    // no host wait between batches; the call synchronises once at the end)
+    int bk = 0;
+    bool used[2] = {false, false};
+    for (int64_t f0 = 0; f0 < nfields; f0 += cap, bk ^= 1) {
       int nb = (int)std::min<int64_t>(cap, nfields - f0);
       ensure_workspace(c, g, nb, (int)cap);
       g_slow.mark("dec_workspace");
@@ -1899,20 +2043,18 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           // a pageable source would make the copy synchronous through the
           // driver's small bounce buffers: stage it (thread team) into a
           // page-locked block of this context instead
-          if (span > c->h_pay_cap) {
-            if (c->h_pay) CK(cudaFreeHost(c->h_pay));
-            c->h_pay = nullptr;
-            c->h_pay_cap = 0;
-            CK(cudaMallocHost(&c->h_pay, (size_t)span));
-            c->h_pay_cap = span;
-          }
-          parallel_memcpy(c->h_pay, psrc, (size_t)span);
-          psrc = c->h_pay;
+          // the block's previous upload (two batches ago) must have landed
+          if (used[bk]) CK(cudaEventSynchronize(c->ev_pbuf[bk]));
+          uint8_t* hp = bk ? pinned_block(c->h_pay2, c->h_pay2_cap, span)
+                           : pinned_block(c->h_pay, c->h_pay_cap, span);
+          parallel_memcpy(hp, psrc, (size_t)span);
+          psrc = hp;
         }
         CK(cudaMemcpyAsync(c->d_stage, psrc, span,
                            (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
                                                           : cudaMemcpyHostToDevice,
                            st));
+        CK(cudaEventRecord(c->ev_pbuf[bk], st));
         if ((int)up.size() > c->unpack_cap) {
           if (c->d_unpack) cudaFree(c->d_unpack);
           c->unpack_cap = (int)up.size() * 2;
@@ -1927,13 +2069,13 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
       float* dst = out + f0 * g.n;
       float* out_dev = dst;
       if (!(flags & EBCC_OUTPUT_ON_DEVICE)) {
-        if (c->out_cap < g.n * nb) {
-          if (c->d_out) cudaFree(c->d_out);
-          c->d_out = dalloc<float>(g.n * nb);
-          c->out_cap = g.n * nb;
-        }
-        out_dev = c->d_out;
+        // (a second buffer only when there is a next batch to overlap)
+        out_dev = (bk && nfields > cap) ? device_block(c->d_out2, c->out2_cap, g.n * nb)
+                                        : device_block(c->d_out, c->out_cap, g.n * nb);
+        // its previous device->host copy (two batches ago) must be done
+        if (used[bk]) CK(cudaStreamWaitEvent(st, c->ev_obuf[bk], 0));
       }
+      used[bk] = true;
       // two decodes: the residual stream (midpoint) on the high-priority side
       // stream with its own decoder state, concurrently with the base stream
       // (lower bound) on `st`; joined before the residual field is added to
@@ -2049,8 +2191,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
       g_trace.add(0, "dec_idwt_issued", -1);
       if (any_res && !res_joined) CK(cudaStreamWaitEvent(st, c->ev_b, 0));
       if (G > 1) {
-        CK(cudaEventRecord(c->ev_copy, c->copy));
-        CK(cudaStreamWaitEvent(st, c->ev_copy, 0));
+        CK(cudaEventRecord(c->ev_obuf[bk], c->copy));
       } else if (to_host) {
         const size_t ob = sizeof(float) * g.n * nb;
         if (pageable) {
@@ -2061,9 +2202,15 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         } else {
           CK(cudaMemcpyAsync(dst, out_dev, ob, cudaMemcpyDeviceToHost, st));
         }
+        CK(cudaEventRecord(c->ev_obuf[bk], st));
       }
-      CK(cudaStreamSynchronize(st));
+      if (g_slow.on()) CK(cudaStreamSynchronize(st));
     }
+    if (c->copy) {  // the last batches' device->host copies
+      CK(cudaEventRecord(c->ev_copy, c->copy));
+      CK(cudaStreamWaitEvent(st, c->ev_copy, 0));
+    }
+    CK(cudaStreamSynchronize(st));
     g_trace.add(0, "dec_batches_done", -1);
     cudaEventRecord(t1, st);
     cudaEventSynchronize(t1);

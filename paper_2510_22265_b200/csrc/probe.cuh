@@ -26,14 +26,19 @@ struct ProbeParam {
   int32_t n_last;
   int32_t active;
   // the caller only needs max_err <= eps_abs (pure-base and truncation
-  // probes): no quantile count, and CTAs starting after another CTA has
-  // already seen an error above eps_abs skip their work
+  // probes): CTAs starting after another CTA has already seen an error above
+  // eps_abs skip their work.  Base-search (count) probes: the caller only
+  // needs count/n >= q and max_err <= eps_abs; once more than `vlim` points
+  // miss eps_rel and an error above eps_abs was seen, both answers are "no"
+  // and the probe may stop likewise.
   int32_t early;
-  int32_t pad;
+  int32_t vlim;        // count probes: n - (smallest count c with c/n >= q)
 };
 
 struct ProbeResult {
-  unsigned long long count;   // #points with |dec - norm| <= eps_rel (base probes)
+  // count probes: #points with !(|dec - norm| <= eps_rel), pushed by the
+  // warps as they find them (a probe that stopped early holds more than vlim)
+  unsigned long long count;
   unsigned long long maxerr;  // bits of max |f32(denorm(rec)) - orig| (non-negative double)
 };
 
