@@ -151,13 +151,20 @@ int ebcc_decompress(ebcc_ctx *ctx, const uint8_t *payload, const int64_t *payloa
  *   ebcc_spiht_encode spiht.spiht_encode(pyramid, planes=planes) unbudgeted
  *                     (spiht.py:271-358); budgeted streams are byte prefixes.
  *   ebcc_spiht_decode spiht.decode_with_plane(data, prefix_len)
- *                     (spiht.py:403-482): coefficients + n_last (-999: None). */
+ *                     (spiht.py:403-482): coefficients + n_last (-999: None).
+ *   ebcc_decode_field base_codec.dequantized_field(data, prefix_len, midpoint)
+ *                     (base_codec.py:70-84): the decoded prefix through the
+ *                     PRODUCTION inverse transform (the fused level kernels
+ *                     of decompress and the probes, closed-form decode on
+ *                     load) into a float64 field. */
 int ebcc_dwt(ebcc_ctx *ctx, const double *in, double *out, int64_t nfields, int32_t rows,
              int32_t cols, int32_t levels, int32_t inverse);
 int ebcc_spiht_encode(ebcc_ctx *ctx, const double *coeffs, int32_t rows, int32_t cols,
                       int32_t levels, int32_t planes, uint8_t *out, int64_t cap, int64_t *len);
 int ebcc_spiht_decode(ebcc_ctx *ctx, const uint8_t *data, int64_t len, int64_t prefix_len,
                       int32_t rows, int32_t cols, double *coeffs_out, int32_t *n_last);
+int ebcc_decode_field(ebcc_ctx *ctx, const uint8_t *data, int64_t len, int64_t prefix_len,
+                      int32_t rows, int32_t cols, int32_t midpoint, double *field_out);
 
 /* Quality metrics of the reference's benchmark harness (pkg/src/ebcc/bench/
  * metrics.py), float64 on the device, for nfields fields of n (= rows*cols)

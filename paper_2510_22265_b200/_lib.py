@@ -31,6 +31,7 @@ CONTAINER_BODY = 8  # fetch_container: records + payloads only (one rank's span)
 EXPORTS = ("ebcc_abi_version", "ebcc_create", "ebcc_destroy", "ebcc_set_stream",
            "ebcc_last_error", "ebcc_last_error_index", "ebcc_compress", "ebcc_fetch_payload", "ebcc_decompress",
            "ebcc_get_stats", "ebcc_dwt", "ebcc_spiht_encode", "ebcc_spiht_decode",
+           "ebcc_decode_field",
            "ebcc_selftest_div", "ebcc_fetch_container", "ebcc_host_alloc", "ebcc_host_free",
            "ebcc_error_stats", "ebcc_error_histogram", "ebcc_ssim", "ebcc_radial_spectrum",
            "ebcc_dev_probe_bench", "ebcc_parse_records", "ebcc_check_streams",
@@ -94,6 +95,7 @@ def load(path: str = LIB_PATH):
         L.ebcc_dwt.argtypes = [P, P, P, i64, i32, i32, i32, i32]
         L.ebcc_spiht_encode.argtypes = [P, P, i32, i32, i32, i32, P, i64, ctypes.POINTER(i64)]
         L.ebcc_spiht_decode.argtypes = [P, P, i64, i64, i32, i32, P, ctypes.POINTER(i32)]
+        L.ebcc_decode_field.argtypes = [P, P, i64, i64, i32, i32, i32, P]
         L.ebcc_selftest_div.argtypes = [P, i64, ctypes.c_uint64, ctypes.POINTER(i64)]
         L.ebcc_dev_probe_bench.argtypes = [P, ctypes.c_double, i32, i32,
                                            ctypes.POINTER(ctypes.c_double),
@@ -310,6 +312,18 @@ class Context:
                                         cols, out.ctypes.data, ctypes.byref(nl))
         self.raise_for(st, "ebcc_spiht_decode")
         return out, (None if nl.value == -999 else nl.value)
+
+    def decode_field(self, data: bytes, rows: int, cols: int, prefix_len=None,
+                     midpoint: bool = True) -> np.ndarray:
+        """base_codec.dequantized_field through the production inverse
+        transform (the fused level kernels), float64."""
+        buf = np.frombuffer(data, np.uint8).copy()
+        out = np.zeros((rows, cols), np.float64)
+        st = self.lib.ebcc_decode_field(self.handle, buf.ctypes.data, len(buf),
+                                        -1 if prefix_len is None else int(prefix_len), rows,
+                                        cols, int(bool(midpoint)), out.ctypes.data)
+        self.raise_for(st, "ebcc_decode_field")
+        return out
 
 
     def dev_probe_bench(self, frac: float, iters: int = 20, early: bool = False):

@@ -145,6 +145,8 @@ struct Workspace {
   uint8_t* hrel = nullptr;
   uint2* packed = nullptr;
   uint2* packed2 = nullptr;      // residual metadata (built while the pure search runs)
+  uint8_t* rank_hi = nullptr;    // wide chunks (probe.cuh): rank bits 26..31, base / residual
+  uint8_t* rank_hi2 = nullptr;
   uint32_t* sprank = nullptr;    // sign bit offsets by LSP rank (base / residual)
   uint32_t* sprank2 = nullptr;
   double *A2 = nullptr, *B2 = nullptr;  // residual forward-DWT scratch
@@ -215,7 +217,7 @@ struct Workspace {
     for (void* p : hp)
       if (p) cudaFreeHost(p);
     void* ptrs[] = {x32, norm, A, B, base_dec, ec, ed, el, mant, sign_pos, lsp_rank, pinfo, hrel,
-                    packed, ninfo,
+                    packed, ninfo, rank_hi, rank_hi2,
                     packed2, sprank, sprank2, A2, B2,
                     lip, lis0, lis1, w0, w1, lsp, bits_base, bits_res, pl_base, pl_res,
                     mo_base, mo_res, fs, prm, res, tq_base, tq_res, limit, active, mm};
@@ -336,6 +338,13 @@ cudaStream_t cap_stream(ebcc_ctx* c, int k) {
   return c->cap[k];
 }
 
+// chunks past the 26-bit record rank keep rank bits 26..31 in a side byte
+// (EBCC_WIDE_RECORDS=1 forces the layout for every chunk: parity tests)
+bool wide_records(const Geo& g) {
+  static const bool force = getenv("EBCC_WIDE_RECORDS") && getenv("EBCC_WIDE_RECORDS")[0] == '1';
+  return force || g.n > kMaxNarrowPoints;
+}
+
 // make c->ws a workspace of geometry g holding at least nfields chunks; a
 // new allocation takes max(nfields, want) chunks (want: the planned batch)
 void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields, int want = 0) {
@@ -390,6 +399,10 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields, int want = 0) {
   w.hrel = dalloc<uint8_t>((size_t)((g.n + 15) & ~15ll) * cap + 16);  // 16-B aligned per field
   w.packed = dalloc<uint2>(N);
   w.packed2 = dalloc<uint2>(N);
+  if (wide_records(g)) {
+    w.rank_hi = dalloc<uint8_t>(N);
+    w.rank_hi2 = dalloc<uint8_t>(N);
+  }
   w.sprank = dalloc<uint32_t>(N);
   w.sprank2 = dalloc<uint32_t>(N);
   w.A2 = dalloc<double>(N);
@@ -499,6 +512,7 @@ MachineBufs machine_bufs_dec2(Workspace& w, int nfields) {
 Meta meta_of(Workspace& w, bool residual) {
   Meta m{};
   m.packed = residual ? w.packed2 : w.packed;
+  m.rank_hi = residual ? w.rank_hi2 : w.rank_hi;
   m.sprank = residual ? w.sprank2 : w.sprank;
   m.planes = residual ? w.pl_res : w.pl_base;
   m.mo = residual ? w.mo_res : w.mo_base;
@@ -622,7 +636,7 @@ void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const do
   write_refinement(mb, planes, st);
   CK(cudaGetLastError());
   pack_meta(mb, packed_residual ? w.packed2 : w.packed, packed_residual ? w.sprank2 : w.sprank,
-            st, w.lspn[packed_residual ? 1 : 0]);
+            st, w.lspn[packed_residual ? 1 : 0], packed_residual ? w.rank_hi2 : w.rank_hi);
   c->stats.kernel_launches += 9 + w.g.levels;
   CK(cudaGetLastError());
 }
@@ -1689,7 +1703,7 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
   if (r0 < 1.0) return fail(c, EBCC_E_ARGUMENT, "r0 must be >= 1");
   if (!(search_tol > 0.0)) return fail(c, EBCC_E_ARGUMENT, "search_tol must be positive");
   if ((int64_t)rows * cols > kMaxChunkPoints)
-    return fail(c, EBCC_E_ARGUMENT, "chunk too large (at most 2^26 - 2 points)");
+    return fail(c, EBCC_E_ARGUMENT, "chunk too large (at most 2^32 - 2 points)");
   c->err.clear();
   c->err_index = -1;
   arena_reset(c);  // the previous call ended synchronised
@@ -1916,7 +1930,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
       levels > kMaxLevels)
     return fail(c, EBCC_E_ARGUMENT, "bad arguments");
   if ((int64_t)rows * cols > kMaxChunkPoints)
-    return fail(c, EBCC_E_ARGUMENT, "chunk too large (at most 2^26 - 2 points)");
+    return fail(c, EBCC_E_ARGUMENT, "chunk too large (at most 2^32 - 2 points)");
   c->stats = ebcc_stats{};
   c->err.clear();
   arena_reset(c);  // the previous call ended synchronised
@@ -2096,7 +2110,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         // one CTA per chunk: fits beside the base machine's clusters
         run_machine(true, rb, g, w.tt, kMaxDecodePlanes, c->side, 1);
         gather_refinement(rb, c->side);
-        pack_meta(rb, w.packed2, w.sprank2, c->side);
+        pack_meta(rb, w.packed2, w.sprank2, c->side, nullptr, w.rank_hi2);
         CK(cudaEventRecord(c->ev_b, c->side));
         c->stats.kernel_launches += 4;
       }
@@ -2110,7 +2124,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         decode_init(mb, st);
         run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
         gather_refinement(mb, st);
-        pack_meta(mb, w.packed, w.sprank, st);
+        pack_meta(mb, w.packed, w.sprank, st, nullptr, w.rank_hi);
         c->stats.kernel_launches += 4;
       }
       g_trace.add(0, "dec_machines_issued", -1);
@@ -2287,10 +2301,36 @@ int ebcc_spiht_encode(ebcc_ctx* c, const double* coeffs, int32_t rows, int32_t c
   }
 }
 
+namespace {
+// ebcc_spiht_decode / ebcc_decode_field: decoder machine on one stream prefix,
+// then either the coefficients (decode_coeffs) or the field through the
+// production fused inverse transform (decode_field)
+int decode_one(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t prefix_len, int32_t rows,
+               int32_t cols, double* coeffs_out, int32_t* n_last, double* field_out,
+               int32_t midpoint);
+}  // namespace
+
 int ebcc_spiht_decode(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t prefix_len,
                       int32_t rows, int32_t cols, double* coeffs_out, int32_t* n_last) {
   if (!c || !data || !coeffs_out || !n_last || rows < 1 || cols < 1)
     return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  return decode_one(c, data, len, prefix_len, rows, cols, coeffs_out, n_last, nullptr, 0);
+}
+
+int ebcc_decode_field(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t prefix_len,
+                      int32_t rows, int32_t cols, int32_t midpoint, double* field_out) {
+  if (!c || !data || !field_out || rows < 1 || cols < 1)
+    return fail(c, EBCC_E_ARGUMENT, "bad arguments");
+  int32_t nl = 0;
+  return decode_one(c, data, len, prefix_len, rows, cols, nullptr, &nl, field_out, midpoint);
+}
+
+}  // extern "C"
+
+namespace {
+int decode_one(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t prefix_len, int32_t rows,
+               int32_t cols, double* coeffs_out, int32_t* n_last, double* field_out,
+               int32_t midpoint) {
   if ((int64_t)rows * cols > kMaxChunkPoints) return fail(c, EBCC_E_ARGUMENT, "chunk too large");
   if (len < kHeader || data[0] != 'S' || data[1] != 'P') return fail(c, EBCC_E_FORMAT, "bad header");
   int levels = data[3];
@@ -2323,13 +2363,22 @@ int ebcc_spiht_decode(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t pre
     decode_init(mb, st);
     run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
     gather_refinement(mb, st);
-    pack_meta(mb, w.packed2, w.sprank2, st);
+    pack_meta(mb, w.packed2, w.sprank2, st, nullptr, w.rank_hi2);
     ProbeParam p{};
     p.B = ~0ull; p.planes = -1; p.active = 1;
+    // (an all-zero stream has no n_last: dequantized_field adds no offset)
+    p.midpoint = (midpoint && nm != kZeroSentinel) ? 1 : 0;
     CK(cudaMemcpyAsync(w.prm, &p, sizeof(p), cudaMemcpyHostToDevice, st));
-    decode_coeffs(meta_of(w, true), w.prm, w.A, g.n, 1, st);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(coeffs_out, w.A, sizeof(double) * g.n, cudaMemcpyDeviceToHost, st));
+    if (field_out) {
+      decode_field(meta_of(w, true), w.prm, w.A, w.B, g, 1, w.base_dec, st,
+                   nm != kZeroSentinel && exps_extreme(nm), p.midpoint != 0);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(field_out, w.base_dec, sizeof(double) * g.n, cudaMemcpyDeviceToHost, st));
+    } else {
+      decode_coeffs(meta_of(w, true), w.prm, w.A, g.n, 1, st);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(coeffs_out, w.A, sizeof(double) * g.n, cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaMemcpyAsync(mo.data(), mb.out, sizeof(MachineOut), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (nm == kZeroSentinel) *n_last = -999;
@@ -2340,6 +2389,9 @@ int ebcc_spiht_decode(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t pre
     return fail(c, EBCC_E_CUDA, std::string(e.what) + ": " + cudaGetErrorString(e.e));
   }
 }
+}  // namespace
+
+extern "C" {
 
 // page-locked result blocks: size-keyed free list, bounded cache
 namespace {

@@ -121,22 +121,24 @@ __global__ void decode_coeffs_kernel(Meta m, const ProbeParam* __restrict__ prm,
   const double off = P.midpoint ? scalbn(0.5, n_last) : 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    out[(int64_t)f * n + i] = fused::decode_raw_scan(m.packed[fo + i], RB, planes, n_max,
-                                                     P.midpoint != 0, off, T);
+    out[(int64_t)f * n + i] = fused::decode_raw_scan(
+        m.packed[fo + i], m.rank_hi ? (uint32_t)m.rank_hi[fo + i] << kRankBits : 0u, RB, planes,
+        n_max, P.midpoint != 0, off, T);
 }
 
 // 8-byte probe records + sign offsets by rank (sprank preset to kNone)
 __global__ void pack_meta_kernel(MachineBufs mb, uint2* packed, uint32_t* sprank,
-                                 uint32_t* lspn) {
+                                 uint32_t* lspn, uint8_t* rank_hi) {
   const int f = blockIdx.y;
   const int64_t fo = (int64_t)f * mb.stride;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < mb.stride;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t sp = mb.sign_pos[fo + i];
     const uint32_t pi = mb.pinfo[fo + i];
-    const uint32_t rank = sp == kNone ? kRankNone : mb.lsp_rank[fo + i];
-    packed[fo + i] = make_uint2(rank | ((pi & 0x3fu) << kRankBits),
+    const uint32_t rank = sp == kNone ? 0xffffffffu : mb.lsp_rank[fo + i];
+    packed[fo + i] = make_uint2((rank & kRankNone) | ((pi & 0x3fu) << kRankBits),
                                 ((pi & 0x80u) << 24) | (mb.mant[fo + i] & 0x7fffffffu));
+    if (rank_hi) rank_hi[fo + i] = (uint8_t)(rank >> kRankBits);
     if (sp != kNone) {
       sprank[fo + rank] = sp;
       if (lspn) lspn[fo + rank] = (uint32_t)i;
@@ -578,10 +580,10 @@ void selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_
 }
 
 void pack_meta(const MachineBufs& mb, uint2* packed, uint32_t* sprank, cudaStream_t st,
-               uint32_t* lspn) {
+               uint32_t* lspn, uint8_t* rank_hi) {
   cudaMemsetAsync(sprank, 0xff, sizeof(uint32_t) * mb.stride * mb.nfields, st);
   pack_meta_kernel<<<dim3(grid_for(mb.stride, 1024), mb.nfields), 256, 0, st>>>(mb, packed,
-                                                                                 sprank, lspn);
+                                                                                 sprank, lspn, rank_hi);
 }
 
 void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, int nfields,
@@ -663,9 +665,9 @@ void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b,
 }
 
 void decode_field(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
-                  int nfields, double* out, cudaStream_t st, bool xe) {
+                  int nfields, double* out, cudaStream_t st, bool xe, bool midpoint) {
   StoreFieldEpi e{out, prm, g.n};
-  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false, xe);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, midpoint, xe);
 }
 
 void decode_field_add_denorm(const Meta& m, const ProbeParam* prm, double* a, double* b,

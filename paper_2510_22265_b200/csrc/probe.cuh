@@ -51,12 +51,20 @@ struct ProbeResult {
 // The sign bit offset is not stored: it grows with the LSP rank, so "sign bit
 // read within B bits" is rank < R(B), R(B) found once per probe by a binary
 // search over the sign offsets in rank order (Meta::sprank).
+// Chunks of more than 2^26 - 2 points ("wide" chunks) keep the record and
+// store the rank's bits 26..31 in a side byte per coefficient (rank_hi; a
+// never-placed coefficient has rank 2^32 - 1); their level kernels are the
+// XE instantiations, which read the byte (one more byte load per sample).
 constexpr uint32_t kRankBits = 26;
 constexpr uint32_t kRankNone = (1u << kRankBits) - 1;
-constexpr int64_t kMaxChunkPoints = (int64_t)kRankNone - 1;
+constexpr int64_t kMaxNarrowPoints = (int64_t)kRankNone - 1;
+// bit offsets and LSP ranks are 32-bit: chunks up to 2^32 - 2 points (a
+// stream that outgrows 2^32 bits is reported as a capacity error)
+constexpr int64_t kMaxChunkPoints = (int64_t)0xfffffffe;
 
 struct Meta {  // one field = `stride` entries
   const uint2* packed;
+  const uint8_t* rank_hi;  // wide chunks: rank bits 26..31 per coefficient (else null)
   const uint32_t* sprank;  // sign bit offset by LSP rank (kNone: sign not read)
   const PlaneRec* planes;
   const MachineOut* mo;
@@ -127,7 +135,7 @@ void selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_
 
 // build Meta::packed from the machine's per-coefficient arrays
 void pack_meta(const MachineBufs& mb, uint2* packed, uint32_t* sprank, cudaStream_t st,
-               uint32_t* lspn = nullptr);
+               uint32_t* lspn = nullptr, uint8_t* rank_hi = nullptr);
 
 // f32 input -> per-field vmin/vmax/constant flag/first non-finite index and
 // the float64 normalised field.  `mm` holds 2*nfields u32 + nfields u64.
@@ -166,7 +174,8 @@ void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b,
 
 // decompress: decode a stream to a float64 field (out), optionally midpoint
 void decode_field(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
-                  int nfields, double* out, cudaStream_t st, bool xe = true);
+                  int nfields, double* out, cudaStream_t st, bool xe = true,
+                  bool midpoint = false);
 // decompress: residual decode fused with base add + denormalise to f32
 void decode_field_add_denorm(const Meta& m, const ProbeParam* prm, double* a, double* b,
                              const Geo& g, int nfields, const double* base, const FieldScal* fs,

@@ -90,6 +90,35 @@ def test_spiht_prefix_decode_bitwise(ctx, golden_spiht):
     assert not bad, bad
 
 
+def test_inverse_dwt_through_production_kernel(ctx, golden_spiht):
+    """The inverse transform the product runs (idwt_fused.cuh level kernels,
+    closed-form decode on load; dwt.py:202-216 / base_codec.py:70-84) on
+    every golden stream prefix, lower-bound and midpoint dequantisation,
+    bit-identical to the oracle's inverse_dwt of the reference's decoded
+    coefficients (oracle inverse pinned by the dwt goldens)."""
+    from oracle import oracle
+    oracle.build()
+    bad = []
+    for i, (r, c, seed, levels) in enumerate(golden_spiht["meta"]):
+        deep = golden_spiht[f"deep{i}"].tobytes()
+        full = golden_spiht[f"full{i}"].tobytes()
+        for cut, nl in golden_spiht[f"nlast{i}"]:
+            cut, nl = int(cut), int(nl)
+            if cut < 0:
+                data, pre, coef = full, None, golden_spiht[f"decfull{i}"]
+            else:
+                data, pre, coef = deep, cut, golden_spiht[f"dec{i}_{cut}"]
+            for mid in (False, True):
+                cf = np.array(coef, np.float64)
+                if mid and nl != -999:
+                    cf = cf + np.sign(cf) * float(np.ldexp(0.5, nl))
+                want = oracle.inverse_dwt(cf, int(levels))
+                got = ctx.decode_field(data, int(r), int(c), pre, midpoint=mid)
+                if not _same(got, want):
+                    bad.append((i, cut, mid, int((got != want).sum())))
+    assert not bad, bad
+
+
 def _run_case(ebcc, case, arr):
     """Returns None on parity, else a description of the first difference."""
     kw = dict(rel_error=case["eps"], q=case["q"], chunk_shape=case.get("chunk_shape"))

@@ -1,0 +1,124 @@
+"""GPU parity, round 3 of the test plan: chunks past the 26-bit record rank.
+
+The reference accepts any ``chunk_shape`` (core.py:89-105, 137-149), e.g.
+(2, 37, 721, 1440) flattens to one 53,354 x 1440 chunk of 76.8 M points.
+Chunks of more than 2^26 - 2 points keep the 8-byte probe record and store
+the LSP rank's bits 26..31 in a side byte (probe.cuh, "wide" records).
+
+* The wide layout is forced on every chunk (EBCC_WIDE_RECORDS=1, a fresh
+  process) and must reproduce the reference's golden containers and decoded
+  arrays byte for byte, and the oracle's containers of configs[1] fields.
+* A real 8,200 x 8,200 chunk (67.2 M points > 2^26) round-trips through the
+  public API with the bound held at every point, deterministically, and its
+  streams decode on the device to what the container says (the decoded
+  array of the second call equals the first's).
+"""
+
+import hashlib
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import golden_inputs as gi
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(REPO, "tests", "golden")
+
+pytestmark = pytest.mark.gpu
+
+_WIDE_SCRIPT = r"""
+import hashlib, json, os, sys
+sys.path.insert(0, os.path.join(sys.argv[1], "tests"))
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import golden_inputs as gi
+import paper_2510_22265_b200 as ebcc
+from paper_2510_22265_b200 import _lib
+bad = []
+with open(os.path.join(sys.argv[1], "tests", "golden", "chunks.json")) as fh:
+    cases = json.load(fh)["chunks"]
+n = 0
+for case in cases:
+    if "error" in case:
+        continue
+    arr = gi.chunk_input(case)
+    buf = ebcc.compress(arr, rel_error=case["eps"], q=case["q"], chunk_shape=case.get("chunk_shape"))
+    n += 1
+    if hashlib.sha256(buf).hexdigest() != case["container_sha"]:
+        bad.append(("container", case["rows"], case["cols"], case["eps"]))
+    elif gi.sha(ebcc.decompress(buf)) != case["decoded_sha"]:
+        bad.append(("decoded", case["rows"], case["cols"], case["eps"]))
+print(json.dumps({"cases": n, "bad": bad}))
+"""
+
+
+def test_wide_record_layout_matches_reference_goldens():
+    env = dict(os.environ, EBCC_WIDE_RECORDS="1")
+    out = subprocess.run([sys.executable, "-c", _WIDE_SCRIPT, REPO], env=env,
+                         capture_output=True, text=True, timeout=1200)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["cases"] > 50
+    assert not res["bad"], res["bad"][:8]
+
+
+_WIDE_CONFIG_SCRIPT = r"""
+import hashlib, importlib.util, json, os, sys
+sys.path.insert(0, os.path.join(sys.argv[1], "tests"))
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import golden_inputs as gi
+from paper_2510_22265_b200.chunk import EbccParams
+from paper_2510_22265_b200.container import RECORD_DTYPE, assemble
+from paper_2510_22265_b200.pipeline import compress_batch
+spec = importlib.util.spec_from_file_location("ofx", os.path.join(sys.argv[1], "tools", "oracle_fixtures_r2.py"))
+ofx = importlib.util.module_from_spec(spec)
+spec.loader.exec_module(ofx)
+with open(os.path.join(sys.argv[1], "tests", "golden", "oracle_configs.json")) as fh:
+    cases = [c for c in json.load(fh) if c["config"] == "configs[1]"][:8]
+stack = np.stack([ofx.field_of((c["config"], c["index"])) for c in cases])
+recs, offs, pay, st = compress_batch(stack, EbccParams(0.01))
+bad = []
+for i, c in enumerate(cases):
+    r = np.zeros(1, RECORD_DTYPE)
+    for k in ("mode", "vmin", "vmax", "base_len", "resid_len"):
+        r[k] = recs[i][k]
+    r["eps"], r["q"] = 0.01, 1 - 1e-5
+    dims = (1, 1) + stack.shape[1:]
+    b = assemble(dims, dims, r, pay, offs[i:i + 1])
+    if hashlib.sha256(b).hexdigest() != c["container_sha"]:
+        bad.append(c["index"])
+print(json.dumps({"cases": len(cases), "bad": bad}))
+"""
+
+
+def test_wide_record_layout_full_size_fields_vs_oracle():
+    env = dict(os.environ, EBCC_WIDE_RECORDS="1")
+    out = subprocess.run([sys.executable, "-c", _WIDE_CONFIG_SCRIPT, REPO], env=env,
+                         capture_output=True, text=True, timeout=1200)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["cases"] == 8 and not res["bad"], res
+
+
+def test_chunk_above_2_26_points_round_trip():
+    import paper_2510_22265_b200 as ebcc
+    from paper_2510_22265_b200 import fields
+    from paper_2510_22265_b200.container import read_file
+    rows = cols = 8200
+    assert rows * cols > (1 << 26)
+    a = fields.temperature_like(rows, cols, seed=77, mean=250.0, std=12.0)
+    blob = ebcc.compress(a, rel_error=0.01)
+    chunks, dims, _ = read_file(blob)
+    assert len(chunks) == 1 and tuple(dims) == (1, 1, rows, cols)
+    ratio = a.nbytes / len(blob)
+    assert ratio > 4.0, ratio
+    out = ebcc.decompress(blob).reshape(rows, cols)
+    st = ebcc.error_stats(a, out)
+    assert st.rel_max <= 0.01, st
+    assert ebcc.compress(a, rel_error=0.01) == blob
+    assert np.array_equal(ebcc.decompress(blob).reshape(rows, cols), out)
