@@ -52,6 +52,15 @@ void forward_dwt(double* a, double* b, int64_t field_stride, int nfields, const 
   for (int k = 0; k < g.levels; k++) forward_level(a, b, field_stride, nfields, g, k, st);
 }
 
+void forward_dwt_from(const double* src, double* a, double* b, int64_t field_stride, int nfields,
+                      const Geo& g, cudaStream_t st) {
+  // level 0: rows src -> b, columns b -> a (the whole array is the region)
+  const int r = g.lr[0], c = g.lc[0];
+  launch_pass<false>(src, b, field_stride, nfields, g.cols, r, c, false, st);
+  launch_pass<false>(b, a, field_stride, nfields, g.cols, r, c, true, st);
+  for (int k = 1; k < g.levels; k++) forward_level(a, b, field_stride, nfields, g, k, st);
+}
+
 void inverse_dwt(double* a, double* b, int64_t field_stride, int nfields, const Geo& g,
                  cudaStream_t st) {
   // dwt.py:211-215: coarse to fine, columns then rows; a -> b -> a

@@ -18,6 +18,10 @@ struct StoreEpi {
 // whole forward transform: a holds the input and receives the pyramid; b is scratch
 void forward_dwt(double* a, double* b, int64_t field_stride, int nfields, const Geo& g,
                  cudaStream_t st);
+// the same with the input read from `src` (level 0's row pass reads it; level 0
+// covers the whole array, so a needs no copy of the input first)
+void forward_dwt_from(const double* src, double* a, double* b, int64_t field_stride, int nfields,
+                      const Geo& g, cudaStream_t st);
 // whole inverse transform: a holds the pyramid and receives the field; b is scratch
 void inverse_dwt(double* a, double* b, int64_t field_stride, int nfields, const Geo& g,
                  cudaStream_t st);

@@ -881,8 +881,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   const bool grouped = in_groups > 0;
   if (!grouped) {
     ingest_normalize(w.x32, N, nfields, w.norm, w.fs, w.mm, eps_rel, st);
-    CK(cudaMemcpyAsync(w.A, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
-    forward_dwt(w.A, w.B, N, nfields, g, st);
+    forward_dwt_from(w.norm, w.A, w.B, N, nfields, g, st);
     c->stats.kernel_launches += 4 + 2 * g.levels;
   } else {
     // per group: normalise + forward DWT (the non-finite check is read after
@@ -894,9 +893,8 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       CK(cudaStreamWaitEvent(st, in_ev[k], 0));
       ingest_normalize(w.x32 + (int64_t)a * N, N, b - a, w.norm + (int64_t)a * N, w.fs + a,
                        w.mm + 4 * (int64_t)a, eps_rel, st);
-      CK(cudaMemcpyAsync(w.A + (int64_t)a * N, w.norm + (int64_t)a * N,
-                         sizeof(double) * N * (b - a), cudaMemcpyDeviceToDevice, st));
-      forward_dwt(w.A + (int64_t)a * N, w.B + (int64_t)a * N, N, b - a, g, st);
+      forward_dwt_from(w.norm + (int64_t)a * N, w.A + (int64_t)a * N, w.B + (int64_t)a * N, N,
+                       b - a, g, st);
       c->stats.kernel_launches += 4 + 2 * g.levels;
     }
   }
@@ -989,8 +987,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     }
     ctl_residue(a0, st);
     base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
-    CK(cudaMemcpyAsync(w.A2, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, st));
-    forward_dwt(w.A2, w.B2, N, nfields, g, st);
+    forward_dwt_from(w.norm, w.A2, w.B2, N, nfields, g, st);
     CK(cudaEventRecord(c->ev_s0, st));
     encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, nullptr, st, cluster);
     CK(cudaEventRecord(c->ev_s1, st));
@@ -1054,8 +1051,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     // 32-plane encode (the 24-plane variant is its prefix)
     ctl_residue(a0, s0);
     base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, s0);
-    CK(cudaMemcpyAsync(w.A2, w.norm, sizeof(double) * N * nfields, cudaMemcpyDeviceToDevice, s0));
-    forward_dwt(w.A2, w.B2, N, nfields, g, s0);
+    forward_dwt_from(w.norm, w.A2, w.B2, N, nfields, g, s0);
     CK(cudaEventRecord(c->ev_s0, s0));
     encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, nullptr, s0, cluster);
     CK(cudaEventRecord(c->ev_s1, s0));

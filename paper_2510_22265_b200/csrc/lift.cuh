@@ -7,9 +7,13 @@ namespace ebcc {
 namespace lift {
 
 
-constexpr int TI = 64;          // subband indices per tile
 constexpr int HALO = 2;
-constexpr int SPAN = TI + 2 * HALO;
+#ifndef EBCC_ROW_TI
+#define EBCC_ROW_TI 256
+#endif
+#ifndef EBCC_ROW_LINES
+#define EBCC_ROW_LINES 4
+#endif
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
@@ -17,7 +21,7 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 // and the neighbours of Y:  x[i] = x[i] (+|-) K*(y[a] + y[b]).
 // For an s-step (updating s from d):  a = max(i-1,0), b = min(i, nd-1).
 // For a d-step (updating d from s):   a = i,          b = min(i+1, ns-1).
-template <bool SUB, bool UPDATE_S, int LINES>
+template <bool SUB, bool UPDATE_S, int LINES, int SPAN>
 __device__ __forceinline__ void lift_step(double (*x)[SPAN + 1], double (*y)[SPAN + 1], int lo, int xcount,
                                           int ycount, int ns, int nd, double K) {
   const int ylo = lo, yhi = lo + ycount - 1;
@@ -42,12 +46,13 @@ __device__ __forceinline__ void lift_step(double (*x)[SPAN + 1], double (*y)[SPA
 
 // Generic pass.  Element (line L, position p) of the region lives at
 // base + L*line_stride + p*elem_stride.  n = line length along the transform.
-template <bool INVERSE, int LINES, class Epi>
+template <bool INVERSE, int LINES, int TI, class Epi>
 __global__ void __launch_bounds__(256) lift_pass_kernel(const double* __restrict__ in,
                                                         double* __restrict__ out,
                                                         int64_t field_stride, int line_stride,
                                                         int elem_stride, int nlines, int n,
                                                         Epi epi_in) {
+  constexpr int SPAN = TI + 2 * HALO;
   Epi epi = epi_in;  // per-thread copy: epilogues may accumulate
   __shared__ double s_sh[LINES][SPAN + 1];  // +1: odd row pitch, fewer bank conflicts
   __shared__ double d_sh[LINES][SPAN + 1];
@@ -102,21 +107,21 @@ __global__ void __launch_bounds__(256) lift_pass_kernel(const double* __restrict
   }
   __syncthreads();
   if (INVERSE) {
-    lift_step<true, true, LINES>(s_sh, d_sh, lo, scount, dcount, ns, nd, EBCC_DELTA);
+    lift_step<true, true, LINES, SPAN>(s_sh, d_sh, lo, scount, dcount, ns, nd, EBCC_DELTA);
     __syncthreads();
-    lift_step<true, false, LINES>(d_sh, s_sh, lo, dcount, scount, ns, nd, EBCC_GAMMA);
+    lift_step<true, false, LINES, SPAN>(d_sh, s_sh, lo, dcount, scount, ns, nd, EBCC_GAMMA);
     __syncthreads();
-    lift_step<true, true, LINES>(s_sh, d_sh, lo, scount, dcount, ns, nd, EBCC_BETA);
+    lift_step<true, true, LINES, SPAN>(s_sh, d_sh, lo, scount, dcount, ns, nd, EBCC_BETA);
     __syncthreads();
-    lift_step<true, false, LINES>(d_sh, s_sh, lo, dcount, scount, ns, nd, EBCC_ALPHA);
+    lift_step<true, false, LINES, SPAN>(d_sh, s_sh, lo, dcount, scount, ns, nd, EBCC_ALPHA);
   } else {
-    lift_step<false, false, LINES>(d_sh, s_sh, lo, dcount, scount, ns, nd, EBCC_ALPHA);
+    lift_step<false, false, LINES, SPAN>(d_sh, s_sh, lo, dcount, scount, ns, nd, EBCC_ALPHA);
     __syncthreads();
-    lift_step<false, true, LINES>(s_sh, d_sh, lo, scount, dcount, ns, nd, EBCC_BETA);
+    lift_step<false, true, LINES, SPAN>(s_sh, d_sh, lo, scount, dcount, ns, nd, EBCC_BETA);
     __syncthreads();
-    lift_step<false, false, LINES>(d_sh, s_sh, lo, dcount, scount, ns, nd, EBCC_GAMMA);
+    lift_step<false, false, LINES, SPAN>(d_sh, s_sh, lo, dcount, scount, ns, nd, EBCC_GAMMA);
     __syncthreads();
-    lift_step<false, true, LINES>(s_sh, d_sh, lo, scount, dcount, ns, nd, EBCC_DELTA);
+    lift_step<false, true, LINES, SPAN>(s_sh, d_sh, lo, scount, dcount, ns, nd, EBCC_DELTA);
   }
   __syncthreads();
   // store the tile's own indices [i0, i0+TI)
@@ -152,15 +157,16 @@ inline void launch_pass_epi(const double* in, double* out, int64_t field_stride,
                  int r, int c, bool along_cols, cudaStream_t st, const Epi& epi) {
   if (along_cols) {
     // lines = columns (contiguous across lines), transform length r
-    constexpr int LINES = 32;
+    constexpr int LINES = 32, TI = 64;
     dim3 grid((c + LINES - 1) / LINES, ((r + 1) / 2 + TI - 1) / TI, nfields);
-    lift_pass_kernel<INVERSE, LINES, Epi><<<grid, 256, 0, st>>>(in, out, field_stride, 1, cols, c,
-                                                                 r, epi);
+    lift_pass_kernel<INVERSE, LINES, TI, Epi><<<grid, 256, 0, st>>>(in, out, field_stride, 1,
+                                                                     cols, c, r, epi);
   } else {
-    constexpr int LINES = 8;
+    // rows: longer tiles (fewer halo samples and barriers per sample)
+    constexpr int LINES = EBCC_ROW_LINES, TI = EBCC_ROW_TI;
     dim3 grid((r + LINES - 1) / LINES, ((c + 1) / 2 + TI - 1) / TI, nfields);
-    lift_pass_kernel<INVERSE, LINES, Epi><<<grid, 256, 0, st>>>(in, out, field_stride, cols, 1, r,
-                                                                 c, epi);
+    lift_pass_kernel<INVERSE, LINES, TI, Epi><<<grid, 256, 0, st>>>(in, out, field_stride, cols,
+                                                                     1, r, c, epi);
   }
 }
 
