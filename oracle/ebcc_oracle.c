@@ -583,8 +583,18 @@ int eo_spiht_decode(const uint8_t *data, int64_t len, int64_t prefix_len, int ro
 }
 
 /* dequantized_field (base_codec.py:70-83) */
+/* opt-in JPEG2000-style base layer (ebcot_oracle.c): 0 SPIHT, 1 EBCOT */
+static int g_base_codec = 0;
+void eo_set_base_codec(int codec) { g_base_codec = codec; }
+
 static int dequantized_field(const uint8_t *data, int64_t len, int64_t prefix_len, int rows,
                              int cols, int midpoint, double *out) {
+  if (len >= 2 && data[0] == 'J' && data[1] == '2') { /* EBCOT base stream */
+    int st = eo_ebcot_decode(data, prefix_len < 0 ? len : prefix_len, rows, cols, out);
+    if (st) return st;
+    eo_inverse_dwt(out, rows, cols, data[3]);
+    return EO_OK;
+  }
   int n_last;
   int st = eo_spiht_decode(data, len, prefix_len, rows, cols, out, &n_last);
   if (st) return st;
@@ -638,7 +648,8 @@ int64_t eo_base_encode_budget(const double *norm, int rows, int cols, int64_t bu
   double *pyr = malloc(sizeof(double) * n);
   memcpy(pyr, norm, sizeof(double) * n);
   eo_forward_dwt(pyr, rows, cols, levels);
-  int64_t len = eo_spiht_encode(pyr, rows, cols, levels, budget, 24, out, cap);
+  int64_t len = g_base_codec == 1 ? eo_ebcot_encode(pyr, rows, cols, levels, budget, out, cap)
+                                   : eo_spiht_encode(pyr, rows, cols, levels, budget, 24, out, cap);
   free(pyr);
   if (len < 0) return len;
   int st = dequantized_field(out, len, -1, rows, cols, 0, decoded);

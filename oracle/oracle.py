@@ -30,8 +30,9 @@ class ChunkResult(ctypes.Structure):
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(HERE, "ebcc_oracle.c")
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
+    srcs = [os.path.join(HERE, f) for f in ("ebcc_oracle.c", "ebcot_oracle.c", "ebcc_oracle.h")]
+    if force or not os.path.exists(LIB_PATH) or \
+            os.path.getmtime(LIB_PATH) < max(os.path.getmtime(f) for f in srcs):
         subprocess.run(["make", "-s", "-C", HERE], check=True)
     return LIB_PATH
 
@@ -58,6 +59,14 @@ def lib():
         L.eo_decompress_chunk.argtypes = [i32, f64, f64, P, i64, i64, i32, i32, P]
         L.eo_base_encode_budget.argtypes = [P, i32, i32, i64, f64, P, i64, P, P]
         L.eo_base_encode_budget.restype = i64
+        L.eo_set_base_codec.argtypes = [i32]
+        L.eo_ebcot_blocks.argtypes = [i32, i32, i32, P, i32]
+        L.eo_ebcot_encode.argtypes = [P, i32, i32, i32, i64, P, i64]
+        L.eo_ebcot_encode.restype = i64
+        L.eo_ebcot_decode.argtypes = [P, i64, i32, i32, P]
+        L.eo_mq_encode.argtypes = [P, P, i64, P]
+        L.eo_mq_encode.restype = i64
+        L.eo_mq_decode.argtypes = [P, i64, P, i64, P]
         _lib = L
     return _lib
 
@@ -108,13 +117,62 @@ def decode_with_plane(data: bytes, rows, cols, prefix_len=None):
     return out.reshape(rows, cols), (None if nl.value == -999 else nl.value)
 
 
+# ---- opt-in JPEG2000-style base layer (parity unpinned: no reference) ----
+BASE_CODECS = {"spiht": 0, "ebcot": 1}
+
+
+def mq_encode(bits, cx) -> bytes:
+    b = np.ascontiguousarray(bits, np.uint8)
+    c = np.ascontiguousarray(cx, np.uint8)
+    out = np.zeros(2 * b.size + 16, np.uint8)
+    n = lib().eo_mq_encode(_p(b), _p(c), b.size, _p(out))
+    return out[:n].tobytes()
+
+
+def mq_decode(data: bytes, cx) -> np.ndarray:
+    c = np.ascontiguousarray(cx, np.uint8)
+    buf = np.frombuffer(data, np.uint8).copy() if data else np.zeros(1, np.uint8)
+    out = np.zeros(c.size, np.uint8)
+    lib().eo_mq_decode(_p(buf), len(data), _p(c), c.size, _p(out))
+    return out
+
+
+def ebcot_blocks(rows, cols, levels) -> np.ndarray:
+    n = lib().eo_ebcot_blocks(rows, cols, levels, None, 0)
+    out = np.zeros((max(n, 1), 5), np.int32)
+    lib().eo_ebcot_blocks(rows, cols, levels, _p(out), n)
+    return out[:n]
+
+
+def ebcot_encode(coeffs, levels, max_bytes=None) -> bytes:
+    c = np.ascontiguousarray(coeffs, dtype=np.float64)
+    cap = 12 + 8 * c.size + 4096
+    out = np.zeros(cap, np.uint8)
+    n = lib().eo_ebcot_encode(_p(c), c.shape[0], c.shape[1], levels,
+                              -1 if max_bytes is None else int(max_bytes), _p(out), cap)
+    if n < 0:
+        raise RuntimeError(f"oracle ebcot encode failed ({-n})")
+    return out[:n].tobytes()
+
+
+def ebcot_decode(data: bytes, rows, cols) -> np.ndarray:
+    buf = np.frombuffer(data, np.uint8).copy()
+    out = np.zeros(rows * cols, np.float64)
+    st = lib().eo_ebcot_decode(_p(buf), len(buf), rows, cols, _p(out))
+    if st:
+        raise RuntimeError(f"oracle ebcot decode failed ({st})")
+    return out.reshape(rows, cols)
+
+
 def budget_for_ratio(rows, cols, ratio):
     return lib().eo_budget_for_ratio(rows, cols, float(ratio))
 
 
-def compress_chunk(values, eps_rel, q=1 - 1e-5, r0=10.0, tol=1e-3, trace=False):
+def compress_chunk(values, eps_rel, q=1 - 1e-5, r0=10.0, tol=1e-3, trace=False,
+                   base_codec="spiht"):
     """Compress one 2D float32 chunk; returns a dict (payload bytes, record
     fields, probe traces when ``trace``)."""
+    lib().eo_set_base_codec(BASE_CODECS[base_codec])
     v = np.ascontiguousarray(values, dtype=np.float32)
     rows, cols = v.shape
     cap = 16 * v.size + 1024
@@ -128,6 +186,7 @@ def compress_chunk(values, eps_rel, q=1 - 1e-5, r0=10.0, tol=1e-3, trace=False):
                                  float(tol), ctypes.byref(res), _p(pay), cap,
                                  _p(tb) if trace else None, _p(tq) if trace else None, tcap,
                                  _p(tt) if trace else None, tcap)
+    lib().eo_set_base_codec(0)
     out = {"status": st, "mode": res.mode, "vmin": res.vmin, "vmax": res.vmax,
            "base_len": res.base_len, "resid_len": res.resid_len,
            "n_base_probes": res.n_base_probes, "n_trunc_probes": res.n_trunc_probes,
@@ -153,8 +212,11 @@ def decompress_chunk(mode, vmin, vmax, payload: bytes, base_len, resid_len, rows
 STATUS_NAMES = {1: "ArgumentError", 2: "FormatError", 3: "ResidualInsufficient"}
 
 
-def compress(array, rel_error=0.01, q=1 - 1e-5, chunk_shape=None) -> bytes:
-    """Oracle equivalent of the reference api.compress (container bytes)."""
+def compress(array, rel_error=0.01, q=1 - 1e-5, chunk_shape=None,
+             base_codec="spiht") -> bytes:
+    """Oracle equivalent of the reference api.compress (container bytes);
+    ``base_codec="ebcot"``: the opt-in JPEG2000-style base layer (container
+    version 2)."""
     from paper_2510_22265_b200 import core
     from paper_2510_22265_b200.chunk import CompressedChunk, Mode
     from paper_2510_22265_b200.container import write_bytes
@@ -163,7 +225,7 @@ def compress(array, rel_error=0.01, q=1 - 1e-5, chunk_shape=None) -> bytes:
     chunks = []
     for origin, block in core.iter_blocks(grid):
         ch = core.flatten_chunk(block, origin)
-        r = compress_chunk(ch.values, rel_error, q)
+        r = compress_chunk(ch.values, rel_error, q, base_codec=base_codec)
         if r["status"]:
             cls = getattr(errors, STATUS_NAMES.get(r["status"], "EbccError"))
             raise cls(f"chunk at origin {origin}: oracle status {r['status']}")
@@ -172,7 +234,8 @@ def compress(array, rel_error=0.01, q=1 - 1e-5, chunk_shape=None) -> bytes:
                                       residual_len=r["resid_len"], payload=r["payload"],
                                       rows=ch.rows, cols=ch.cols, block_shape=ch.block_shape,
                                       origin=origin))
-    return write_bytes(chunks, grid.dims, grid.chunk_shape)
+    return write_bytes(chunks, grid.dims, grid.chunk_shape,
+                       version=2 if base_codec == "ebcot" else 1)
 
 
 def decompress(buf: bytes) -> np.ndarray:

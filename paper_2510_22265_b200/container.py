@@ -28,6 +28,10 @@ from .errors import FormatError, IoError, UnsupportedVersion
 
 MAGIC = b"EBCC"
 VERSION = 1
+# version 2: the same layout with JPEG2000-style ('J2') base streams (the
+# opt-in base_codec="ebcot"; the reference reads only version 1)
+VERSION_EBCOT = 2
+VERSIONS = (VERSION, VERSION_EBCOT)
 
 HEADER = struct.Struct("<4sH4I4II")
 RECORD = struct.Struct("<BffffII")
@@ -36,8 +40,8 @@ RECORD_DTYPE = np.dtype([("mode", "u1"), ("eps", "<f4"), ("q", "<f4"), ("vmin", 
 assert RECORD_DTYPE.itemsize == RECORD.size == 25
 
 
-def pack_header(dims, chunk_shape, count: int) -> bytes:
-    return HEADER.pack(MAGIC, VERSION, *dims, *chunk_shape, count)
+def pack_header(dims, chunk_shape, count: int, version: int = VERSION) -> bytes:
+    return HEADER.pack(MAGIC, version, *dims, *chunk_shape, count)
 
 
 def pack_record(mode, eps, q, vmin, vmax, base_len, resid_len) -> bytes:
@@ -45,7 +49,7 @@ def pack_record(mode, eps, q, vmin, vmax, base_len, resid_len) -> bytes:
 
 
 def assemble(dims, chunk_shape, records: np.ndarray, payload: np.ndarray,
-             offsets: np.ndarray) -> bytes:
+             offsets: np.ndarray, version: int = VERSION) -> bytes:
     """Container bytes from a record array and one contiguous payload buffer.
 
     ``records`` has RECORD_DTYPE; chunk i's payload is
@@ -57,7 +61,7 @@ def assemble(dims, chunk_shape, records: np.ndarray, payload: np.ndarray,
     if len(records) != expected:
         raise FormatError(f"grid {dims} with chunk shape {chunk_shape} needs {expected} "
                           f"chunks, got {len(records)}")
-    parts = [pack_header(dims, chunk_shape, len(records))]
+    parts = [pack_header(dims, chunk_shape, len(records), version)]
     rec_bytes = records.astype(RECORD_DTYPE, copy=False).tobytes()
     lens = records["base_len"].astype(np.int64) + records["resid_len"].astype(np.int64)
     for i in range(len(records)):
@@ -67,7 +71,7 @@ def assemble(dims, chunk_shape, records: np.ndarray, payload: np.ndarray,
     return b"".join(parts)
 
 
-def write_file(chunks, dims, chunk_shape, sink) -> int:
+def write_file(chunks, dims, chunk_shape, sink, version: int = VERSION) -> int:
     dims = pad_dims(dims)
     chunk_shape = pad_dims(chunk_shape)
     expected = block_count(dims, chunk_shape)
@@ -75,7 +79,7 @@ def write_file(chunks, dims, chunk_shape, sink) -> int:
         raise FormatError(f"grid {dims} with chunk shape {chunk_shape} needs {expected} "
                           f"chunks, got {len(chunks)}")
     out = io.BytesIO()
-    out.write(pack_header(dims, chunk_shape, len(chunks)))
+    out.write(pack_header(dims, chunk_shape, len(chunks), version))
     for cc in chunks:
         out.write(pack_record(cc.mode, cc.epsilon_rel, cc.q, cc.vmin, cc.vmax, cc.base_len,
                               cc.residual_len))
@@ -92,9 +96,9 @@ def write_file(chunks, dims, chunk_shape, sink) -> int:
     return len(blob)
 
 
-def write_bytes(chunks, dims, chunk_shape) -> bytes:
+def write_bytes(chunks, dims, chunk_shape, version: int = VERSION) -> bytes:
     sink = io.BytesIO()
-    write_file(chunks, dims, chunk_shape, sink)
+    write_file(chunks, dims, chunk_shape, sink, version)
     return sink.getvalue()
 
 
@@ -126,7 +130,7 @@ def parse(source):
     head = HEADER.unpack_from(data, 0)
     if head[0] != MAGIC:
         raise FormatError(f"bad magic {head[0]!r}", offset=0)
-    if head[1] != VERSION:
+    if head[1] not in VERSIONS:
         raise UnsupportedVersion(f"unsupported format version {head[1]}", offset=4)
     dims = tuple(head[2:6])
     chunk_shape = tuple(head[6:10])
