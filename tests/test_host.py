@@ -96,7 +96,9 @@ def test_container_errors_and_io(tmp_path):
     with pytest.raises(FormatError):
         read_file(b"XBCC" + blob[4:])
     with pytest.raises(UnsupportedVersion):
-        read_file(blob[:4] + b"\x02\x00" + blob[6:])
+        read_file(blob[:4] + b"\x03\x00" + blob[6:])
+    # version 2 = this repository's opt-in JPEG2000-style base layer
+    assert read_file(blob[:4] + b"\x02\x00" + blob[6:])[1] == (0, 0, 0, 0)
     with pytest.raises(IoError):
         read_file("/nonexistent/x.ebcc")
     p = tmp_path / "e.ebcc"
