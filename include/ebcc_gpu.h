@@ -49,6 +49,13 @@ extern "C" {
                                     only (no 42-byte file header; header42 may
                                     be NULL) - one rank's span of a container
                                     assembled by several processes           */
+#define EBCC_BASE_EBCOT 16       /* compress: the opt-in JPEG2000-style base
+                                    layer ('J2' streams: deadzone quantisation,
+                                    EBCOT tier-1 + MQ coder; container
+                                    version 2).  The reference has no such
+                                    layer: parity unpinned.
+                                    decompress recognises 'J2' streams by
+                                    their magic.                              */
 
 /* Chunk modes (pipeline.py:38-41). */
 #define EBCC_MODE_CONSTANT 0

@@ -26,6 +26,8 @@ INPUT_ON_DEVICE = 1
 OUTPUT_ON_DEVICE = 2
 FULL_SEARCH = 4  # compress: every probe of the reference's searches (no candidate pruning)
 CONTAINER_BODY = 8  # fetch_container: records + payloads only (one rank's span)
+BASE_EBCOT = 16  # compress: the opt-in JPEG2000-style base layer ('J2'; parity unpinned)
+BASE_CODECS = {"spiht": 0, "ebcot": BASE_EBCOT}
 
 # the exported symbols include/ebcc_gpu.h declares (checked by the CPU tests)
 EXPORTS = ("ebcc_abi_version", "ebcc_create", "ebcc_destroy", "ebcc_set_stream",

@@ -11,6 +11,7 @@
 #include <cstdio>
 
 #include "ctl.cuh"
+#include "ebcot.cuh"
 
 namespace ebcc {
 namespace {
@@ -44,7 +45,24 @@ __device__ __forceinline__ int64_t ratio_budget(const CtlChunk& s, double ratio)
   int64_t b = (int64_t)py_floordiv((double)s.raw, ratio);
   return clamp_budget(s, b > kHeader ? b : kHeader);
 }
+// J2 base: slots of the longest unit-aligned prefix within b bytes (-1: the
+// bare header)
+__device__ __forceinline__ int64_t eb_slots(const CtlChunk& s, int64_t b) {
+  const int64_t room = b - kHeader - s.eb_sub;
+  if (room < 0) return -1;
+  int lo = 0, hi = s.eb_nslot;  // largest k with cum[k] <= room
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((int64_t)s.eb_cum[mid] <= room) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
 __device__ __forceinline__ int64_t stream_len(const CtlChunk& s, int64_t b) {
+  if (s.eb_cum) {
+    const int64_t k = eb_slots(s, b);
+    return k < 0 ? kHeader : kHeader + s.eb_sub + (int64_t)s.eb_cum[k];
+  }
   const int64_t full = kHeader + (int64_t)((s.T_base + 7) / 8);
   return b < full ? b : full;
 }
@@ -329,8 +347,14 @@ __device__ void tmemo_add(CtlChunk& s, int pi, int64_t t, const ProbeResult& r) 
 
 __device__ ProbeParam base_request(const CtlChunk& s, int64_t b, bool early) {
   ProbeParam p{};
-  uint64_t B = (uint64_t)(stream_len(s, b) - kHeader) * 8;
-  if (B > s.T_base) B = s.T_base;
+  uint64_t B;
+  if (s.eb_cum) {  // J2 base: the slots the prefix holds
+    const int64_t k = eb_slots(s, b);
+    B = k < 0 ? 0 : (uint64_t)k;
+  } else {
+    B = (uint64_t)(stream_len(s, b) - kHeader) * 8;
+    if (B > s.T_base) B = s.T_base;
+  }
   p.B = B;
   p.planes = kBasePlanes;
   p.active = 1;
@@ -409,6 +433,8 @@ __global__ void __launch_bounds__(1024) ctl_setup_kernel(CtlArgs a) {
     s.ntmemo[0] = s.ntmemo[1] = 0;
     for (int k = 0; k < kCtlSlots; k++) s.tpend[k] = -1;
     s.tpend_pi = 0;
+    s.eb_cum = nullptr;
+    s.eb_sub = s.eb_nslot = 0;
   }
   if (threadIdx.x == 0) *a.stats = CtlStats{};
 }
@@ -423,6 +449,11 @@ __global__ void __launch_bounds__(1024) ctl_base_kernel(CtlArgs a, int start, in
       if (start) {
         s.T_base = a.mo_base[f].total_bits;
         if (a.mo_base[f].overflow) s.status |= kCtlCapacity;
+        if (a.eb_cum) {  // J2 base: unit boundaries of the encoded stream
+          s.eb_nslot = kJ2Slots * a.eb_nb;
+          s.eb_cum = a.eb_cum + (int64_t)f * (s.eb_nslot + 1);
+          s.eb_sub = a.eb_nmax[f] == kExpNone ? 0 : a.eb_nb;
+        }
       }
       if (s.pend) {  // the probe that answered s.pend_budget
         memo_add(s, s.pend_budget, a.res[f], true);
@@ -576,6 +607,8 @@ __global__ void __launch_bounds__(1024) ctl_finalize_kernel(CtlArgs a) {
     o.T_base = s.T_base;
     o.T24 = s.T24;
     o.T32 = s.T32;
+    o.len_base = s.active && s.base_budget >= 0 ? stream_len(s, s.base_budget) : -1;
+    o.len_pure = s.active && s.pure_budget >= 0 ? stream_len(s, s.pure_budget) : -1;
     a.out[f] = o;
   }
 }

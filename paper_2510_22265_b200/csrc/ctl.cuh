@@ -49,6 +49,10 @@ struct CtlChunk {
   int32_t active;        // not constant, finite input
   int32_t status;
   int32_t vlim, pad_v;   // violations a count probe may see and still reach q
+  // opt-in J2 base layer (ebcot.cuh): the stream served for a budget is the
+  // longest unit-aligned prefix; eb_cum[k] = body bytes of the first k slots
+  const uint32_t* eb_cum;  // null: SPIHT base (prefix = the budget's bytes)
+  int32_t eb_sub, eb_nslot;  // block-table bytes (0: all-zero pyramid), slots
   // --- base memo (shared by the base and the pure-base searches) ---
   int32_t nmemo, pend;   // pend: memo budget of the probe in flight (-1 none)
   int64_t pend_budget;
@@ -88,6 +92,7 @@ struct CtlOut {
   int32_t pure_pruned, trunc_pruned;
   int32_t pad;
   uint64_t T_base, T24, T32;
+  int64_t len_base, len_pure;  // stream lengths of the chosen budgets (-1: none)
 };
 
 // per-call parameters (device resident, written before each batch)
@@ -121,6 +126,11 @@ struct CtlArgs {
   cudaGraphConditionalHandle h_loop;   // WHILE condition of the current loop
   cudaGraphConditionalHandle h_pure;   // IF: the pure-base branch has probes
   cudaGraphConditionalHandle h_trunc;  // IF: the truncation branch has probes
+  // opt-in J2 base layer: per chunk (eb_nb * 72 + 1) cumulative unit bytes,
+  // n_max (null: SPIHT base)
+  const uint32_t* eb_cum;
+  const int32_t* eb_nmax;
+  int eb_nb;
 };
 
 // active flags, machine-output init and controller state of every chunk

@@ -39,6 +39,7 @@
 #include "../../include/ebcc_gpu.h"
 #include "dwt.cuh"
 #include "idwt_fused.cuh"
+#include "ebcot.cuh"
 #include "probe.cuh"
 #include "spiht.cuh"
 #include "ctx.cuh"
@@ -184,6 +185,14 @@ struct Workspace {
     uint8_t* active = nullptr;
   } dec2;
   unsigned int* mm = nullptr;
+  // opt-in J2 base layer (ebcot.cuh), allocated on first use
+  struct EbSet {
+    EbBufs b{};
+    EbGeo geo{};
+    int32_t* blk_of = nullptr;
+    EbBlock* blocks = nullptr;
+    uint64_t* body_len = nullptr;
+  } eb;
   // pinned host mirrors of the per-step control arrays
   ProbeParam* h_prm = nullptr;
   ProbeResult* h_res = nullptr;
@@ -202,7 +211,7 @@ struct Workspace {
   // instantiated search graphs of this workspace, by batch shape
   struct SearchGraph {
     cudaGraphExec_t exec = nullptr;
-    int nf = -1, slots = 0, prune = -1, early = -1, inc = -1, cluster = -1;
+    int nf = -1, slots = 0, prune = -1, early = -1, inc = -1, cluster = -1, j2 = -1;
   };
   std::vector<SearchGraph> graphs;
 
@@ -236,6 +245,10 @@ struct Workspace {
     if (h_prm) cudaFreeHost(h_prm);
     if (h_res) cudaFreeHost(h_res);
     if (has_tt) free_tree_tables(tt);
+    void* ebp[] = {eb.b.qs, eb.b.flags, eb.b.plow, eb.b.cw, eb.b.uval, eb.b.uoff, eb.b.ztab,
+                   eb.b.cum, eb.b.nmax, eb.b.status, eb.blk_of, eb.blocks, eb.body_len};
+    for (void* p : ebp)
+      if (p) cudaFree(p);
     *this = Workspace{};
   }
 };
@@ -667,8 +680,8 @@ void encode_pyramids(ebcc_ctx* c, int nfields, bool residual, int planes,
   encode_collect(c, nfields, residual, active, mo, pl, c->stream);
 }
 
-void put_header(uint8_t* h, int n_max, int levels, int rows, int cols) {
-  h[0] = 'S'; h[1] = 'P';
+void put_header(uint8_t* h, int n_max, int levels, int rows, int cols, bool j2 = false) {
+  h[0] = j2 ? 'J' : 'S'; h[1] = j2 ? '2' : 'P';
   h[2] = (uint8_t)(int8_t)n_max;
   h[3] = (uint8_t)levels;
   uint32_t r = (uint32_t)rows, cc = (uint32_t)cols;
@@ -830,6 +843,36 @@ void add_conditional(cudaStream_t st, cudaStream_t bst, cudaGraphConditionalHand
   CK(cudaStreamEndCapture(bst, &out));
 }
 
+// the opt-in J2 base layer's buffers for nfields chunks of w's geometry
+// (allocated on first use, for the workspace capacity); stream bodies live in
+// bits_base (words_base words per chunk)
+EbBufs& ensure_ebcot(Workspace& w, int nfields, cudaStream_t st) {
+  Workspace::EbSet& e = w.eb;
+  if (!e.blocks) {
+    e.geo = ebcot_build_geo(w.g, &e.blk_of, &e.blocks, st);
+    CK(cudaGetLastError());
+    const int64_t N = w.g.n * (int64_t)w.cap, nb = e.geo.nb, cap = w.cap;
+    e.b.qs = dalloc<uint32_t>(N);
+    e.b.flags = dalloc<uint8_t>(N);
+    e.b.plow = dalloc<int8_t>(N);
+    e.b.cw_stride = w.g.n * kCwPerPoint + nb * kCwPerBlock;
+    e.b.cw = dalloc<uint8_t>(cap * e.b.cw_stride);
+    e.b.uval = dalloc<uint32_t>(cap * nb * kJ2Passes);
+    e.b.uoff = dalloc<int64_t>(cap * nb * kJ2Passes);
+    e.b.ztab = dalloc<uint8_t>(cap * nb);
+    e.b.cum = dalloc<uint32_t>(cap * (kJ2Slots * nb + 1));
+    e.b.nmax = dalloc<int32_t>(cap);
+    e.b.status = dalloc<int32_t>(cap);
+    e.body_len = dalloc<uint64_t>(cap);
+  }
+  e.b.nfields = nfields;
+  e.b.n = w.g.n;
+  e.b.body = reinterpret_cast<uint8_t*>(w.bits_base);
+  e.b.body_stride = w.words_base * 4;
+  e.b.body_len = e.body_len;
+  return e.b;
+}
+
 CtlArgs ctl_args(Workspace& w, int nfields, int slots) {
   CtlArgs a{};
   a.cs = w.ctl;
@@ -869,7 +912,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
                    bool prune,
                    ebcc_chunk_rec* recs, int64_t out_base_off, std::vector<PackPart>& parts,
                    std::vector<int64_t>& sizes, int in_groups = 0,
-                   const cudaEvent_t* in_ev = nullptr) {
+                   const cudaEvent_t* in_ev = nullptr, bool j2 = false) {
   Workspace& w = c->ws;
   const Geo& g = w.g;
   cudaStream_t st = c->stream;
@@ -933,7 +976,15 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   const int ntp = TS * nfields;
   *w.h_ctl_prm = CtlParams{q, r0, tol, prune ? 1 : 0, early_ok() ? 1 : 0, TS, 0};
   CK(cudaMemcpyAsync(w.ctl_prm, w.h_ctl_prm, sizeof(CtlParams), cudaMemcpyHostToDevice, st));
-  const CtlArgs a0 = ctl_args(w, nfields, TS);
+  CtlArgs a0 = ctl_args(w, nfields, TS);
+  // opt-in J2 base layer (ebcot.cuh): its encoder, probes and residue
+  EbBufs* eb = j2 ? &ensure_ebcot(w, nfields, st) : nullptr;
+  const EbGeo egeo = w.eb.geo;
+  if (eb) {
+    a0.eb_cum = eb->cum;
+    a0.eb_nmax = eb->nmax;
+    a0.eb_nb = egeo.nb;
+  }
   ctl_setup(a0, st);
   const int cluster = machine_cluster_size(false, std::max(nfields, c->machine_fields));
   // on the high-priority stream: the list machine needs whole SMs, and with
@@ -941,7 +992,12 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   CK(cudaEventRecord(c->ev_a, st));
   CK(cudaStreamWaitEvent(c->side, c->ev_a, 0));
   CK(cudaEventRecord(c->tev[0], c->side));
-  encode_launch(c, nfields, false, kBasePlanes, w.A, false, nullptr, c->side, cluster);
+  if (eb) {
+    ebcot_encode(w.A, egeo, g, *eb, w.active, c->side);
+    ebcot_nmax_to(*eb, w.mo_base, c->side);
+  } else {
+    encode_launch(c, nfields, false, kBasePlanes, w.A, false, nullptr, c->side, cluster);
+  }
   CK(cudaEventRecord(c->tev[1], c->side));
   CK(cudaEventRecord(c->ev_b, c->side));
   CK(cudaStreamWaitEvent(st, c->ev_b, 0));
@@ -953,7 +1009,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   Workspace::SearchGraph* sg = nullptr;
   for (Workspace::SearchGraph& x : w.graphs)
     if (x.nf == nfields && x.slots == TS && x.prune == (int)prune && x.early == early &&
-        x.inc == (int)inc_ok && x.cluster == cluster)
+        x.inc == (int)inc_ok && x.cluster == cluster && x.j2 == (int)j2)
       sg = &x;
   // EBCC_GRAPHS=0: the same sequence issued eagerly, the loop conditions read
   // back by the host after every controller step (profiling only: ncu does
@@ -965,6 +1021,12 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields * (i ? kTruncSlots : 1), st));
     CK(cudaMemsetAsync(w.icomputed, 0, sizeof(unsigned long long) * 2 * kMaxLevels, st));
     auto base_probe = [&](bool early_p) {
+      if (eb) {  // J2 base: closed-form prefix decode, inverse DWT, reduction
+        ebcot_probe_decode(egeo, *eb, w.prm, nfields, nfields, w.A, st);
+        inverse_dwt(w.A, w.B, N, nfields, g, st);
+        ebcot_probe_reduce(w.A, w.x32, w.fs, w.prm, N, nfields, !early_p, w.res, st);
+        return;
+      }
       probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32,
                  w.fs, w.res, st, inc_base, false, early_p);
     };
@@ -986,7 +1048,13 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       base_probe(false);
     }
     ctl_residue(a0, st);
-    base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
+    if (eb) {
+      ebcot_probe_decode(egeo, *eb, w.prm, nfields, nfields, w.A, st);
+      inverse_dwt(w.A, w.B, N, nfields, g, st);
+      ebcot_residue(w.A, w.prm, N, nfields, w.base_dec, w.norm, st);
+    } else {
+      base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
+    }
     forward_dwt_from(w.norm, w.A2, w.B2, N, nfields, g, st);
     CK(cudaEventRecord(c->ev_s0, st));
     encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, nullptr, st, cluster);
@@ -1025,6 +1093,12 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields * (i ? kTruncSlots : 1), s0));
     CK(cudaMemsetAsync(w.icomputed, 0, sizeof(unsigned long long) * 2 * kMaxLevels, s0));
     auto base_probe = [&](cudaStream_t ps, bool early_p) {
+      if (eb) {  // J2 base: closed-form prefix decode, inverse DWT, reduction
+        ebcot_probe_decode(egeo, *eb, w.prm, nfields, nfields, w.A, ps);
+        inverse_dwt(w.A, w.B, N, nfields, g, ps);
+        ebcot_probe_reduce(w.A, w.x32, w.fs, w.prm, N, nfields, !early_p, w.res, ps);
+        return;
+      }
       probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32,
                  w.fs, w.res, ps, inc_base, false, early_p);
     };
@@ -1050,7 +1124,13 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     // residue = norm - base decode at the chosen budget; residual DWT +
     // 32-plane encode (the 24-plane variant is its prefix)
     ctl_residue(a0, s0);
-    base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, s0);
+    if (eb) {
+      ebcot_probe_decode(egeo, *eb, w.prm, nfields, nfields, w.A, s0);
+      inverse_dwt(w.A, w.B, N, nfields, g, s0);
+      ebcot_residue(w.A, w.prm, N, nfields, w.base_dec, w.norm, s0);
+    } else {
+      base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, s0);
+    }
     forward_dwt_from(w.norm, w.A2, w.B2, N, nfields, g, s0);
     CK(cudaEventRecord(c->ev_s0, s0));
     encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, nullptr, s0, cluster);
@@ -1091,7 +1171,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     CK(cudaStreamEndCapture(s0, &gr));
     Workspace::SearchGraph ng;
     ng.nf = nfields; ng.slots = TS; ng.prune = prune; ng.early = early; ng.inc = inc_ok;
-    ng.cluster = cluster;
+    ng.cluster = cluster; ng.j2 = j2;
     CK(cudaGraphInstantiate(&ng.exec, gr, 0));
     cudaGraphDestroy(gr);
     w.graphs.push_back(ng);
@@ -1149,10 +1229,10 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     }
     if (o.status & kCtlCapacity)
       throw CudaFail{cudaErrorMemoryAllocation, "search state capacity (memo / list / loop guard)"};
-    const int64_t full = kHeader + (int64_t)((o.T_base + 7) / 8);
-    auto stream_len = [&](int64_t b) { return b < full ? b : full; };
-    const int64_t pure_len = o.pure_budget >= 0 ? stream_len(o.pure_budget) : -1;
-    const int64_t base_len = stream_len(o.base_budget);
+    // (the controller's stream lengths: the budget's bytes, or for a J2
+    // base the longest unit-aligned prefix)
+    const int64_t pure_len = o.pure_budget >= 0 ? o.len_pure : -1;
+    const int64_t base_len = o.len_base;
     const int64_t two_len = o.trunc_t >= 0 ? base_len + kHeader + o.trunc_t : -1;
     if (pure_len < 0 && two_len < 0) {
       r.status = EBCC_E_RESIDUAL;
@@ -1167,9 +1247,10 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     int64_t off = out_base_off;
     for (int64_t z : sizes) off += z;
     PackPart bp{};
-    bp.src = w.bits_base + (int64_t)f * w.words_base;
+    bp.src = w.bits_base + (int64_t)f * w.words_base;  // (J2: the stream body)
     bp.bit_limit = ~0ull;
-    put_header(bp.hdr, base_nmax, g.levels, g.rows, g.cols);
+    put_header(bp.hdr, base_nmax == kExpNone ? kZeroSentinel : base_nmax, g.levels, g.rows,
+               g.cols, j2);
     if (pure_len >= 0 && (two_len < 0 || pure_len <= two_len)) {
       r.mode = EBCC_MODE_PURE_BASE;
       r.base_len = pure_len;
@@ -1587,7 +1668,8 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
       int s;
       try {
         s = compress_batch(c, nb, eps_rel, q, r0, search_tol, !(flags & EBCC_FULL_SEARCH),
-                           recs + f0, done, bparts, bsizes, in_groups, c->ev_groups.data());
+                           recs + f0, done, bparts, bsizes, in_groups, c->ev_groups.data(),
+                           (flags & EBCC_BASE_EBCOT) != 0);
       } catch (IngestFail&) {
         c->err_index += f0 * g.n;
         return fail(c, EBCC_E_INGEST, "non-finite value in the input");
@@ -1985,6 +2067,7 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
       std::vector<uint64_t> blim(nb, 0), rlim(nb, 0);
       std::vector<uint8_t> bact(nb, 0), ract(nb, 0), pure(nb, 0), cst(nb, 0);
       std::vector<FieldScal> fsv(nb);
+      int j2 = -1;  // base streams of the batch: 0 SPIHT ('SP'), 1 J2 (opt-in layer)
       // stream headers of device-resident payloads: all copied, one wait
       uint8_t* hdrs = nullptr;
       if (flags & EBCC_INPUT_ON_DEVICE) {
@@ -2013,6 +2096,10 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           return fail(c, EBCC_E_FORMAT, "stream shorter than header");
         const uint8_t* bh = (flags & EBCC_INPUT_ON_DEVICE) ? hdrs + 2 * kHeader * i
                                                             : payload + offsets[f0 + i];
+        const int is_j2 = bh[0] == 'J' && bh[1] == '2';
+        if (j2 >= 0 && is_j2 != j2)
+          return fail(c, EBCC_E_FORMAT, "mixed base stream formats in one chunk shape");
+        j2 = is_j2;
         int nb_max = (int8_t)bh[2];
         bmo[i].n_max = nb_max == kZeroSentinel ? kExpNone : nb_max;
         blim[i] = (uint64_t)(r.base_len - kHeader) * 8;
@@ -2110,7 +2197,31 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         CK(cudaEventRecord(c->ev_b, c->side));
         c->stats.kernel_launches += 4;
       }
-      {
+      if (j2 == 1) {
+        // opt-in J2 base layer: parse the units, MQ-decode every code-block,
+        // inverse DWT into base_dec (all-zero streams decode to zeros)
+        EbBufs& eb = ensure_ebcot(w, nb, st);
+        std::vector<int32_t> enm(nb);
+        std::vector<uint64_t> blen(nb, 0);
+        std::vector<uint8_t> eact(nb);
+        for (int i = 0; i < nb; i++) {
+          enm[i] = bmo[i].n_max;
+          eact[i] = !cst[i];
+          if (!cst[i]) blen[i] = (uint64_t)(recs[f0 + i].base_len - kHeader);
+        }
+        h2d_small(c, eb.nmax, enm.data(), sizeof(int32_t) * nb, st);
+        h2d_small(c, w.eb.body_len, blen.data(), sizeof(uint64_t) * nb, st);
+        h2d_small(c, w.active, eact.data(), nb, st);
+        CK(cudaMemsetAsync(eb.status, 0, sizeof(int32_t) * nb, st));
+        ebcot_stream_decode(w.eb.geo, g, eb, w.active, w.base_dec, st);
+        inverse_dwt(w.base_dec, w.B, g.n, nb, g, st);
+        c->stats.kernel_launches += 2 + 2 * g.levels;
+        std::vector<int32_t> est(nb);
+        CK(cudaMemcpyAsync(est.data(), eb.status, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int i = 0; i < nb; i++)
+          if (est[i]) return fail(c, EBCC_E_FORMAT, "malformed J2 base stream");
+      } else {
         MachineBufs mb = machine_bufs(w, nb, false);
         h2d_small(c, mb.out, bmo.data(), sizeof(MachineOut) * nb, st);
         h2d_small(c, const_cast<uint64_t*>(w.limit), blim.data(), sizeof(uint64_t) * nb, st);
@@ -2162,8 +2273,10 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           gcst[i] = in && cst[i];
         }
         h2d_small(c, w.prm, prm.data(), sizeof(ProbeParam) * nb, st);
-        decode_field(meta_of(w, false), w.prm, w.A, w.B, g, nb, w.base_dec, st, xe_b);
-        c->stats.kernel_launches += g.levels;
+        if (j2 != 1) {  // (a J2 base field is already in base_dec)
+          decode_field(meta_of(w, false), w.prm, w.A, w.B, g, nb, w.base_dec, st, xe_b);
+          c->stats.kernel_launches += g.levels;
+        }
         CK(cudaGetLastError());
         if (g_slow.on()) {
           CK(cudaStreamSynchronize(st));
@@ -2571,10 +2684,11 @@ int ebcc_check_streams(const uint8_t* data, int64_t len, const uint8_t* records2
   if (!data || n < 0 || (n && (!records25 || !offsets)) || !levels || !bad) return EBCC_E_ARGUMENT;
   *levels = 0;
   *bad = -1;
-  auto hdr_ok = [&](int64_t off, int64_t ln, int* lv) {
+  // base streams may also be 'J2' (the opt-in JPEG2000-style layer)
+  auto hdr_ok = [&](int64_t off, int64_t ln, int* lv, bool base) {
     if (ln < kHeader || off < 0 || off + ln > len) return false;
     const uint8_t* h = data + off;
-    if (h[0] != 'S' || h[1] != 'P') return false;
+    if (!(h[0] == 'S' && h[1] == 'P') && !(base && h[0] == 'J' && h[1] == '2')) return false;
     uint32_t r, c;
     memcpy(&r, h + 4, 4);
     memcpy(&c, h + 8, 4);
@@ -2591,9 +2705,9 @@ int ebcc_check_streams(const uint8_t* data, int64_t len, const uint8_t* records2
     memcpy(&bl, rec + 17, 4);
     memcpy(&rl, rec + 21, 4);
     int lv = 0, rlv = 0;
-    if (!hdr_ok(offsets[i], bl, &lv)) { *bad = i; return EBCC_E_FORMAT; }
+    if (!hdr_ok(offsets[i], bl, &lv, true)) { *bad = i; return EBCC_E_FORMAT; }
     if (mode == EBCC_MODE_TWO_LAYER && rl > 0 &&
-        (!hdr_ok(offsets[i] + bl, rl, &rlv) || rlv != lv)) { *bad = i; return EBCC_E_FORMAT; }
+        (!hdr_ok(offsets[i] + bl, rl, &rlv, false) || rlv != lv)) { *bad = i; return EBCC_E_FORMAT; }
     if (lv > 5) { *bad = i; return EBCC_E_FORMAT; }
     if (*levels && lv != *levels) { *bad = i; return EBCC_E_ARGUMENT; }
     *levels = lv;

@@ -47,7 +47,7 @@ def default_levels(rows: int, cols: int) -> int:
 # batched device calls
 
 def compress_batch(stack: np.ndarray, params: EbccParams, ctx=None, fetch: bool = True,
-                   full_search: bool = False):
+                   full_search: bool = False, base_codec: str = "spiht"):
     """Compress a (n, rows, cols) float32 stack of chunks on the device.
 
     Returns (records[REC_DTYPE], offsets int64[n], payload uint8[total],
@@ -57,13 +57,18 @@ def compress_batch(stack: np.ndarray, params: EbccParams, ctx=None, fetch: bool 
     total) for :meth:`_lib.Context.fetch_container`.  ``full_search`` runs
     every probe of the reference's searches (the default stops a search whose
     candidate can no longer be chosen: same bytes, fewer probes).
+    ``base_codec="ebcot"`` selects the opt-in JPEG2000-style base layer
+    ('J2' streams, container version 2; the reference has no such layer).
     """
+    if base_codec not in _lib.BASE_CODECS:
+        raise ArgumentError(f"unknown base codec {base_codec!r}")
     ctx = ctx or _lib.context()
     stack = np.ascontiguousarray(stack, dtype=np.float32)
     n, rows, cols = stack.shape
     recs, offs, total, st = ctx.compress(stack, n, rows, cols, params.epsilon_rel, params.q,
                                          params.r0, params.search_tol,
-                                         flags=_lib.FULL_SEARCH if full_search else 0)
+                                         flags=(_lib.FULL_SEARCH if full_search else 0) |
+                                         _lib.BASE_CODECS[base_codec])
     if st not in (_lib.OK, _lib.E_RESIDUAL):
         ctx.raise_for(st, "ebcc_compress")
     if not fetch:
@@ -119,7 +124,8 @@ def _each_group(fn, groups: dict, ctx):
     return [fn(it) for it in groups.items()]
 
 
-def compress_chunks(chunks: list, params: EbccParams, ctx=None) -> list:
+def compress_chunks(chunks: list, params: EbccParams, ctx=None,
+                    base_codec: str = "spiht") -> list:
     """Compress a list of flattened Chunk objects (any shapes), tile order kept."""
     if not chunks:
         return []
@@ -141,7 +147,7 @@ def compress_chunks(chunks: list, params: EbccParams, ctx=None) -> list:
         stack = np.empty((len(idx), rows, cols), dtype=np.float32)
         for k, i in enumerate(idx):
             stack[k] = chunks[i].values
-        return compress_batch(stack, params, ctx)
+        return compress_batch(stack, params, ctx, base_codec=base_codec)
 
     for ((rows, cols), idx), (recs, offs, payload, st) in zip(groups.items(),
                                                               _each_group(run, groups, ctx)):
@@ -171,17 +177,19 @@ def compress_chunk(chunk: Chunk, params: EbccParams, ctx=None) -> CompressedChun
         raise
 
 
-def compress_grid(grid: GridArray, params: EbccParams, ctx=None) -> list:
+def compress_grid(grid: GridArray, params: EbccParams, ctx=None,
+                  base_codec: str = "spiht") -> list:
     """pipeline.compress_grid (pipeline.py:358-367), batched on the device."""
     chunks = [flatten_chunk(block, origin) for origin, block in iter_blocks(grid)]
-    return compress_chunks(chunks, params, ctx)
+    return compress_chunks(chunks, params, ctx, base_codec)
 
 
 def _parse_sp(data: bytes, rows: int, cols: int, what: str):
     if len(data) < HEADER_SIZE:
         raise FormatError(f"stream shorter than {HEADER_SIZE}-byte header", offset=len(data))
     magic, n_max, levels, r, c = _SP_HEADER.unpack_from(data, 0)
-    if magic != b"SP":
+    # (a base stream may be 'J2': the opt-in JPEG2000-style layer, container v2)
+    if magic != b"SP" and not (what == "base" and magic == b"J2"):
         raise FormatError(f"bad stream magic {magic!r}", offset=0)
     if r < 1 or c < 1 or levels < 1:
         raise FormatError(f"bad stream dimensions {r}x{c}/{levels}", offset=2)
@@ -266,7 +274,7 @@ def decompress_grid(chunks, dims, chunk_shape=None, ctx=None) -> np.ndarray:
 # container-level fast paths used by api.compress / api.decompress
 
 def grid_to_records(grid: GridArray, params: EbccParams, ctx=None, orig_shape=None,
-                    container: bool = False):
+                    container: bool = False, base_codec: str = "spiht"):
     """Compress a grid straight to (records[RECORD_DTYPE], payload, offsets).
 
     Default chunking (one 2D slice per (t, p)) is fed to the device without a
@@ -290,7 +298,8 @@ def grid_to_records(grid: GridArray, params: EbccParams, ctx=None, orig_shape=No
         stack = grid.data.reshape(t * p, h, w)
         ctx = ctx or _lib.context()
         try:
-            recs, offs, payload, st = compress_batch(stack, params, ctx, fetch=not container)
+            recs, offs, payload, st = compress_batch(stack, params, ctx, fetch=not container,
+                                                     base_codec=base_codec)
         except IngestError as exc:
             at = tuple(int(i) for i in np.unravel_index(int(exc.index), shape))
             raise IngestError(f"non-finite value at index {at}", index=at) from None
@@ -307,13 +316,14 @@ def grid_to_records(grid: GridArray, params: EbccParams, ctx=None, orig_shape=No
         out["base_len"] = recs["base_len"]
         out["resid_len"] = recs["resid_len"]
         if container:
-            from .container import pack_header
-            return ctx.fetch_container(pack_header(grid.dims, grid.chunk_shape, len(out)), out,
-                                       payload)
+            from .container import VERSION, VERSION_EBCOT, pack_header
+            version = VERSION_EBCOT if base_codec == "ebcot" else VERSION
+            return ctx.fetch_container(pack_header(grid.dims, grid.chunk_shape, len(out), version),
+                                       out, payload)
         return out, payload, offs, recs
     from .core import _require_finite
     _require_finite(grid.data.reshape(shape))
-    chunks = compress_grid(grid, params, ctx)
+    chunks = compress_grid(grid, params, ctx, base_codec)
     out = np.zeros(len(chunks), dtype=RECORD_DTYPE)
     offs = np.zeros(len(chunks), dtype=np.int64)
     pos = 0
@@ -325,8 +335,9 @@ def grid_to_records(grid: GridArray, params: EbccParams, ctx=None, orig_shape=No
     payload = np.frombuffer(b"".join(cc.payload for cc in chunks), np.uint8) if pos else \
         np.zeros(0, np.uint8)
     if container:
-        from .container import assemble
-        return assemble(grid.dims, grid.chunk_shape, out, payload, offs)
+        from .container import VERSION, VERSION_EBCOT, assemble
+        return assemble(grid.dims, grid.chunk_shape, out, payload, offs,
+                        VERSION_EBCOT if base_codec == "ebcot" else VERSION)
     return out, payload, offs, None
 
 
