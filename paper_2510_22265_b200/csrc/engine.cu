@@ -1578,17 +1578,27 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
         CK(cudaMemcpyAsync(c->ws.x32, c->d_in2, in_bytes, cudaMemcpyDeviceToDevice, st));
         CK(cudaEventRecord(c->ev_in2_used, st));
         g_trace.add(g_lane, "in_prefetched", (int)f0);
-      } else if (host_in && is_pageable(src)) {
+      }
+      // pageable input not prefetched (the first batch): staged group by
+      // group below, each group's upload issued as soon as it is staged
+      const float* stage_from = nullptr;
+      if (!prefetched && host_in && is_pageable(src)) {
         CK(cudaGetLastError());
         uint8_t* stg = stage_buf(stage_k, (int64_t)in_bytes);
         CK(cudaGetLastError());
-        parallel_memcpy(stg, src, in_bytes);
+        stage_from = src;
         src = reinterpret_cast<const float*>(stg);
         stage_k ^= 1;
-        g_trace.add(g_lane, "in_staged", (int)f0);
       }
       CK(cudaGetLastError());
       const bool chained = chain && f0 == 0 && !(flags & EBCC_INPUT_ON_DEVICE);
+      if (stage_from && chained && lane > 0) {
+        // a later lane's upload queues behind the earlier lanes': stage it
+        // whole now, concurrently with theirs
+        parallel_memcpy(const_cast<float*>(src), stage_from, in_bytes);
+        stage_from = nullptr;
+        g_trace.add(g_lane, "in_staged", (int)f0);
+      }
       // host input: copied in field groups on the copy stream, each group
       // transformed as soon as it lands (compress_batch)
       static const int in_groups_env =
@@ -1613,12 +1623,17 @@ int compress_impl(ebcc_ctx* c, const float* fields, int64_t nfields, int32_t row
       if (in_groups) {
         for (int k = 0; k < in_groups; k++) {
           const int64_t a = (int64_t)nb * k / in_groups, b = (int64_t)nb * (k + 1) / in_groups;
+          if (b > a && stage_from)
+            parallel_memcpy(const_cast<float*>(src) + a * g.n, stage_from + a * g.n,
+                            sizeof(float) * g.n * (b - a));
           if (b > a)
             CK(cudaMemcpyAsync(c->ws.x32 + a * g.n, src + a * g.n, sizeof(float) * g.n * (b - a),
                                cudaMemcpyHostToDevice, cst));
           CK(cudaEventRecord(c->ev_groups[k], cst));
         }
+        if (stage_from) g_trace.add(g_lane, "in_staged", (int)f0);
       } else if (!prefetched) {
+        if (stage_from) parallel_memcpy(const_cast<float*>(src), stage_from, in_bytes);
         CK(cudaMemcpyAsync(c->ws.x32, src, in_bytes,
                            (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
                                                           : cudaMemcpyHostToDevice,
