@@ -202,7 +202,13 @@ struct MqDec {
 };
 
 // ---- tier-1 contexts (T.800 Tables D.1, D.3, D.4) ---------------------------
-constexpr uint8_t F_SIG = 1, F_VIS = 2, F_REF = 4, F_NEG = 8;
+// Per-sample state word: own flags in bits 0..3, the significance of the 8
+// neighbours in bits 4..11 and the signs of the 4 edge neighbours in bits
+// 12..15, kept up to date when a sample turns significant (one load per
+// visit instead of nine; neighbours outside the code-block never count).
+constexpr uint16_t F_SIG = 1, F_VIS = 2, F_REF = 4, F_NEG = 8;
+constexpr int NB_W = 4, NB_E = 5, NB_N = 6, NB_S = 7, NB_NW = 8, NB_NE = 9, NB_SW = 10, NB_SE = 11;
+constexpr uint16_t NSIG_MASK = 0x0FF0;
 
 __device__ __forceinline__ int sig_ctx(int orient, int h, int v, int d) {
   if (orient == 1) { const int t = h; h = v; v = t; }
@@ -220,33 +226,29 @@ __device__ __forceinline__ int sig_ctx(int orient, int h, int v, int d) {
   return d >= 2 ? 2 : (d == 1 ? 1 : 0);
 }
 
-// one code-block's view of the per-coefficient state (pyramid positions)
+// one code-block's view of the per-sample state (pyramid positions)
 struct Blk {
-  uint8_t* f;      // flags of the field, row stride `cols`
+  uint16_t* f;     // state words of the field, row stride `cols`
   int64_t base;    // position of the block's (0, 0)
   int cols, h, w, orient;
-  __device__ __forceinline__ int at(int y, int x) const {
-    if (y < 0 || x < 0 || y >= h || x >= w) return 0;
+  __device__ __forceinline__ uint16_t& ref(int y, int x) const {
     return f[base + (int64_t)y * cols + x];
   }
-  __device__ __forceinline__ uint8_t& ref(int y, int x) const {
-    return f[base + (int64_t)y * cols + x];
+  __device__ __forceinline__ int word(int y, int x) const { return ref(y, x); }
+  __device__ __forceinline__ int sig_context(int wd) const {
+    const int hh = ((wd >> NB_W) & 1) + ((wd >> NB_E) & 1);
+    const int vv = ((wd >> NB_N) & 1) + ((wd >> NB_S) & 1);
+    const int dd = __popc((wd >> NB_NW) & 15);
+    return sig_ctx(orient, hh, vv, dd);
   }
-  __device__ __forceinline__ void neigh(int y, int x, int& hh, int& vv, int& dd) const {
-    hh = (at(y, x - 1) & F_SIG) + (at(y, x + 1) & F_SIG);
-    vv = (at(y - 1, x) & F_SIG) + (at(y + 1, x) & F_SIG);
-    dd = (at(y - 1, x - 1) & F_SIG) + (at(y - 1, x + 1) & F_SIG) + (at(y + 1, x - 1) & F_SIG) +
-         (at(y + 1, x + 1) & F_SIG);
-  }
-  __device__ __forceinline__ int contrib(int y0, int x0, int y1, int x1) const {
-    int s = 0;
-    const int a = at(y0, x0), c = at(y1, x1);
-    if (a & F_SIG) s += (a & F_NEG) ? -1 : 1;
-    if (c & F_SIG) s += (c & F_NEG) ? -1 : 1;
-    return s > 0 ? 1 : (s < 0 ? -1 : 0);
-  }
-  __device__ __forceinline__ int sign_ctx(int y, int x, int& xr) const {
-    const int hc = contrib(y, x - 1, y, x + 1), vc = contrib(y - 1, x, y + 1, x);
+  __device__ __forceinline__ int sign_ctx(int wd, int& xr) const {
+    auto contrib = [&](int sa, int sb) {
+      int s = 0;
+      if ((wd >> sa) & 1) s += ((wd >> (sa + 8)) & 1) ? -1 : 1;
+      if ((wd >> sb) & 1) s += ((wd >> (sb + 8)) & 1) ? -1 : 1;
+      return s > 0 ? 1 : (s < 0 ? -1 : 0);
+    };
+    const int hc = contrib(NB_W, NB_E), vc = contrib(NB_N, NB_S);
     int cx;
     xr = 0;
     if (hc == 1) cx = vc == 1 ? 13 : (vc == 0 ? 12 : 11);
@@ -254,11 +256,27 @@ struct Blk {
     else { cx = vc == 1 ? 11 : (vc == 0 ? 12 : 13); xr = 1; }
     return cx;
   }
-  __device__ __forceinline__ int mr_ctx(int y, int x) const {
-    if (at(y, x) & F_REF) return 16;
-    int a, b, c;
-    neigh(y, x, a, b, c);
-    return (a + b + c) ? 15 : 14;
+  __device__ __forceinline__ int mr_ctx(int wd) const {
+    if (wd & F_REF) return 16;
+    return (wd & NSIG_MASK) ? 15 : 14;
+  }
+  // (y, x) turns significant with sign neg: its own bit and its neighbours'
+  __device__ __forceinline__ void set_sig(int y, int x, int neg) const {
+    ref(y, x) |= F_SIG | (neg ? F_NEG : 0);
+    auto nb = [&](int yy, int xx, int bit, bool edge) {
+      if (yy < 0 || xx < 0 || yy >= h || xx >= w) return;
+      uint16_t add = (uint16_t)(1u << bit);
+      if (edge && neg) add |= (uint16_t)(1u << (bit + 8));
+      ref(yy, xx) |= add;
+    };
+    nb(y, x - 1, NB_E, true);
+    nb(y, x + 1, NB_W, true);
+    nb(y - 1, x, NB_S, true);
+    nb(y + 1, x, NB_N, true);
+    nb(y - 1, x - 1, NB_SE, false);
+    nb(y - 1, x + 1, NB_SW, false);
+    nb(y + 1, x - 1, NB_NE, false);
+    nb(y + 1, x + 1, NB_NW, false);
   }
 };
 
@@ -302,11 +320,8 @@ __device__ void run_pass(const Blk& b, uint32_t* q, int8_t* plow, int p, int pty
       int y = y0;
       if (ptype == 2 && sh == 4) {  // cleanup run mode
         bool run_ok = true;
-        for (int k = 0; k < 4 && run_ok; k++) {
-          int hh, vv, dd;
-          b.neigh(y0 + k, x, hh, vv, dd);
-          if ((b.at(y0 + k, x) & (F_SIG | F_VIS)) || hh + vv + dd) run_ok = false;
-        }
+        for (int k = 0; k < 4 && run_ok; k++)
+          if (b.word(y0 + k, x) & (F_SIG | F_VIS | NSIG_MASK)) run_ok = false;
         if (run_ok) {
           int first = 4;
           if (ENC)
@@ -322,25 +337,23 @@ __device__ void run_pass(const Blk& b, uint32_t* q, int8_t* plow, int p, int pty
           }
           const int yy = y0 + first;
           int xr;
-          const int scx = b.sign_ctx(yy, x, xr);
-          const int neg = ENC ? ((b.at(yy, x) & F_NEG) != 0) : 0;
+          const int wd = b.word(yy, x);
+          const int scx = b.sign_ctx(wd, xr);
+          const int neg = ENC ? (int)(qi(yy, x) >> 31) : 0;
           const int sb = c.code(scx, neg ^ xr) ^ xr;
-          if (ENC) {
-            // significant in a cleanup pass: sp bit stays 0
-          } else {
+          if (!ENC) {
             qi(yy, x) |= 1u << p;
             pl(yy, x) = (int8_t)p;
-            if (sb) b.ref(yy, x) |= F_NEG;
           }
-          b.ref(yy, x) |= F_SIG;
+          b.set_sig(yy, x, sb);  // (cleanup significance: the sp bit stays 0)
           y = yy + 1;
         }
       }
       for (; y < y0 + sh; y++) {
-        const int fl = b.at(y, x);
+        const int wd = b.word(y, x);
         if (ptype == 1) {  // magnitude refinement: significant before this plane
-          if (!(fl & F_SIG) || (fl & F_VIS)) continue;
-          const int cx = b.mr_ctx(y, x);
+          if (!(wd & F_SIG) || (wd & F_VIS)) continue;
+          const int cx = b.mr_ctx(wd);
           const int bit = c.code(cx, ENC ? (int)((qi(y, x) >> p) & 1) : 0);
           if (!ENC) {
             qi(y, x) |= (uint32_t)bit << p;
@@ -349,30 +362,27 @@ __device__ void run_pass(const Blk& b, uint32_t* q, int8_t* plow, int p, int pty
           b.ref(y, x) |= F_REF;
           continue;
         }
-        if (fl & F_SIG) continue;
-        int hh, vv, dd;
-        b.neigh(y, x, hh, vv, dd);
+        if (wd & F_SIG) continue;
         if (ptype == 0) {
-          if (hh + vv + dd == 0) continue;
+          if (!(wd & NSIG_MASK)) continue;
           b.ref(y, x) |= F_VIS;
-        } else if (fl & F_VIS) {
+        } else if (wd & F_VIS) {
           continue;
         }
-        const int cx = sig_ctx(b.orient, hh, vv, dd);
+        const int cx = b.sig_context(wd);
         const int bit = c.code(cx, ENC ? (int)((qi(y, x) >> p) & 1) : 0);
         if (bit) {
           int xr;
-          const int scx = b.sign_ctx(y, x, xr);
-          const int neg = ENC ? ((fl & F_NEG) != 0) : 0;
+          const int scx = b.sign_ctx(wd, xr);
+          const int neg = ENC ? (int)(qi(y, x) >> 31) : 0;
           const int sb = c.code(scx, neg ^ xr) ^ xr;
           if (ENC) {
             if (ptype == 0) qi(y, x) |= 1u << 30;  // significant in a SP pass
           } else {
             qi(y, x) |= 1u << p;
             pl(y, x) = (int8_t)p;
-            if (sb) b.ref(y, x) |= F_NEG;
           }
-          b.ref(y, x) |= F_SIG;
+          b.set_sig(y, x, sb);
         }
       }
     }
@@ -416,7 +426,7 @@ __global__ void nmax_kernel(const double* __restrict__ coef, int64_t n, int32_t*
 }
 
 __global__ void quantize_kernel(const double* __restrict__ coef, int64_t n, const int32_t* nmax,
-                                uint32_t* qs, uint8_t* flags, const uint8_t* active) {
+                                uint32_t* qs, uint16_t* flags, const uint8_t* active) {
   const int f = blockIdx.y;
   if (active && !active[f]) return;
   const int nm = nmax[f];
@@ -427,7 +437,7 @@ __global__ void quantize_kernel(const double* __restrict__ coef, int64_t n, cons
     uint32_t q = 0;
     if (nm != kExpNone) q = (uint32_t)floor(scalbn(fabs(c), -e0));
     qs[(int64_t)f * n + i] = q | (c < 0.0 ? 0x80000000u : 0u);
-    flags[(int64_t)f * n + i] = c < 0.0 ? F_NEG : 0;
+    flags[(int64_t)f * n + i] = 0;  // (the sign is in qs until the sample turns significant)
   }
 }
 
@@ -465,7 +475,7 @@ __global__ void __launch_bounds__(64) t1_encode_kernel(EbGeo eg, int cols, EbBuf
     pass_of(pt, j, p, ptype);
     if (ptype == 0)
       for (int y = 0; y < B.h; y++)
-        for (int x = 0; x < B.w; x++) blk.ref(y, x) &= (uint8_t)~F_VIS;
+        for (int x = 0; x < B.w; x++) blk.ref(y, x) &= (uint16_t)~F_VIS;
     PassCoder<true> c{&e, nullptr, &s, 0, false, seg + used, segcap - used, nullptr, 0};
     run_pass<true>(blk, q, nullptr, p, ptype, c);
     if (c.started) {
@@ -685,7 +695,7 @@ __global__ void __launch_bounds__(64) t1_decode_kernel(EbGeo eg, int cols, EbBuf
       pass_of(pt, j, p, ptype);
       if (ptype == 0)
         for (int y = 0; y < B.h; y++)
-          for (int x = 0; x < B.w; x++) blk.ref(y, x) &= (uint8_t)~F_VIS;
+          for (int x = 0; x < B.w; x++) blk.ref(y, x) &= (uint16_t)~F_VIS;
       const bool sym = uv[j] != 0xFFFFFFFFu;
       PassCoder<false> c{nullptr, &d, &s, 0, false, nullptr, 0, body + uo[j],
                          sym ? (int64_t)uv[j] - 1 : 0};

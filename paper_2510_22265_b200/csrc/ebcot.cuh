@@ -46,7 +46,7 @@ struct EbBufs {
   int nfields;
   int64_t n;
   uint32_t* qs;        // [f][n] magnitude | significance-in-SP << 30 | negative << 31
-  uint8_t* flags;      // [f][n] tier-1 state
+  uint16_t* flags;     // [f][n] tier-1 state word (own flags, neighbours' significance / signs)
   int8_t* plow;        // [f][n] decoder: lowest decoded plane
   uint8_t* cw;         // [f][cw_stride] per-block codeword scratch
   int64_t cw_stride;   // n * kCwPerPoint + nb * kCwPerBlock bytes per field

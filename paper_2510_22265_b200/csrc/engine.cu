@@ -192,6 +192,7 @@ struct Workspace {
     int32_t* blk_of = nullptr;
     EbBlock* blocks = nullptr;
     uint64_t* body_len = nullptr;
+    double* ll = nullptr;  // second LL buffer of the fused probe levels (with B)
   } eb;
   // pinned host mirrors of the per-step control arrays
   ProbeParam* h_prm = nullptr;
@@ -246,7 +247,7 @@ struct Workspace {
     if (h_res) cudaFreeHost(h_res);
     if (has_tt) free_tree_tables(tt);
     void* ebp[] = {eb.b.qs, eb.b.flags, eb.b.plow, eb.b.cw, eb.b.uval, eb.b.uoff, eb.b.ztab,
-                   eb.b.cum, eb.b.nmax, eb.b.status, eb.blk_of, eb.blocks, eb.body_len};
+                   eb.b.cum, eb.b.nmax, eb.b.status, eb.blk_of, eb.blocks, eb.body_len, eb.ll};
     for (void* p : ebp)
       if (p) cudaFree(p);
     *this = Workspace{};
@@ -853,7 +854,7 @@ EbBufs& ensure_ebcot(Workspace& w, int nfields, cudaStream_t st) {
     CK(cudaGetLastError());
     const int64_t N = w.g.n * (int64_t)w.cap, nb = e.geo.nb, cap = w.cap;
     e.b.qs = dalloc<uint32_t>(N);
-    e.b.flags = dalloc<uint8_t>(N);
+    e.b.flags = dalloc<uint16_t>(N);
     e.b.plow = dalloc<int8_t>(N);
     e.b.cw_stride = w.g.n * kCwPerPoint + nb * kCwPerBlock;
     e.b.cw = dalloc<uint8_t>(cap * e.b.cw_stride);
@@ -864,6 +865,7 @@ EbBufs& ensure_ebcot(Workspace& w, int nfields, cudaStream_t st) {
     e.b.nmax = dalloc<int32_t>(cap);
     e.b.status = dalloc<int32_t>(cap);
     e.body_len = dalloc<uint64_t>(cap);
+    e.ll = dalloc<double>(N);
   }
   e.b.nfields = nfields;
   e.b.n = w.g.n;
@@ -980,6 +982,10 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   // opt-in J2 base layer (ebcot.cuh): its encoder, probes and residue
   EbBufs* eb = j2 ? &ensure_ebcot(w, nfields, st) : nullptr;
   const EbGeo egeo = w.eb.geo;
+  Meta mj2{};  // J2 probes: the fused levels over the decoded f64 pyramid in A
+  mj2.coef = w.A;
+  mj2.mo = w.mo_base;
+  mj2.stride = N;
   if (eb) {
     a0.eb_cum = eb->cum;
     a0.eb_nmax = eb->nmax;
@@ -1021,10 +1027,10 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields * (i ? kTruncSlots : 1), st));
     CK(cudaMemsetAsync(w.icomputed, 0, sizeof(unsigned long long) * 2 * kMaxLevels, st));
     auto base_probe = [&](bool early_p) {
-      if (eb) {  // J2 base: closed-form prefix decode, inverse DWT, reduction
+      if (eb) {  // J2 base: closed-form prefix decode, then the fused probe levels
         ebcot_probe_decode(egeo, *eb, w.prm, nfields, nfields, w.A, st);
-        inverse_dwt(w.A, w.B, N, nfields, g, st);
-        ebcot_probe_reduce(w.A, w.x32, w.fs, w.prm, N, nfields, !early_p, w.res, st);
+        probe_base(mj2, w.prm, w.B, w.eb.ll, g, nfields, w.norm, w.x32, w.fs, w.res, st,
+                   nullptr, true, early_p);
         return;
       }
       probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32,
@@ -1050,8 +1056,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     ctl_residue(a0, st);
     if (eb) {
       ebcot_probe_decode(egeo, *eb, w.prm, nfields, nfields, w.A, st);
-      inverse_dwt(w.A, w.B, N, nfields, g, st);
-      ebcot_residue(w.A, w.prm, N, nfields, w.base_dec, w.norm, st);
+      base_to_residue(mj2, w.prm, w.B, w.eb.ll, g, nfields, w.norm, w.base_dec, w.norm, st);
     } else {
       base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
     }
@@ -1093,10 +1098,10 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields * (i ? kTruncSlots : 1), s0));
     CK(cudaMemsetAsync(w.icomputed, 0, sizeof(unsigned long long) * 2 * kMaxLevels, s0));
     auto base_probe = [&](cudaStream_t ps, bool early_p) {
-      if (eb) {  // J2 base: closed-form prefix decode, inverse DWT, reduction
+      if (eb) {  // J2 base: closed-form prefix decode, then the fused probe levels
         ebcot_probe_decode(egeo, *eb, w.prm, nfields, nfields, w.A, ps);
-        inverse_dwt(w.A, w.B, N, nfields, g, ps);
-        ebcot_probe_reduce(w.A, w.x32, w.fs, w.prm, N, nfields, !early_p, w.res, ps);
+        probe_base(mj2, w.prm, w.B, w.eb.ll, g, nfields, w.norm, w.x32, w.fs, w.res, ps,
+                   nullptr, true, early_p);
         return;
       }
       probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32,
@@ -1126,8 +1131,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     ctl_residue(a0, s0);
     if (eb) {
       ebcot_probe_decode(egeo, *eb, w.prm, nfields, nfields, w.A, s0);
-      inverse_dwt(w.A, w.B, N, nfields, g, s0);
-      ebcot_residue(w.A, w.prm, N, nfields, w.base_dec, w.norm, s0);
+      base_to_residue(mj2, w.prm, w.B, w.eb.ll, g, nfields, w.norm, w.base_dec, w.norm, s0);
     } else {
       base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, s0);
     }

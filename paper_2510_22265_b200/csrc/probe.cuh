@@ -65,6 +65,10 @@ constexpr int64_t kMaxChunkPoints = (int64_t)0xfffffffe;
 struct Meta {  // one field = `stride` entries
   const uint2* packed;
   const uint8_t* rank_hi;  // wide chunks: rank bits 26..31 per coefficient (else null)
+  // non-null: the coefficients are this f64 pyramid (stride `stride`), not
+  // closed-form decodes of records (the opt-in J2 base layer's probes; the
+  // XE instantiations read it, like rank_hi)
+  const double* coef;
   const uint32_t* sprank;  // sign bit offset by LSP rank (kNone: sign not read)
   const PlaneRec* planes;
   const MachineOut* mo;
