@@ -106,7 +106,7 @@ def _gather_errors(err, group):
 
 
 def compress_shard(local_stack, dims, rel_error: float = 0.01, q: float = 1.0 - 1e-5,
-                   group=None, ctx=None, coder=None) -> bytes | None:
+                   group=None, ctx=None, coder=None, base_codec: str = "spiht") -> bytes | None:
     """Compress this rank's block of the default chunks of a ``dims`` grid.
 
     ``local_stack`` holds chunks ``shard_bounds(T*P, world, rank)`` (each an
@@ -144,7 +144,8 @@ def compress_shard(local_stack, dims, rel_error: float = 0.01, q: float = 1.0 - 
             recs, hpay, hoffs = coder(local)
             st = _lib.OK
         elif hi > lo:
-            recs, _, total, st = compress_batch(local, params, ctx, fetch=False)
+            recs, _, total, st = compress_batch(local, params, ctx, fetch=False,
+                                                base_codec=base_codec)
             if st == _lib.E_RESIDUAL:
                 i = lo + int(np.flatnonzero(recs["status"] == _lib.E_RESIDUAL)[0])
                 raise ResidualInsufficient(f"chunk at origin {(i // p, i % p, 0, 0)}: no "
@@ -184,7 +185,9 @@ def compress_shard(local_stack, dims, rel_error: float = 0.01, q: float = 1.0 - 
         ctx.fetch_container_into(None, r25, total, seg.ptr + start,
                                  int(rec_span[lo:hi].sum()), _lib.CONTAINER_BODY)
     if rank == 0:
-        seg.view[:42] = np.frombuffer(pack_header(dims, (1, 1, h, w), n), np.uint8)
+        from .container import VERSION, VERSION_EBCOT
+        version = VERSION_EBCOT if base_codec == "ebcot" else VERSION
+        seg.view[:42] = np.frombuffer(pack_header(dims, (1, 1, h, w), n, version), np.uint8)
     dist.barrier(group)
     out = seg.mm[:] if rank == 0 else None
     seg.close()
@@ -192,23 +195,26 @@ def compress_shard(local_stack, dims, rel_error: float = 0.01, q: float = 1.0 - 
 
 
 def compress(array, rel_error: float = 0.01, q: float = 1.0 - 1e-5, chunk_shape=None,
-             group=None) -> bytes | None:
+             group=None, base_codec: str = "spiht") -> bytes | None:
     """``paper_2510_22265_b200.compress`` over the ranks of ``group``: every
     rank passes the same (T, P, H, W) array (or a view of it; a rank reads
-    only its block); rank 0 returns the container, the others None."""
+    only its block); rank 0 returns the container, the others None.
+    ``base_codec="ebcot"``: the opt-in JPEG2000-style base layer (version 2)."""
     dist = _dist()
     data = np.asarray(array)
     dims = pad_dims(data.shape)
     if chunk_shape is not None and tuple(pad_dims(chunk_shape)) != (1, 1) + dims[2:]:
         from .api import compress as single
-        out = single(array, rel_error, q, chunk_shape) if dist.get_rank(group) == 0 else None
+        out = single(array, rel_error, q, chunk_shape, base_codec) \
+            if dist.get_rank(group) == 0 else None
         dist.barrier(group)
         return out
     if data.size == 0:
         grid_from_array(data)  # the reference's IngestError("empty input array")
     t, p, h, w = dims
     lo, hi = shard_bounds(t * p, dist.get_world_size(group), dist.get_rank(group))
-    return compress_shard(data.reshape(t * p, h, w)[lo:hi], dims, rel_error, q, group)
+    return compress_shard(data.reshape(t * p, h, w)[lo:hi], dims, rel_error, q, group,
+                          base_codec=base_codec)
 
 
 def decompress(buf, group=None) -> np.ndarray | None:

@@ -231,3 +231,17 @@ def test_ingest_error_precedes_shape_errors():
             grid_from_array(a[1], chunk_shape=(1, 0, 1, 1), check_finite=check)
     with pytest.raises(ArgumentError):
         grid_from_array(np.ones((2, 1, 1, 3, 4), np.float32), check_finite=False)
+
+
+def test_base_codec_argument_and_container_v2_header():
+    """base_codec is validated before any device work; a version-2 header
+    (the opt-in J2 base layer) parses like version 1."""
+    from paper_2510_22265_b200.container import VERSION_EBCOT, pack_header, parse
+    from paper_2510_22265_b200.errors import ArgumentError
+    from paper_2510_22265_b200.pipeline import compress_batch
+    from paper_2510_22265_b200.chunk import EbccParams
+    with pytest.raises(ArgumentError):
+        compress_batch(np.zeros((1, 4, 4), np.float32), EbccParams(0.01), base_codec="jpeg")
+    hdr = pack_header((0, 0, 0, 0), (1, 1, 1, 1), 0, VERSION_EBCOT)
+    assert hdr[4:6] == b"\x02\x00"
+    assert parse(hdr)[0] == (0, 0, 0, 0)
