@@ -2163,13 +2163,20 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
           if (used[bk]) CK(cudaEventSynchronize(c->ev_pbuf[bk]));
           uint8_t* hp = bk ? pinned_block(c->h_pay2, c->h_pay2_cap, span)
                            : pinned_block(c->h_pay, c->h_pay_cap, span);
-          parallel_memcpy(hp, psrc, (size_t)span);
-          psrc = hp;
+          // staged in 64 MiB pieces, each uploaded as soon as it is staged
+          // (the first batch's upload overlaps its own staging)
+          constexpr int64_t kPiece = 64ll << 20;
+          for (int64_t o = 0; o < span; o += kPiece) {
+            const int64_t len = std::min(kPiece, span - o);
+            parallel_memcpy(hp + o, psrc + o, (size_t)len);
+            CK(cudaMemcpyAsync(c->d_stage + o, hp + o, len, cudaMemcpyHostToDevice, st));
+          }
+        } else {
+          CK(cudaMemcpyAsync(c->d_stage, psrc, span,
+                             (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
+                                                            : cudaMemcpyHostToDevice,
+                             st));
         }
-        CK(cudaMemcpyAsync(c->d_stage, psrc, span,
-                           (flags & EBCC_INPUT_ON_DEVICE) ? cudaMemcpyDeviceToDevice
-                                                          : cudaMemcpyHostToDevice,
-                           st));
         CK(cudaEventRecord(c->ev_pbuf[bk], st));
         if ((int)up.size() > c->unpack_cap) {
           if (c->d_unpack) cudaFree(c->d_unpack);
