@@ -226,15 +226,22 @@ __device__ __forceinline__ int sig_ctx(int orient, int h, int v, int d) {
   return d >= 2 ? 2 : (d == 1 ? 1 : 0);
 }
 
-// one code-block's view of the per-sample state (pyramid positions)
+// one code-block's view of the per-sample state: words stripe-major (the 4
+// samples of a stripe column are one 8-byte word group); q / plow stay in
+// the pyramid layout (base, cols)
 struct Blk {
-  uint16_t* f;     // state words of the field, row stride `cols`
-  int64_t base;    // position of the block's (0, 0)
+  uint16_t* f;     // the block's state words
+  int64_t base;    // pyramid position of the block's (0, 0)
   int cols, h, w, orient;
-  __device__ __forceinline__ uint16_t& ref(int y, int x) const {
-    return f[base + (int64_t)y * cols + x];
+  __device__ __forceinline__ int64_t idx(int y, int x) const {
+    return ((int64_t)(y >> 2) * w + x) * 4 + (y & 3);
   }
+  __device__ __forceinline__ uint16_t& ref(int y, int x) const { return f[idx(y, x)]; }
   __device__ __forceinline__ int word(int y, int x) const { return ref(y, x); }
+  // the 4 words of stripe column (y0, x) (y0 a multiple of 4)
+  __device__ __forceinline__ uint2 column(int y0, int x) const {
+    return *reinterpret_cast<const uint2*>(f + idx(y0, x));
+  }
   __device__ __forceinline__ int sig_context(int wd) const {
     const int hh = ((wd >> NB_W) & 1) + ((wd >> NB_E) & 1);
     const int vv = ((wd >> NB_N) & 1) + ((wd >> NB_S) & 1);
@@ -317,6 +324,20 @@ __device__ void run_pass(const Blk& b, uint32_t* q, int8_t* plow, int p, int pty
   for (int y0 = 0; y0 < b.h; y0 += 4) {
     const int sh = b.h - y0 < 4 ? b.h - y0 : 4;
     for (int x = 0; x < b.w; x++) {
+      {  // nothing to code in this stripe column: skip it with one load
+        const uint2 cw = b.column(y0, x);
+        const uint32_t wds[4] = {cw.x & 0xFFFFu, cw.x >> 16, cw.y & 0xFFFFu, cw.y >> 16};
+        bool work = false;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          if (k >= sh) break;
+          const uint32_t wd = wds[k];
+          if (ptype == 0) work |= !(wd & F_SIG) && (wd & NSIG_MASK);
+          else if (ptype == 1) work |= (wd & F_SIG) && !(wd & F_VIS);
+          else work |= !(wd & (F_SIG | F_VIS));
+        }
+        if (!work) continue;
+      }
       int y = y0;
       if (ptype == 2 && sh == 4) {  // cleanup run mode
         bool run_ok = true;
@@ -426,7 +447,7 @@ __global__ void nmax_kernel(const double* __restrict__ coef, int64_t n, int32_t*
 }
 
 __global__ void quantize_kernel(const double* __restrict__ coef, int64_t n, const int32_t* nmax,
-                                uint32_t* qs, uint16_t* flags, const uint8_t* active) {
+                                uint32_t* qs, const uint8_t* active) {
   const int f = blockIdx.y;
   if (active && !active[f]) return;
   const int nm = nmax[f];
@@ -437,7 +458,6 @@ __global__ void quantize_kernel(const double* __restrict__ coef, int64_t n, cons
     uint32_t q = 0;
     if (nm != kExpNone) q = (uint32_t)floor(scalbn(fabs(c), -e0));
     qs[(int64_t)f * n + i] = q | (c < 0.0 ? 0x80000000u : 0u);
-    flags[(int64_t)f * n + i] = 0;  // (the sign is in qs until the sample turns significant)
   }
 }
 
@@ -449,7 +469,9 @@ __global__ void __launch_bounds__(64) t1_encode_kernel(EbGeo eg, int cols, EbBuf
   if (k >= eg.nb || (active && !active[f])) return;
   const EbBlock B = eg.blocks[k];
   uint32_t* q = b.qs + (int64_t)f * b.n;
-  Blk blk{b.flags + (int64_t)f * b.n, (int64_t)B.r0 * cols + B.c0, cols, B.h, B.w, B.orient};
+  Blk blk{b.flags + (int64_t)f * eg.state_stride + B.soff, (int64_t)B.r0 * cols + B.c0, cols,
+          B.h, B.w, B.orient};
+  for (int64_t i = 0; i < (int64_t)((B.h + 3) / 4) * 4 * B.w; i++) blk.f[i] = 0;
   uint32_t* uv = b.uval + ((int64_t)f * eg.nb + k) * kJ2Passes;
   for (int j = 0; j < kJ2Passes; j++) uv[j] = 0;
   if (b.nmax[f] == kExpNone) {
@@ -670,13 +692,14 @@ __global__ void __launch_bounds__(64) t1_decode_kernel(EbGeo eg, int cols, EbBuf
   const EbBlock B = eg.blocks[k];
   uint32_t* q = b.qs + (int64_t)f * b.n;
   int8_t* plow = b.plow + (int64_t)f * b.n;
-  Blk blk{b.flags + (int64_t)f * b.n, (int64_t)B.r0 * cols + B.c0, cols, B.h, B.w, B.orient};
+  Blk blk{b.flags + (int64_t)f * eg.state_stride + B.soff, (int64_t)B.r0 * cols + B.c0, cols,
+          B.h, B.w, B.orient};
+  for (int64_t i = 0; i < (int64_t)((B.h + 3) / 4) * 4 * B.w; i++) blk.f[i] = 0;
   for (int y = 0; y < B.h; y++)
     for (int x = 0; x < B.w; x++) {
       const int64_t i = blk.base + (int64_t)y * cols + x;
       q[i] = 0;
       plow[i] = -1;
-      blk.f[i] = 0;
     }
   const int nm = b.nmax[f];
   const uint8_t* body = b.body + (int64_t)f * b.body_stride;
@@ -708,12 +731,13 @@ __global__ void __launch_bounds__(64) t1_decode_kernel(EbGeo eg, int cols, EbBuf
   for (int y = 0; y < B.h; y++)
     for (int x = 0; x < B.w; x++) {
       const int64_t i = blk.base + (int64_t)y * cols + x;
+      const int wd = blk.word(y, x);
       double val = 0.0;
-      if (blk.f[i] & F_SIG) {
+      if (wd & F_SIG) {
         const int pl = plow[i];
         const uint32_t m = q[i] >> pl;
         val = scalbn((double)(2 * m + 1), pl - 1 + e0);
-        if (blk.f[i] & F_NEG) val = -val;
+        if (wd & F_NEG) val = -val;
       }
       o[i] = val;
     }
@@ -808,12 +832,14 @@ EbGeo ebcot_build_geo(const Geo& g, int32_t** blk_of_out, EbBlock** blocks_out, 
     for (int by = 0; by < h; by += kJ2Block)
       for (int bx = 0; bx < w; bx += kJ2Block)
         bl.push_back(EbBlock{r0 + by, c0 + bx, std::min(kJ2Block, h - by),
-                             std::min(kJ2Block, w - bx), orient, 0, 0});
+                             std::min(kJ2Block, w - bx), orient, 0, 0, 0});
   }
-  int64_t acc = 0;
+  int64_t acc = 0, sacc = 0;
   for (EbBlock& e : bl) {
     e.off = acc;
     acc += (int64_t)e.h * e.w;
+    e.soff = sacc;
+    sacc += (int64_t)((e.h + 3) / 4) * 4 * e.w;
   }
   std::vector<int32_t> of((size_t)g.n);
   for (int k = 0; k < (int)bl.size(); k++)
@@ -829,7 +855,7 @@ EbGeo ebcot_build_geo(const Geo& g, int32_t** blk_of_out, EbBlock** blocks_out, 
   cudaStreamSynchronize(st);
   *blk_of_out = dof;
   *blocks_out = db;
-  return EbGeo{(int)bl.size(), db, dof};
+  return EbGeo{(int)bl.size(), db, dof, sacc};
 }
 
 void ebcot_encode(const double* coef, const EbGeo& eg, const Geo& g, EbBufs& b,
@@ -837,7 +863,7 @@ void ebcot_encode(const double* coef, const EbGeo& eg, const Geo& g, EbBufs& b,
   const int nf = b.nfields;
   init_kernel<<<(nf + 255) / 256, 256, 0, st>>>(b.nmax, b.status, nf);
   nmax_kernel<<<dim3(grid_x(g.n), nf), 256, 0, st>>>(coef, g.n, b.nmax, active);
-  quantize_kernel<<<dim3(grid_x(g.n), nf), 256, 0, st>>>(coef, g.n, b.nmax, b.qs, b.flags, active);
+  quantize_kernel<<<dim3(grid_x(g.n), nf), 256, 0, st>>>(coef, g.n, b.nmax, b.qs, active);
   t1_encode_kernel<<<dim3((eg.nb + 63) / 64, nf), 64, 0, st>>>(eg, g.cols, b, active);
   assemble_kernel<<<nf, 1024, 0, st>>>(eg, g.cols, b, active);
 }

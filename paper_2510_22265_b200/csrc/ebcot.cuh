@@ -31,7 +31,8 @@ struct EbBlock {
   int r0, c0, h, w;
   int orient;  // 0 LL / LH, 1 HL (H and V swapped), 2 HH
   int pad;
-  int64_t off;  // samples of the blocks before it (its codeword scratch offset)
+  int64_t off;   // samples of the blocks before it (its codeword scratch offset)
+  int64_t soff;  // its tier-1 state words: stripe-major, ceil(h/4) * 4 * w
 };
 
 // geometry tables (one set per chunk shape)
@@ -39,6 +40,7 @@ struct EbGeo {
   int nb;                   // code-blocks
   const EbBlock* blocks;    // [nb]
   const int32_t* blk_of;    // [n] code-block of each pyramid position
+  int64_t state_stride;     // tier-1 state words per field (sum of the blocks' soff spans)
 };
 
 // per-batch buffers (all fields `n` coefficients apart)
@@ -46,7 +48,8 @@ struct EbBufs {
   int nfields;
   int64_t n;
   uint32_t* qs;        // [f][n] magnitude | significance-in-SP << 30 | negative << 31
-  uint16_t* flags;     // [f][n] tier-1 state word (own flags, neighbours' significance / signs)
+  uint16_t* flags;     // [f][state_stride] tier-1 state words (own flags, neighbours'
+                       // significance / signs), stripe-major per code-block
   int8_t* plow;        // [f][n] decoder: lowest decoded plane
   uint8_t* cw;         // [f][cw_stride] per-block codeword scratch
   int64_t cw_stride;   // n * kCwPerPoint + nb * kCwPerBlock bytes per field

@@ -854,7 +854,7 @@ EbBufs& ensure_ebcot(Workspace& w, int nfields, cudaStream_t st) {
     CK(cudaGetLastError());
     const int64_t N = w.g.n * (int64_t)w.cap, nb = e.geo.nb, cap = w.cap;
     e.b.qs = dalloc<uint32_t>(N);
-    e.b.flags = dalloc<uint16_t>(N);
+    e.b.flags = dalloc<uint16_t>(e.geo.state_stride * cap);
     e.b.plow = dalloc<int8_t>(N);
     e.b.cw_stride = w.g.n * kCwPerPoint + nb * kCwPerBlock;
     e.b.cw = dalloc<uint8_t>(cap * e.b.cw_stride);
