@@ -336,10 +336,11 @@ struct ebcc_ctx {
   // batch plans (chunks per device batch), cached per call shape so that
   // repeated calls neither query the free memory nor reallocate
   struct Plan {
-    int rows = 0, cols = 0, levels = 0, lanes = 0;
+    int rows = 0, cols = 0, levels = 0, lanes = 0, j2 = 0;
     int64_t nfields = -1, cap = 0;
-    bool matches(const Geo& g, int64_t nf, int l) const {
-      return rows == g.rows && cols == g.cols && levels == g.levels && nfields == nf && lanes == l;
+    bool matches(const Geo& g, int64_t nf, int l, int j = 0) const {
+      return rows == g.rows && cols == g.cols && levels == g.levels && nfields == nf && lanes == l &&
+             j2 == j;
     }
   } cplan, dplan;
 };
@@ -810,7 +811,8 @@ int64_t max_batch() {
 
 // chunks per batch: free-memory bound, queried only when the workspace does
 // not already cover the call (cudaMemGetInfo can stall for milliseconds)
-int64_t plan_batch(ebcc_ctx* c, const Geo& g, int64_t want, int lanes, bool tree);
+int64_t plan_batch(ebcc_ctx* c, const Geo& g, int64_t want, int lanes, bool tree,
+                   bool j2 = false);
 int64_t balance(int64_t n, int64_t cap);
 
 // feasibility-only probes may skip settled CTAs (EBCC_EARLY=0 disables)
@@ -850,6 +852,7 @@ void add_conditional(cudaStream_t st, cudaStream_t bst, cudaGraphConditionalHand
 EbBufs& ensure_ebcot(Workspace& w, int nfields, cudaStream_t st) {
   Workspace::EbSet& e = w.eb;
   if (!e.blocks) {
+    AllocScope acc(&w.bytes);  // (later batch plans see these bytes)
     e.geo = ebcot_build_geo(w.g, &e.blk_of, &e.blocks, st);
     CK(cudaGetLastError());
     const int64_t N = w.g.n * (int64_t)w.cap, nb = e.geo.nb, cap = w.cap;
@@ -1483,9 +1486,10 @@ int64_t per_field_bytes(const ebcc_ctx* c, const Geo& g) {
 // chunks each: 85% of (free HBM + what this tree's workspaces hold) minus a
 // 1 GiB reserve, split evenly.  `tree` = every lane's workspace may be
 // reallocated (compress); otherwise only c->ws (decompress).
-int64_t plan_batch(ebcc_ctx* c, const Geo& g, int64_t want, int lanes, bool tree) {
+int64_t plan_batch(ebcc_ctx* c, const Geo& g, int64_t want, int lanes, bool tree, bool j2) {
   want = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, 4096), max_batch()));
-  const int64_t pf = per_field_bytes(c, g);
+  // the opt-in J2 base layer's buffers (ensure_ebcot): ~24 B/pt + per-block tables
+  const int64_t pf = per_field_bytes(c, g) + (j2 ? g.n * 26 + (1 << 20) : 0);
   auto cap_now = [&]() {
     size_t freeb = 0, totalb = 0;
     CK(cudaMemGetInfo(&freeb, &totalb));
@@ -1813,10 +1817,11 @@ extern "C" int ebcc_compress(ebcc_ctx* c, const float* fields, int64_t nfields, 
       const int levels = clamp_levels(rows, cols, default_levels(rows, cols));
       const Geo g = make_geo(rows, cols, levels);
       for (int k = 0; k < (L > 1 ? L : 0); k++) lane_ctx(c, k);  // the tree the plan covers
-      if (!c->cplan.matches(g, nfields, L)) {
-        c->cplan.cap = plan_batch(c, g, (nfields + L - 1) / L, L, true);
+      const int j2 = (flags & EBCC_BASE_EBCOT) ? 1 : 0;
+      if (!c->cplan.matches(g, nfields, L, j2)) {
+        c->cplan.cap = plan_batch(c, g, (nfields + L - 1) / L, L, true, j2 != 0);
         c->cplan.rows = g.rows; c->cplan.cols = g.cols; c->cplan.levels = g.levels;
-        c->cplan.nfields = nfields; c->cplan.lanes = L;
+        c->cplan.nfields = nfields; c->cplan.lanes = L; c->cplan.j2 = j2;
       }
     }
     const int64_t plan_cap = c->cplan.cap;
@@ -2052,10 +2057,23 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         if (!c->lanes.empty()) std::swap(c->ws, c->lanes[0]->ws);
       }
     } lane_ws(c);
-    if (!c->dplan.matches(g, nfields, 1)) {
-      c->dplan.cap = plan_batch(c, g, nfields, 1, false);
+    // J2 base streams (the opt-in layer) need the ebcot buffers: the first
+    // stream's magic decides the plan
+    int j2_plan = 0;
+    for (int64_t i = 0; i < nfields; i++) {
+      if (recs[i].mode == EBCC_MODE_CONSTANT || recs[i].base_len < 2) continue;
+      uint8_t mg[2] = {0, 0};
+      if (flags & EBCC_INPUT_ON_DEVICE)
+        CK(cudaMemcpy(mg, payload + offsets[i], 2, cudaMemcpyDeviceToHost));
+      else
+        memcpy(mg, payload + offsets[i], 2);
+      j2_plan = mg[0] == 'J' && mg[1] == '2';
+      break;
+    }
+    if (!c->dplan.matches(g, nfields, 1, j2_plan)) {
+      c->dplan.cap = plan_batch(c, g, nfields, 1, false, j2_plan != 0);
       c->dplan.rows = g.rows; c->dplan.cols = g.cols; c->dplan.levels = g.levels;
-      c->dplan.nfields = nfields; c->dplan.lanes = 1;
+      c->dplan.nfields = nfields; c->dplan.lanes = 1; c->dplan.j2 = j2_plan;
     }
     const int64_t cap = balance(nfields, c->dplan.cap);
     g_slow.mark("dec_meminfo");
