@@ -17,6 +17,8 @@ namespace ebcc {
 namespace {
 
 constexpr int kBasePlanes = 24, kDeepPlanes = 32;
+static_assert(sizeof(CtlChunk) * kCtlSmemChunks <= 227 * 1024, "staged states exceed shared memory");
+static_assert(sizeof(CtlChunk) % 8 == 0, "staged as 8-byte words");
 constexpr int kSuspend = 1, kDone = 0;
 
 // CPython float floor division (Objects/floatobject.c float_divmod), as
@@ -71,6 +73,25 @@ __device__ __forceinline__ int memo_find(const CtlChunk& s, int64_t b) {
     if (s.memo[i].budget == b) return i;
   return -1;
 }
+__device__ __forceinline__ int smemo_find(const CtlChunk& s, int64_t b) {
+  for (int i = 0; i < s.nsmemo; i++)
+    if (s.smemo[i].budget == b) return i;
+  return -1;
+}
+// the memo entry of budget b; a speculative answer moves into the memo when
+// the search asks for its budget (the reference's probe at that point)
+__device__ int memo_get(CtlChunk& s, int64_t b) {
+  const int i = memo_find(s, b);
+  if (i >= 0) return i;
+  const int j = smemo_find(s, b);
+  if (j < 0) return -1;
+  if (s.nmemo >= kCtlMemo) {
+    s.status |= kCtlCapacity;
+    return -1;
+  }
+  s.memo[s.nmemo] = s.smemo[j];
+  return s.nmemo++;
+}
 __device__ __forceinline__ double q_of(const CtlChunk& s, int i) {
   return __ddiv_rn((double)s.memo[i].count, (double)s.n);
 }
@@ -85,13 +106,73 @@ __device__ __forceinline__ int tmemo_find(const CtlChunk& s, int pi, int64_t t) 
 
 // ---- _search_base (pipeline.py:142-199) -------------------------------------
 // s.want_b / s.cur_b: the key and memo index of the access in progress
+// (a suspension also sets s.bspec: the keys the next step asks whichever way
+// this probe answers, for the speculative slots)
 #define CTL_GET_B(KEY, LABEL)                           \
   s.want_b = (KEY);                                     \
   case LABEL:                                           \
-    if ((s.cur_b = memo_find(s, s.want_b)) < 0) {       \
+    if ((s.cur_b = memo_get(s, s.want_b)) < 0) {        \
       s.pc_b = LABEL;                                   \
+      base_spec(s, LABEL);                              \
       return kSuspend;                                  \
     }
+
+// first step of the byte-exact refinement (pipeline.py:193-198 seeding, then
+// _bisect_min_feasible) if the memo also held budget b with feasibility feas
+// (-1: the bracket is already closed)
+__device__ int64_t refine_first(const CtlChunk& s, int64_t b, bool feas) {
+  int64_t hi = -1, lo = kHeader - 1;
+  for (int i = 0; i < s.nmemo; i++)
+    if (q_of(s, i) >= s.q && (hi < 0 || s.memo[i].budget < hi)) hi = s.memo[i].budget;
+  if (feas && (hi < 0 || b < hi)) hi = b;
+  for (int i = 0; i < s.nmemo; i++)
+    if (q_of(s, i) < s.q && s.memo[i].budget < hi && s.memo[i].budget > lo) lo = s.memo[i].budget;
+  if (!feas && b < hi && b > lo) lo = b;
+  return hi - lo > 1 ? clamp_budget(s, (lo + hi) / 2) : -1;
+}
+// the ratio bisection's next key on [lo, hi], or the refinement's first
+__device__ int64_t ratio_step(const CtlChunk& s, double lo, double hi, int64_t b, bool feas) {
+  if (__dsub_rn(hi, lo) > s.tol) return ratio_budget(s, __dmul_rn(0.5, __dadd_rn(lo, hi)));
+  return refine_first(s, b, feas);
+}
+// keys of the base search's next access for each answer of the probe at
+// s.want_b (the code below, label by label; infeasible first)
+__device__ void base_spec(CtlChunk& s, int label) {
+  const int64_t b = s.want_b;
+  int64_t k0 = -1, k1 = -1;
+  switch (label) {
+    case 1:  // r0: halve r_low / double r_high
+      if (s.r0c > 1.0) k0 = ratio_budget(s, fmax(1.0, __ddiv_rn(s.r0c, 2.0)));
+      k1 = s.r0c < s.r_cap ? ratio_budget(s, fmin(s.r_cap, __dmul_rn(s.r0c, 2.0)))
+                           : ratio_step(s, s.r0c, s.r0c, b, true);
+      break;
+    case 2:  // r_low: halve again / bisect [r_low, r_high]
+      if (s.r_low > 1.0) k0 = ratio_budget(s, fmax(1.0, __ddiv_rn(s.r_low, 2.0)));
+      k1 = ratio_step(s, s.r_low, s.r_high, b, true);
+      break;
+    case 5:  // r_high: double again / bisect
+      if (s.r_high < s.r_cap) {
+        k1 = ratio_budget(s, fmin(s.r_cap, __dmul_rn(s.r_high, 2.0)));
+        k0 = ratio_step(s, s.r_low, s.r_high, b, false);
+      } else {
+        k0 = ratio_step(s, s.r_low, s.r_high, b, false);
+        k1 = ratio_step(s, s.r_low, s.r_high, b, true);
+      }
+      break;
+    case 6:  // ratio bisection
+      k0 = ratio_step(s, s.r_low, s.r_mid, b, false);
+      k1 = ratio_step(s, s.r_mid, s.r_high, b, true);
+      break;
+    case 7:  // byte bisection
+      if (s.hi_b - s.mid_b > 1) k0 = clamp_budget(s, (s.mid_b + s.hi_b) / 2);
+      if (s.mid_b - s.lo_b > 1) k1 = clamp_budget(s, (s.lo_b + s.mid_b) / 2);
+      break;
+    default:
+      break;
+  }
+  s.bspec[0] = k0;
+  s.bspec[1] = k1;
+}
 
 __device__ int adv_base(CtlChunk& s) {
   switch (s.pc_b) {
@@ -167,10 +248,42 @@ __device__ int adv_base(CtlChunk& s) {
 #define CTL_GET_P(KEY, LABEL)                           \
   s.want_p = (KEY);                                     \
   case LABEL:                                           \
-    if ((s.cur_p = memo_find(s, s.want_p)) < 0) {       \
+    if ((s.cur_p = memo_get(s, s.want_p)) < 0) {        \
       s.pc_p = LABEL;                                   \
+      pure_spec(s, LABEL);                              \
       return kSuspend;                                  \
     }
+
+// the pure-base bisection's first key after the bracket is seeded from the
+// memo (the entries at kHeader and raw do not move it)
+__device__ int64_t pure_first(const CtlChunk& s) {
+  int64_t lo = kHeader, hi = s.raw;
+  for (int i = 0; i < s.nmemo; i++)
+    if (pure_ok_at(s, i) && s.memo[i].budget < hi) hi = s.memo[i].budget;
+  for (int i = 0; i < s.nmemo; i++)
+    if (s.memo[i].budget < hi && !pure_ok_at(s, i) && s.memo[i].budget > lo) lo = s.memo[i].budget;
+  return hi - lo > 1 ? clamp_budget(s, (lo + hi) / 2) : -1;
+}
+__device__ void pure_spec(CtlChunk& s, int label) {
+  int64_t k0 = -1, k1 = -1;
+  switch (label) {
+    case 1:
+      k0 = clamp_budget(s, s.raw);
+      k1 = pure_first(s);
+      break;
+    case 2:
+      k0 = pure_first(s);
+      break;
+    case 3:
+      if (s.hi_p - s.mid_p > 1) k0 = clamp_budget(s, (s.mid_p + s.hi_p) / 2);
+      if (s.mid_p - s.lo_p > 1) k1 = clamp_budget(s, (s.lo_p + s.mid_p) / 2);
+      break;
+    default:
+      break;
+  }
+  s.bspec[0] = k0;
+  s.bspec[1] = k1;
+}
 
 __device__ int adv_pure(CtlChunk& s) {
   switch (s.pc_p) {
@@ -320,18 +433,47 @@ __device__ int n_last_of(const MachineOut& mo, const PlaneRec* pl, int planes, u
 // counted: a base-search probe (its count field holds violations; a probe
 // that stopped early reported more than vlim of them, so the count stored
 // here is below the threshold exactly when the full count would be)
+__device__ CtlEntry make_entry(const CtlChunk& s, int64_t b, const ProbeResult& r, bool counted) {
+  double e;
+  unsigned long long bits = r.maxerr;
+  memcpy(&e, &bits, 8);
+  const unsigned long long v = r.count;
+  const unsigned long long hits = !counted ? 0ull : (v >= (unsigned long long)s.n ? 0ull : (unsigned long long)s.n - v);
+  return CtlEntry{b, hits, e};
+}
 __device__ void memo_add(CtlChunk& s, int64_t b, const ProbeResult& r, bool counted) {
   if (memo_find(s, b) >= 0) return;
   if (s.nmemo >= kCtlMemo) {
     s.status |= kCtlCapacity;
     return;
   }
-  double e;
-  unsigned long long bits = r.maxerr;
-  memcpy(&e, &bits, 8);
-  const unsigned long long v = r.count;
-  const unsigned long long hits = !counted ? 0ull : (v >= (unsigned long long)s.n ? 0ull : (unsigned long long)s.n - v);
-  s.memo[s.nmemo++] = CtlEntry{b, hits, e};
+  s.memo[s.nmemo++] = make_entry(s, b, r, counted);
+}
+// a speculative answer (dropped when the side memo is full: the search then
+// probes that budget itself)
+__device__ void smemo_add(CtlChunk& s, int64_t b, const ProbeResult& r, bool counted) {
+  if (memo_find(s, b) >= 0 || smemo_find(s, b) >= 0 || s.nsmemo >= kCtlSMemo) return;
+  s.smemo[s.nsmemo++] = make_entry(s, b, r, counted);
+}
+// the speculative slots' requests for the access in flight at key `want`
+template <class Req>
+__device__ void post_spec(CtlChunk& s, int bslots, int64_t want, ProbeParam* ps, Req req) {
+  for (int k = 1; k < bslots; k++) {
+    const int64_t b2 = s.bspec[k - 1];
+    s.bspend[k - 1] = -1;
+    if (b2 < 0 || b2 == want || (k == 2 && b2 == s.bspec[0]) || memo_find(s, b2) >= 0 ||
+        smemo_find(s, b2) >= 0)
+      continue;
+    s.bspend[k - 1] = b2;
+    ps[k] = req(b2);
+  }
+}
+// park the speculative slots' answers
+__device__ void ingest_spec(CtlChunk& s, const CtlArgs& a, int f, bool counted) {
+  for (int k = 1; k < a.bslots; k++) {
+    if (s.bspend[k - 1] >= 0) smemo_add(s, s.bspend[k - 1], a.res[k * a.nfields + f], counted);
+    s.bspend[k - 1] = -1;
+  }
 }
 __device__ void tmemo_add(CtlChunk& s, int pi, int64_t t, const ProbeResult& r) {
   if (tmemo_find(s, pi, t) >= 0) return;
@@ -395,6 +537,28 @@ __device__ ProbeParam trunc_request(const CtlChunk& s, const CtlArgs& a, int f, 
 // the controller is one CTA; `any` is or-reduced over it
 __device__ __forceinline__ bool block_any(bool v) { return __syncthreads_or(v) != 0; }
 
+// Few chunks: their states are staged through shared memory, so the one
+// thread advancing a chunk pays shared-memory latency instead of a chain of
+// dependent L2 misses (cold L1 at every launch).
+extern __shared__ __align__(16) unsigned char ctl_sm[];
+__device__ CtlChunk* stage_in(const CtlArgs& a) {
+  if (!a.smem) return a.cs;
+  const size_t words = sizeof(CtlChunk) / 8 * (size_t)a.nfields;
+  const uint64_t* src = reinterpret_cast<const uint64_t*>(a.cs);
+  uint64_t* dst = reinterpret_cast<uint64_t*>(ctl_sm);
+  for (size_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  __syncthreads();
+  return reinterpret_cast<CtlChunk*>(ctl_sm);
+}
+__device__ void stage_out(const CtlArgs& a) {
+  if (!a.smem) return;
+  __syncthreads();
+  const size_t words = sizeof(CtlChunk) / 8 * (size_t)a.nfields;
+  const uint64_t* src = reinterpret_cast<const uint64_t*>(ctl_sm);
+  uint64_t* dst = reinterpret_cast<uint64_t*>(a.cs);
+  for (size_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
+
 __global__ void __launch_bounds__(1024) ctl_setup_kernel(CtlArgs a) {
   const CtlParams P = *a.prm_in;
   for (int f = threadIdx.x; f < a.nfields; f += blockDim.x) {
@@ -435,6 +599,9 @@ __global__ void __launch_bounds__(1024) ctl_setup_kernel(CtlArgs a) {
     s.tpend_pi = 0;
     s.eb_cum = nullptr;
     s.eb_sub = s.eb_nslot = 0;
+    s.nsmemo = 0;
+    s.bspec[0] = s.bspec[1] = -1;
+    for (int k = 0; k + 1 < kCtlSlots; k++) s.bspend[k] = -1;
   }
   if (threadIdx.x == 0) *a.stats = CtlStats{};
 }
@@ -442,9 +609,11 @@ __global__ void __launch_bounds__(1024) ctl_setup_kernel(CtlArgs a) {
 __global__ void __launch_bounds__(1024) ctl_base_kernel(CtlArgs a, int start, int set) {
   const bool early = a.prm_in->early != 0;
   bool any = false;
-  for (int f = threadIdx.x; f < a.nfields; f += blockDim.x) {
-    CtlChunk& s = a.cs[f];
-    ProbeParam p{};
+  CtlChunk* cs = stage_in(a);
+  const int nf = a.nfields;
+  for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+    CtlChunk& s = cs[f];
+    ProbeParam p[kCtlSlots] = {};
     if (s.active) {
       if (start) {
         s.T_base = a.mo_base[f].total_bits;
@@ -459,16 +628,21 @@ __global__ void __launch_bounds__(1024) ctl_base_kernel(CtlArgs a, int start, in
         memo_add(s, s.pend_budget, a.res[f], true);
         s.pend = 0;
       }
+      ingest_spec(s, a, f, true);
       if (!s.done_b && !(s.status & kCtlCapacity) && adv_base(s) == kSuspend) {
         s.pend = 1;
         s.pend_budget = s.want_b;
-        p = base_request(s, s.want_b, early);
+        p[0] = base_request(s, s.want_b, early);
+        post_spec(s, a.bslots, s.want_b, p, [&](int64_t b) { return base_request(s, b, early); });
         any = true;
       }
     }
-    a.res[f] = ProbeResult{};
-    a.prm[f] = p;
+    for (int k = 0; k < a.bslots; k++) {
+      a.res[k * nf + f] = ProbeResult{};
+      a.prm[k * nf + f] = p[k];
+    }
   }
+  stage_out(a);
   any = block_any(any);
   if (threadIdx.x == 0) {
     if (set & 1) cudaGraphSetConditional(a.h_loop, any ? 1u : 0u);
@@ -501,31 +675,40 @@ __global__ void __launch_bounds__(1024) ctl_joint_kernel(CtlArgs a, int start, i
         s.T32 = mo.total_bits;
         s.T24 = a.pl_res[(int64_t)f * kMaxPlaneRecs + kBasePlanes].start;
       }
-      s.pend = 0;
+      // (a pure-base probe may be in flight: the joint loop ingests it)
       for (int k = 0; k < kCtlSlots; k++) s.tpend[k] = -1;
     }
     return;
   }
+  CtlChunk* cs = stage_in(a);
   for (int f = threadIdx.x; f < nf; f += blockDim.x) {
-    CtlChunk& s = a.cs[f];
-    ProbeParam pp{};
+    CtlChunk& s = cs[f];
+    ProbeParam pp[kCtlSlots] = {};
     ProbeParam tp[kCtlSlots] = {};
+    const bool do_p = a.jmode & 1, do_t = a.jmode & 2;
     if (s.active) {
-      if (s.pend) {
-        memo_add(s, s.pend_budget, a.res[f], false);
-        s.pend = 0;
+      if (do_p) {
+        if (s.pend) {
+          memo_add(s, s.pend_budget, a.res[f], false);
+          s.pend = 0;
+        }
+        ingest_spec(s, a, f, false);
       }
-      for (int k = 0; k < a.slots; k++)
-        if (s.tpend[k] >= 0) tmemo_add(s, s.tpend_pi, s.tpend[k], a.tres[k * nf + f]);
-      for (int k = 0; k < kCtlSlots; k++) s.tpend[k] = -1;
+      if (do_t) {
+        for (int k = 0; k < a.slots; k++)
+          if (s.tpend[k] >= 0) tmemo_add(s, s.tpend_pi, s.tpend[k], a.tres[k * nf + f]);
+        for (int k = 0; k < kCtlSlots; k++) s.tpend[k] = -1;
+      }
       bool p_open = false, t_open = false;
-      if (!s.done_p && !(s.status & kCtlCapacity) && adv_pure(s) == kSuspend) {
+      if (do_p && !s.done_p && !(s.status & kCtlCapacity) && adv_pure(s) == kSuspend) {
         s.pend = 1;
         s.pend_budget = s.want_p;
-        pp = base_request(s, s.want_p, P.early != 0);
+        pp[0] = base_request(s, s.want_p, P.early != 0);
+        post_spec(s, a.bslots, s.want_p, pp,
+                  [&](int64_t b) { return base_request(s, b, P.early != 0); });
         p_open = true;
       }
-      if (!s.done_t && !(s.status & kCtlCapacity) && adv_trunc(s) == kSuspend) {
+      if (do_t && !s.done_t && !(s.status & kCtlCapacity) && adv_trunc(s) == kSuspend) {
         s.tpend_pi = s.pass;
         s.tpend[0] = s.want_t;
         tp[0] = trunc_request(s, a, f, s.pass, s.want_t, P.early != 0);
@@ -554,7 +737,8 @@ __global__ void __launch_bounds__(1024) ctl_joint_kernel(CtlArgs a, int start, i
           s.pure_budget = -1;
           s.pure_pruned = 1;
           s.pend = 0;
-          pp = ProbeParam{};
+          for (int k = 0; k < kCtlSlots; k++) pp[k] = ProbeParam{};
+          for (int k = 0; k + 1 < kCtlSlots; k++) s.bspend[k] = -1;
           p_open = false;
         } else if (t_open && pure_ub >= 0 && two_lb >= pure_ub) {
           s.done_t = 1;  // pure-base is no longer (ties go to pure-base)
@@ -571,17 +755,24 @@ __global__ void __launch_bounds__(1024) ctl_joint_kernel(CtlArgs a, int start, i
       anyp |= p_open;
       anyt |= t_open;
     }
-    a.prm[f] = pp;
-    a.res[f] = ProbeResult{};
-    for (int k = 0; k < a.slots; k++) {
+    for (int k = 0; do_p && k < a.bslots; k++) {
+      a.prm[k * nf + f] = pp[k];
+      a.res[k * nf + f] = ProbeResult{};
+    }
+    for (int k = 0; do_t && k < a.slots; k++) {
       a.tprm[k * nf + f] = tp[k];
       a.tres[k * nf + f] = ProbeResult{};
     }
   }
+  stage_out(a);
   anyp = block_any(anyp);
   anyt = block_any(anyt);
   if (threadIdx.x == 0) {
-    if (set & 1) cudaGraphSetConditional(a.h_loop, (anyp || anyt) ? 1u : 0u);
+    bool loop = anyp || anyt;
+    // the pure-only loop stops once the residual is encoded; its last posted
+    // probes still run (h_pure), and the joint loop ingests them
+    if (a.jmode == 1 && *reinterpret_cast<volatile unsigned long long*>(&a.stats->stop)) loop = false;
+    if (set & 1) cudaGraphSetConditional(a.h_loop, loop ? 1u : 0u);
     if (set & 2) cudaGraphSetConditional(a.h_pure, anyp ? 1u : 0u);
     if (set & 4) cudaGraphSetConditional(a.h_trunc, anyt ? 1u : 0u);
     a.stats->joint_steps++;
@@ -618,20 +809,34 @@ inline int ctl_threads(int nfields) {
   while (t < nfields && t < 1024) t *= 2;
   return t;
 }
+// staged launches: more threads for the copies, the states' bytes of smem
+inline int ctl_threads(const CtlArgs& a) { return a.smem ? 256 : ctl_threads(a.nfields); }
+inline size_t ctl_smem(const CtlArgs& a) { return a.smem ? sizeof(CtlChunk) * a.nfields : 0; }
+void ctl_smem_init() {
+  static bool done = false;
+  if (done) return;
+  const int bytes = (int)(sizeof(CtlChunk) * kCtlSmemChunks);
+  cudaFuncSetAttribute(ctl_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(ctl_joint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done = true;
+}
 
 }  // namespace
 
 void ctl_setup(const CtlArgs& a, cudaStream_t st) {
   ctl_setup_kernel<<<1, ctl_threads(a.nfields), 0, st>>>(a);
 }
+bool ctl_smem_ok(int nfields) { return nfields <= kCtlSmemChunks; }
 void ctl_base(const CtlArgs& a, bool start, int set, cudaStream_t st) {
-  ctl_base_kernel<<<1, ctl_threads(a.nfields), 0, st>>>(a, start ? 1 : 0, set);
+  ctl_smem_init();
+  ctl_base_kernel<<<1, ctl_threads(a), ctl_smem(a), st>>>(a, start ? 1 : 0, set);
 }
 void ctl_residue(const CtlArgs& a, cudaStream_t st) {
   ctl_residue_kernel<<<1, ctl_threads(a.nfields), 0, st>>>(a);
 }
 void ctl_joint(const CtlArgs& a, bool start, int set, cudaStream_t st) {
-  ctl_joint_kernel<<<1, ctl_threads(a.nfields), 0, st>>>(a, start ? 1 : 0, set);
+  ctl_smem_init();
+  ctl_joint_kernel<<<1, ctl_threads(a), start ? 0 : ctl_smem(a), st>>>(a, start ? 1 : 0, set);
 }
 void ctl_finalize(const CtlArgs& a, cudaStream_t st) {
   ctl_finalize_kernel<<<1, ctl_threads(a.nfields), 0, st>>>(a);

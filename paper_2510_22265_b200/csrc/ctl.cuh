@@ -26,7 +26,9 @@ namespace ebcc {
 
 constexpr int kCtlMemo = 256;    // distinct base budgets per chunk
 constexpr int kCtlTMemo = 160;   // truncation offsets per planes variant
-constexpr int kCtlSlots = 3;     // truncation probes per chunk and step
+constexpr int kCtlSlots = 3;     // probes per chunk and step of each search
+constexpr int kCtlSMemo = 64;    // speculative base-memo entries per chunk
+constexpr int kCtlSmemChunks = 12;  // chunk states a controller CTA stages in shared memory
 
 struct CtlEntry {
   int64_t budget;
@@ -57,6 +59,14 @@ struct CtlChunk {
   int32_t nmemo, pend;   // pend: memo budget of the probe in flight (-1 none)
   int64_t pend_budget;
   CtlEntry memo[kCtlMemo];
+  // speculative base-memo probes (the budgets the base / pure-base search
+  // asks next whichever way the probe in flight answers): answers park here
+  // and move into `memo` only when the search asks for that budget, so the
+  // memo always holds exactly the reference's entries
+  int64_t bspec[2];                // next-step keys of the access in progress (-1 none)
+  int64_t bspend[kCtlSlots - 1];   // their probes in flight (-1 none)
+  int32_t nsmemo, pad_s;
+  CtlEntry smemo[kCtlSMemo];
   // --- the access each coroutine is at: key and memo index ---
   int64_t want_b, want_p, want_t;
   int32_t cur_b, cur_p, cur_t, pad1;
@@ -104,6 +114,9 @@ struct CtlParams {
 // counters of one batch (instrumentation)
 struct CtlStats {  // controller steps, and steps that launched probes of each kind
   unsigned long long base_steps, joint_steps, base_probes, pure_probes, trunc_probes;
+  // nonzero once the residual encode has finished: a pure-base loop running
+  // beside it hands its (suspended) search to the joint loop
+  unsigned long long stop;
 };
 
 struct CtlArgs {
@@ -116,12 +129,15 @@ struct CtlArgs {
   MachineOut* mo_res;
   const PlaneRec* pl_res;
   uint8_t* active;
-  ProbeParam* prm;        // base-stream probes (nfields)
+  ProbeParam* prm;        // base-stream probes (bslots x nfields, probe v -> chunk v % nfields)
   ProbeResult* res;
   ProbeParam* tprm;       // truncation probes (slots x nfields, probe v -> chunk v % nfields)
   ProbeResult* tres;
   int nfields;
-  int slots;
+  int slots;              // truncation probe slots
+  int bslots;             // base-stream probe slots (1: no speculation)
+  int smem;               // the chunks' states fit the controller CTA's shared memory
+  int jmode;              // ctl_joint advances: 1 the pure-base search, 2 truncation, 3 both
   int64_t n;
   cudaGraphConditionalHandle h_loop;   // WHILE condition of the current loop
   cudaGraphConditionalHandle h_pure;   // IF: the pure-base branch has probes
@@ -133,6 +149,8 @@ struct CtlArgs {
   int eb_nb;
 };
 
+// CtlArgs::smem may be set (the states fit the controller's shared memory)
+bool ctl_smem_ok(int nfields);
 // active flags, machine-output init and controller state of every chunk
 void ctl_setup(const CtlArgs& a, cudaStream_t st);
 // `set` selects the conditional handles a launch writes: 1 h_loop, 2 h_pure,
@@ -143,7 +161,10 @@ void ctl_base(const CtlArgs& a, bool start, int set, cudaStream_t st);
 // ProbeParam of the chosen base budget for base_to_residue
 void ctl_residue(const CtlArgs& a, cudaStream_t st);
 // pure-base + truncation searches: start = T24 / T32 only; otherwise ingest
-// + advance both + candidate pruning + post
+// + advance the searches `jmode` selects + candidate pruning + post.  A
+// pure-only loop (jmode 1) may run beside the residual encode: it touches no
+// truncation state, and its answer is never pruned (the truncation search,
+// run after it, is pruned against it)
 void ctl_joint(const CtlArgs& a, bool start, int set, cudaStream_t st);
 // candidate-choice inputs of every chunk into CtlOut
 void ctl_finalize(const CtlArgs& a, cudaStream_t st);

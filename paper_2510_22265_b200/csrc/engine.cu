@@ -131,12 +131,24 @@ bool is_pageable(const void* p) {
 // truncation probes per chunk and step: the bisection's next midpoint plus
 // the two points one level further (one of which the next step needs)
 constexpr int kTruncSlots = kCtlSlots;
+// batches up to this many points speculate (slots beside each bisection
+// midpoint): the GPU has slack at that size
+constexpr int64_t kSpecPoints = 8ll << 20;
+// ... and up to these the base / pure-base searches speculate too (measured:
+// 1 or 2 fields of 721 x 1440 gain, 4 lose), and the pure-base search runs
+// beside the residual encode (1 field gains, 2 lose)
+constexpr int64_t kSpecBasePoints = 5ll << 19;
+constexpr int64_t kSplitPoints = 5ll << 18;
 struct IngestFail {};
 
 // ---------------------------------------------------------------------------
 struct Workspace {
   Geo g{};
   int cap = 0;  // fields
+  // batches of at most spec_cap fields run kCtlSlots base-stream probes per
+  // step (speculation); the base probe slots are sized for np0 probes
+  int spec_cap = 0;
+  int64_t np0 = 0;
   int64_t bytes = 0;  // device bytes held (allocations counted by AllocScope)
   float* x32 = nullptr;
   double *norm = nullptr, *A = nullptr, *B = nullptr, *base_dec = nullptr;
@@ -195,8 +207,6 @@ struct Workspace {
     double* ll = nullptr;  // second LL buffer of the fused probe levels (with B)
   } eb;
   // pinned host mirrors of the per-step control arrays
-  ProbeParam* h_prm = nullptr;
-  ProbeResult* h_res = nullptr;
   TreeTables tt{};
   bool has_tt = false;
   // device controller (ctl.cuh): per-chunk search state, results, params
@@ -243,8 +253,6 @@ struct Workspace {
                   dec2.lis0, dec2.lis1, dec2.w0, dec2.w1, dec2.limit, dec2.active};
     for (void* p : d2)
       if (p) cudaFree(p);
-    if (h_prm) cudaFreeHost(h_prm);
-    if (h_res) cudaFreeHost(h_res);
     if (has_tt) free_tree_tables(tt);
     void* ebp[] = {eb.b.qs, eb.b.flags, eb.b.plow, eb.b.cw, eb.b.uval, eb.b.uoff, eb.b.ztab,
                    eb.b.cum, eb.b.nmax, eb.b.status, eb.blk_of, eb.blocks, eb.body_len, eb.ll};
@@ -322,11 +330,12 @@ struct ebcc_ctx {
   cudaEvent_t ev_in = nullptr;   // lanes: this lane's input copy has landed (CopyChain)
   std::vector<cudaEvent_t> ev_groups;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+  cudaEvent_t ph[5] = {};  // EBCC_PROFILE=1: search-graph phase marks
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr;  // fork/join of the joint probe step
   cudaEvent_t cev0 = nullptr, cev1 = nullptr;    // per-call timing (batch loop)
   cudaEvent_t oev0 = nullptr, oev1 = nullptr;    // per-call timing (ebcc_compress)
   cudaEvent_t tm_a = nullptr, tm_b = nullptr;
-  cudaStream_t cap[5] = {};      // graph capture streams (created on first use)
+  cudaStream_t cap[6] = {};      // graph capture streams (created on first use)
   cudaEvent_t tev[2] = {};       // base-encode timing
   cudaStream_t join = nullptr;   // caller's default stream the library stream follows
   cudaEvent_t ev_join = nullptr;
@@ -438,19 +447,22 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields, int want = 0) {
   w.mo_base = dalloc<MachineOut>(cap);
   w.mo_res = dalloc<MachineOut>(cap);
   w.fs = dalloc<FieldScal>(cap);
-  // two parameter/result slots: pure-base probes and truncation probes
-  w.tq_base = dalloc<uint8_t>((size_t)kTqBytes * cap);
+  w.spec_cap = (int)std::min<int64_t>(cap, std::max<int64_t>(1, kSpecPoints / g.n));
+  w.np0 = std::max<int64_t>(cap, (int64_t)kCtlSlots * w.spec_cap);
+  // per-probe decode tables: base-stream probes, truncation probes
+  w.tq_base = dalloc<uint8_t>((size_t)kTqBytes * w.np0);
   w.tq_res = dalloc<uint8_t>((size_t)kTqBytes * kTruncSlots * cap);
-  // parameter/result slots: base-stream probes, then kTruncSlots x truncation probes
-  w.prm = dalloc<ProbeParam>((1 + kTruncSlots) * (size_t)cap);
-  w.res = dalloc<ProbeResult>((1 + kTruncSlots) * (size_t)cap);
+  // parameter/result slots: np0 base-stream probes, then kTruncSlots x cap
+  // truncation probes
+  w.prm = dalloc<ProbeParam>(w.np0 + kTruncSlots * (size_t)cap);
+  w.res = dalloc<ProbeResult>(w.np0 + kTruncSlots * (size_t)cap);
   w.limit = dalloc<uint64_t>(cap);
   w.active = dalloc<uint8_t>(cap);
   w.mm = dalloc<unsigned int>(4 * cap + 2);
   inc_capacity(g, &w.inc_tiles, &w.inc_tiles0);
   w.inc_lstride = g.levels > 1 ? (int64_t)g.lr[1] * g.cols : 1;
   for (int i = 0; i < 2; i++) {
-    const size_t np = (size_t)cap * (i ? kTruncSlots : 1);  // probes per step
+    const size_t np = i ? (size_t)cap * kTruncSlots : (size_t)w.np0;  // probes per step
     w.Linc[i] = dalloc<double>((size_t)w.inc_lstride * np);
     w.lspn[i] = dalloc<uint32_t>(N);
     w.iflags[i] = dalloc<uint8_t>((size_t)w.inc_tiles * np);
@@ -460,8 +472,6 @@ void ensure_workspace(ebcc_ctx* c, const Geo& g, int nfields, int want = 0) {
     CK(cudaMemset(w.iflags[i], kTileDirty, (size_t)w.inc_tiles * np));
   }
   w.icomputed = dalloc<unsigned long long>(2 * kMaxLevels);
-  CK(cudaMallocHost(&w.h_prm, sizeof(ProbeParam) * (1 + kTruncSlots) * cap));
-  CK(cudaMallocHost(&w.h_res, sizeof(ProbeResult) * (1 + kTruncSlots) * cap));
   w.ctl = dalloc<CtlChunk>(cap);
   w.ctl_out = dalloc<CtlOut>(cap);
   w.ctl_prm = dalloc<CtlParams>(1);
@@ -891,10 +901,13 @@ CtlArgs ctl_args(Workspace& w, int nfields, int slots) {
   a.active = w.active;
   a.prm = w.prm;
   a.res = w.res;
-  a.tprm = w.prm + w.cap;
-  a.tres = w.res + w.cap;
+  a.tprm = w.prm + w.np0;
+  a.tres = w.res + w.np0;
   a.nfields = nfields;
   a.slots = slots;
+  a.bslots = 1;
+  a.smem = ctl_smem_ok(nfields) ? 1 : 0;
+  a.jmode = 3;
   a.n = w.g.n;
   return a;
 }
@@ -976,12 +989,19 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   }
   const Inc* inc_base = inc_ok ? &inc_s[0] : nullptr;
   const Inc* inc_res = inc_ok ? &inc_s[1] : nullptr;
-  const int spec_auto = N * (int64_t)nfields <= (8ll << 20) ? kTruncSlots : 1;
+  const int spec_auto = N * (int64_t)nfields <= kSpecPoints ? kTruncSlots : 1;
   const int TS = inc_res ? (spec_env ? spec_env : spec_auto) : 1;  // truncation probe slots
   const int ntp = TS * nfields;
+  // base-stream probe slots: the base and pure-base searches speculate the
+  // same way (SPIHT base, batches that fit the slot buffers)
+  static const bool bspec_env = !(getenv("EBCC_BSPEC") && getenv("EBCC_BSPEC")[0] == '0');
+  const int SB = (bspec_env && TS > 1 && !j2 && nfields <= w.spec_cap &&
+                  N * (int64_t)nfields <= kSpecBasePoints) ? TS : 1;
+  const int nbp = SB * nfields;
   *w.h_ctl_prm = CtlParams{q, r0, tol, prune ? 1 : 0, early_ok() ? 1 : 0, TS, 0};
   CK(cudaMemcpyAsync(w.ctl_prm, w.h_ctl_prm, sizeof(CtlParams), cudaMemcpyHostToDevice, st));
   CtlArgs a0 = ctl_args(w, nfields, TS);
+  a0.bslots = SB;
   // opt-in J2 base layer (ebcot.cuh): its encoder, probes and residue
   EbBufs* eb = j2 ? &ensure_ebcot(w, nfields, st) : nullptr;
   const EbGeo egeo = w.eb.geo;
@@ -1027,7 +1047,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   if (!graphs) {
     Meta mbase = meta_of(w, false), mres = meta_of(w, true);
     for (int i = 0; i < 2; i++)
-      CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields * (i ? kTruncSlots : 1), st));
+      CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * (i ? ntp : nbp), st));
     CK(cudaMemsetAsync(w.icomputed, 0, sizeof(unsigned long long) * 2 * kMaxLevels, st));
     auto base_probe = [&](bool early_p) {
       if (eb) {  // J2 base: closed-form prefix decode, then the fused probe levels
@@ -1036,8 +1056,8 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
                    nullptr, true, early_p);
         return;
       }
-      probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32,
-                 w.fs, w.res, st, inc_base, false, early_p);
+      probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nbp, w.norm, w.x32,
+                 w.fs, w.res, st, inc_base, false, early_p, nfields);
     };
     auto stats_now = [&]() {
       CK(cudaMemcpyAsync(w.h_ctl_stats, w.ctl_stats, sizeof(CtlStats), cudaMemcpyDeviceToHost, st));
@@ -1077,8 +1097,8 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       prev = cs;
       if (!anyp && !anyt) break;
       if (anyt)
-        probe_trunc(mres, w.prm + w.cap, inc_res ? w.Linc[1] : w.A2, w.B2, g, ntp, w.base_dec,
-                    w.x32, w.fs, w.res + w.cap, st, inc_res, false, nfields);
+        probe_trunc(mres, w.prm + w.np0, inc_res ? w.Linc[1] : w.A2, w.B2, g, ntp, w.base_dec,
+                    w.x32, w.fs, w.res + w.np0, st, inc_res, false, nfields);
       if (anyp) base_probe(true);
     }
     ctl_finalize(a0, st);
@@ -1091,14 +1111,14 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
   } else if (!sg) {
     Meta mbase = meta_of(w, false), mres = meta_of(w, true);
     cudaStream_t s0 = cap_stream(c, 0), s1 = cap_stream(c, 1), s2 = cap_stream(c, 2),
-                 s3 = cap_stream(c, 3), s4 = cap_stream(c, 4);
+                 s3 = cap_stream(c, 3), s4 = cap_stream(c, 4), s5 = cap_stream(c, 5);
     CK(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal));
     cudaStreamCaptureStatus cst;
     cudaGraph_t top = nullptr;
     CK(cudaStreamGetCaptureInfo(s0, &cst, nullptr, &top, nullptr, nullptr));
     // incremental-probe state is invalid at the batch start
     for (int i = 0; i < 2; i++)
-      CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * nfields * (i ? kTruncSlots : 1), s0));
+      CK(cudaMemsetAsync(w.istate[i], 0, sizeof(IncState) * (i ? ntp : nbp), s0));
     CK(cudaMemsetAsync(w.icomputed, 0, sizeof(unsigned long long) * 2 * kMaxLevels, s0));
     auto base_probe = [&](cudaStream_t ps, bool early_p) {
       if (eb) {  // J2 base: closed-form prefix decode, then the fused probe levels
@@ -1107,11 +1127,12 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
                    nullptr, true, early_p);
         return;
       }
-      probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nfields, w.norm, w.x32,
-                 w.fs, w.res, ps, inc_base, false, early_p);
+      probe_base(mbase, w.prm, inc_base ? w.Linc[0] : w.A, w.B, g, nbp, w.norm, w.x32,
+                 w.fs, w.res, ps, inc_base, false, early_p, nfields);
     };
     // base quantile search: start (T_base, first requests), the first probe
     // (its level-0 kernel timed for the roofline), then the loop
+    fused::timer_record(c->ph[0], s0);
     CtlArgs ab = a0;
     ctl_base(ab, true, 0, s0);
     fused::g_level0_timer = &c->l0;
@@ -1131,19 +1152,59 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     });
     // residue = norm - base decode at the chosen budget; residual DWT +
     // 32-plane encode (the 24-plane variant is its prefix)
-    ctl_residue(a0, s0);
-    if (eb) {
-      ebcot_probe_decode(egeo, *eb, w.prm, nfields, nfields, w.A, s0);
-      base_to_residue(mj2, w.prm, w.B, w.eb.ll, g, nfields, w.norm, w.base_dec, w.norm, s0);
-    } else {
-      base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, s0);
+    fused::timer_record(c->ph[1], s0);
+    // small batches (speculating, the GPU has slack): the pure-base search
+    // needs only the base stream, so it runs as its own loop beside the
+    // residue, the residual DWT and the residual encode, and hands over to
+    // the joint loop (candidate pruning) when the encode is done; the residue
+    // decode takes its parameters and decode tables from the (idle)
+    // truncation slots
+    const bool split = SB > 1 && N * (int64_t)nfields <= kSplitPoints;
+    if (split) {
+      CK(cudaEventRecord(c->ev_f0, s0));
+      CK(cudaStreamWaitEvent(s5, c->ev_f0, 0));
+      cudaGraphConditionalHandle hq;
+      CK(cudaGraphConditionalHandleCreate(&hq, top, 1, cudaGraphCondAssignDefault));
+      add_conditional(s5, s1, hq, cudaGraphCondTypeWhile, [&](cudaGraph_t body, cudaStream_t bs) {
+        cudaGraphConditionalHandle hp;
+        CK(cudaGraphConditionalHandleCreate(&hp, body, 0, 0));
+        CtlArgs al = a0;
+        al.jmode = 1;
+        al.h_loop = hq;
+        al.h_pure = hp;
+        ctl_joint(al, false, 3, bs);
+        add_conditional(bs, s3, hp, cudaGraphCondTypeIf,
+                        [&](cudaGraph_t, cudaStream_t is) { base_probe(is, true); });
+      });
+    }
+    {
+      CtlArgs ar = a0;
+      Meta mr = mbase;
+      if (split) {
+        ar.prm = a0.tprm;
+        mr.tq = w.tq_res;
+      }
+      ctl_residue(ar, s0);
+      if (eb) {
+        ebcot_probe_decode(egeo, *eb, ar.prm, nfields, nfields, w.A, s0);
+        base_to_residue(mj2, ar.prm, w.B, w.eb.ll, g, nfields, w.norm, w.base_dec, w.norm, s0);
+      } else {
+        base_to_residue(mr, ar.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, s0);
+      }
     }
     forward_dwt_from(w.norm, w.A2, w.B2, N, nfields, g, s0);
-    CK(cudaEventRecord(c->ev_s0, s0));
+    fused::timer_record(c->ev_s0, s0);
     encode_launch(c, nfields, true, kDeepPlanes, w.A2, true, nullptr, s0, cluster);
-    CK(cudaEventRecord(c->ev_s1, s0));
-    // pure-base search and truncation search (24 planes, then 32): each step
-    // probes both kinds of candidates as two concurrent IF branches
+    fused::timer_record(c->ev_s1, s0);
+    if (split) {
+      CK(cudaMemsetAsync(&w.ctl_stats->stop, 1, sizeof(unsigned long long), s0));
+      fused::timer_record(c->ph[4], s5);
+      CK(cudaEventRecord(c->ev_f1, s5));
+      CK(cudaStreamWaitEvent(s0, c->ev_f1, 0));
+    }
+    // pure-base search (unless done above) and truncation search (24 planes,
+    // then 32): each step probes both kinds of candidates as two concurrent
+    // IF branches
     ctl_joint(a0, true, 0, s0);
     cudaGraphConditionalHandle hj;
     CK(cudaGraphConditionalHandleCreate(&hj, top, 1, cudaGraphCondAssignDefault));
@@ -1159,14 +1220,15 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       CK(cudaEventRecord(c->ev_f0, bs));
       CK(cudaStreamWaitEvent(s2, c->ev_f0, 0));
       add_conditional(s2, s4, ht, cudaGraphCondTypeIf, [&](cudaGraph_t, cudaStream_t is) {
-        probe_trunc(mres, w.prm + w.cap, inc_res ? w.Linc[1] : w.A2, w.B2, g, ntp, w.base_dec,
-                    w.x32, w.fs, w.res + w.cap, is, inc_res, false, nfields);
+        probe_trunc(mres, w.prm + w.np0, inc_res ? w.Linc[1] : w.A2, w.B2, g, ntp, w.base_dec,
+                    w.x32, w.fs, w.res + w.np0, is, inc_res, false, nfields);
       });
       add_conditional(bs, s3, hp, cudaGraphCondTypeIf,
                       [&](cudaGraph_t, cudaStream_t is) { base_probe(is, true); });
       CK(cudaEventRecord(c->ev_f1, s2));
       CK(cudaStreamWaitEvent(bs, c->ev_f1, 0));
     });
+    fused::timer_record(c->ph[2], s0);
     ctl_finalize(a0, s0);
     CK(cudaMemcpyAsync(w.h_ctl_out, w.ctl_out, sizeof(CtlOut) * nfields, cudaMemcpyDeviceToHost, s0));
     CK(cudaMemcpyAsync(w.h_fs, w.fs, sizeof(FieldScal) * nfields, cudaMemcpyDeviceToHost, s0));
@@ -1174,6 +1236,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     CK(cudaMemcpyAsync(w.h_mo + w.cap, w.mo_res, sizeof(MachineOut) * nfields,
                        cudaMemcpyDeviceToHost, s0));
     CK(cudaMemcpyAsync(w.h_ctl_stats, w.ctl_stats, sizeof(CtlStats), cudaMemcpyDeviceToHost, s0));
+    fused::timer_record(c->ph[3], s0);
     cudaGraph_t gr = nullptr;
     CK(cudaStreamEndCapture(s0, &gr));
     Workspace::SearchGraph ng;
@@ -1195,6 +1258,25 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
     float ms = 0;
     if (cudaEventElapsedTime(&ms, c->tev[0], c->tev[1]) == cudaSuccess) c->stats.ms_encode += ms;
     if (cudaEventElapsedTime(&ms, c->ev_s0, c->ev_s1) == cudaSuccess) c->stats.ms_encode += ms;
+    static const bool prof = getenv("EBCC_PROFILE") && getenv("EBCC_PROFILE")[0] == '1';
+    if (prof && graphs) {
+      float t[6] = {};
+      cudaEventElapsedTime(&t[0], c->tev[0], c->tev[1]);
+      cudaEventElapsedTime(&t[1], c->ph[0], c->ph[1]);
+      cudaEventElapsedTime(&t[2], c->ph[1], c->ev_s0);
+      cudaEventElapsedTime(&t[3], c->ev_s0, c->ev_s1);
+      cudaEventElapsedTime(&t[4], c->ev_s1, c->ph[2]);
+      cudaEventElapsedTime(&t[5], c->ph[2], c->ph[3]);
+      const CtlStats cs = *w.h_ctl_stats;
+      float tp = -1;
+      if (SB > 1 && N * (int64_t)nfields <= kSplitPoints) cudaEventElapsedTime(&tp, c->ph[1], c->ph[4]);
+      if (tp >= 0) fprintf(stderr, "[ebcc phases] pure-base loop beside the residual encode: %.3f ms\n", tp);
+      fprintf(stderr,
+              "[ebcc phases] %d fields: base encode %.3f | base search %.3f (%llu steps) | "
+              "residue+dwt %.3f | residual encode %.3f | joint search %.3f (%llu steps) | "
+              "finalize %.3f ms\n",
+              nfields, t[0], t[1], cs.base_steps, t[2], t[3], t[4], cs.joint_steps, t[5]);
+    }
     if (cudaEventElapsedTime(&ms, c->l0.a, c->l0.b) == cudaSuccess) {
       c->stats.ms_probe_kernel += ms;
       c->stats.probe_kernel_count++;
@@ -1350,6 +1432,7 @@ int ebcc_create(int32_t device, ebcc_ctx** out) {
     cudaEventCreate(&c->oev1);
     cudaEventCreate(&c->ev_s0);
     cudaEventCreate(&c->ev_s1);
+    for (cudaEvent_t& e : c->ph) cudaEventCreate(&e);
     cudaEventCreate(&c->tm_a);
     cudaEventCreate(&c->tm_b);
     cudaEventCreate(&c->tev[0]);
@@ -1400,6 +1483,8 @@ void ebcc_destroy(ebcc_ctx* c) {
   if (c->ev_f0) cudaEventDestroy(c->ev_f0);
   if (c->ev_f1) cudaEventDestroy(c->ev_f1);
   for (cudaEvent_t e : {c->cev0, c->cev1, c->oev0, c->oev1})
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ph)
     if (e) cudaEventDestroy(e);
   if (c->ev_s0) cudaEventDestroy(c->ev_s0);
   if (c->ev_s1) cudaEventDestroy(c->ev_s1);

@@ -593,9 +593,11 @@ void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, i
 
 void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                 int nfields, const double* norm, const float* orig, const FieldScal* fs,
-                ProbeResult* res, cudaStream_t st, const Inc* inc, bool xe, bool early) {
+                ProbeResult* res, cudaStream_t st, const Inc* inc, bool xe, bool early, int nphys) {
+  // nfields probes; probe v reads chunk v % nphys (several per chunk: the
+  // incremental path only)
   auto run = [&](auto e) {
-    if (inc) fused::inverse_inc(m, prm, *inc, a, g, nfields, st, e, false, xe);
+    if (inc) fused::inverse_inc(m, prm, *inc, a, g, nfields, st, e, false, xe, nphys);
     else fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false, xe);
   };
   if (early) run(BaseProbeEpi<false>{norm, orig, fs, prm, res, g.n, 0, 0.0, FieldScal{}, 0});

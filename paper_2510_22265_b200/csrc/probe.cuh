@@ -154,7 +154,7 @@ void decode_coeffs(const Meta& m, const ProbeParam* prm, double* a, int64_t n, i
 void probe_base(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                 int nfields, const double* norm, const float* orig, const FieldScal* fs,
                 ProbeResult* res, cudaStream_t st, const Inc* inc = nullptr, bool xe = true,
-                bool early = false);
+                bool early = false, int nphys = -1);
 
 // residual probe: decode (midpoint) -> IDWT -> + base -> max error
 void probe_trunc(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,

@@ -25,6 +25,7 @@ for it in range(4):
     recs, offs, total, st = ctx.compress(x.data_ptr(), nf, 721, 1440, 0.01, 1 - 1e-5, 10.0, 1e-3,
                                          flags=F, payload=pay.data_ptr(), payload_cap=pay.numel())
     t1 = time.perf_counter()
+    cst = ctx.stats()
     ctx.decompress(pay.data_ptr(), offs, recs, 721, 1440, 5, out.data_ptr(), flags=F)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
@@ -33,4 +34,5 @@ for it in range(4):
 c = min(r[0] for r in res)
 d = min(r[1] for r in res)
 print(f"{tag} {nf} fields: compress {1e3*c:.1f} ms ({4*host.size/c/1e9:.2f} GB/s), "
-      f"decompress {1e3*d:.1f} ms ({4*host.size/d/1e9:.2f} GB/s), total payload {total}", flush=True)
+      f"decompress {1e3*d:.1f} ms ({4*host.size/d/1e9:.2f} GB/s), total payload {total}, "
+      f"probe steps {cst.get('probe_launches')}", flush=True)
