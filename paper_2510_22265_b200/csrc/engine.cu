@@ -72,7 +72,9 @@ template <class T>
 T* dalloc(size_t count) {
   void* p = nullptr;
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc(&p, sizeof(T) * count);
+  // 256 bytes of slack: the level kernels' staged row copies (16-byte
+  // granules) may read one element past a buffer's last row
+  cudaError_t e = cudaMalloc(&p, sizeof(T) * count + 256);
   if (e != cudaSuccess) throw CudaFail{e, "cudaMalloc"};
   if (g_alloc_acc) *g_alloc_acc += (int64_t)(sizeof(T) * count);
   return static_cast<T*>(p);
