@@ -238,6 +238,10 @@ struct BaseProbeEpi {
   using Pre = float;
   __device__ Pre pre(int f, int64_t off) const { return orig[(int64_t)f * n + off]; }
   __device__ Pre pre_masked(int f, int64_t off) const { return pre(f, off); }
+  // the level kernel stages the originals of a chunk's rows in shared memory
+  static constexpr bool kStageOrig = true;
+  __host__ __device__ const float* stage_src() const { return orig; }
+  __device__ Pre pre_staged(int, int64_t, float o) const { return o; }
   __device__ bool begin(int v, int f) {  // probe v of chunk f
     cnt = 0; mx = 0.0; bad = false; cc = 0;
     if (count && threadIdx.x == 0) tile_violations() = 0;  // read after the chunk barriers
@@ -356,6 +360,11 @@ struct TruncProbeEpi {
   // both inputs prefetched before the row lifting (the kernel runs at 3
   // CTAs/SM, 80 registers: room for them)
   __device__ Pre pre_masked(int f, int64_t off) const { return pre(f, off); }
+  static constexpr bool kStageOrig = true;
+  __host__ __device__ const float* stage_src() const { return orig; }
+  __device__ Pre pre_staged(int f, int64_t off, float o) const {
+    return {base[(int64_t)f * n + off], o};
+  }
   __device__ void put_masked(int, int64_t, double v, const Pre& p, bool valid) {
     const double rec = __dadd_rn(p.base, v);
     bad |= valid && denorm_err(s, rec, p.orig) > s.eps_abs;
@@ -385,6 +394,7 @@ struct TruncProbeEpi {
 };
 
 struct ResidueEpi {
+  EBCC_NO_STAGE
   static constexpr bool kAbort = false;
   static constexpr int kMinBlocks = EBCC_MINB;
   static constexpr bool kMasked = false, kProbe = false;
@@ -406,6 +416,7 @@ struct ResidueEpi {
 };
 
 struct StoreFieldEpi {
+  EBCC_NO_STAGE
   static constexpr bool kAbort = false;
   static constexpr int kMinBlocks = EBCC_MINB;
   static constexpr bool kMasked = false, kProbe = false;
@@ -425,6 +436,7 @@ struct StoreFieldEpi {
 };
 
 struct AddDenormEpi {
+  EBCC_NO_STAGE
   static constexpr bool kAbort = false;
   static constexpr int kMinBlocks = EBCC_MINB;
   static constexpr bool kMasked = false, kProbe = false;
