@@ -72,8 +72,8 @@ template <class T>
 T* dalloc(size_t count) {
   void* p = nullptr;
   if (count == 0) count = 1;
-  // 256 bytes of slack: the level kernels' staged row copies (16-byte
-  // granules) may read one element past a buffer's last row
+  // 256 bytes of slack behind every workspace buffer (vector loads of a
+  // buffer's last partial granule stay inside the allocation)
   cudaError_t e = cudaMalloc(&p, sizeof(T) * count + 256);
   if (e != cudaSuccess) throw CudaFail{e, "cudaMalloc"};
   if (g_alloc_acc) *g_alloc_acc += (int64_t)(sizeof(T) * count);
