@@ -2320,11 +2320,15 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         std::vector<uint8_t> mact(nb);
         for (int i = 0; i < nb; i++) mact[i] = ract[i] && rmo[i].n_max != kExpNone;
         h2d_small(c, w.dec2.active, mact.data(), nb, c->side);
-        decode_init(rb, c->side);
+        decode_init(rb, c->side, w.rank_hi2 ? nullptr : w.packed2);
         // one CTA per chunk: fits beside the base machine's clusters
         run_machine(true, rb, g, w.tt, kMaxDecodePlanes, c->side, 1);
-        gather_refinement(rb, c->side);
-        pack_meta(rb, w.packed2, w.sprank2, c->side, nullptr, w.rank_hi2);
+        if (w.rank_hi2) {  // wide records: significands, then pack_meta
+          gather_refinement(rb, c->side);
+          pack_meta(rb, w.packed2, w.sprank2, c->side, nullptr, w.rank_hi2);
+        } else {
+          gather_pack(rb, w.packed2, w.sprank2, c->side);
+        }
         CK(cudaEventRecord(c->ev_b, c->side));
         c->stats.kernel_launches += 4;
       }
@@ -2359,10 +2363,14 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         std::vector<uint8_t> mact(nb);
         for (int i = 0; i < nb; i++) mact[i] = bact[i] && bmo[i].n_max != kExpNone;
         h2d_small(c, w.active, mact.data(), nb, st);
-        decode_init(mb, st);
+        decode_init(mb, st, w.rank_hi ? nullptr : w.packed);
         run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
-        gather_refinement(mb, st);
-        pack_meta(mb, w.packed, w.sprank, st, nullptr, w.rank_hi);
+        if (w.rank_hi) {
+          gather_refinement(mb, st);
+          pack_meta(mb, w.packed, w.sprank, st, nullptr, w.rank_hi);
+        } else {
+          gather_pack(mb, w.packed, w.sprank, st);
+        }
         c->stats.kernel_launches += 4;
       }
       g_trace.add(0, "dec_machines_issued", -1);
@@ -2600,10 +2608,14 @@ int decode_one(ebcc_ctx* c, const uint8_t* data, int64_t len, int64_t prefix_len
     CK(cudaMemcpyAsync(w.limit, &lim, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
     uint8_t act = nm != kZeroSentinel;
     CK(cudaMemcpyAsync(w.active, &act, 1, cudaMemcpyHostToDevice, st));
-    decode_init(mb, st);
+    decode_init(mb, st, w.rank_hi2 ? nullptr : w.packed2);
     run_machine(true, mb, g, w.tt, kMaxDecodePlanes, st);
-    gather_refinement(mb, st);
-    pack_meta(mb, w.packed2, w.sprank2, st, nullptr, w.rank_hi2);
+    if (w.rank_hi2) {
+      gather_refinement(mb, st);
+      pack_meta(mb, w.packed2, w.sprank2, st, nullptr, w.rank_hi2);
+    } else {
+      gather_pack(mb, w.packed2, w.sprank2, st);
+    }
     ProbeParam p{};
     p.B = ~0ull; p.planes = -1; p.active = 1;
     // (an all-zero stream has no n_last: dequantized_field adds no offset)

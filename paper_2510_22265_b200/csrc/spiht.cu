@@ -1146,6 +1146,42 @@ __global__ void refine_gather_kernel(MachineBufs mb) {
   }
 }
 
+// decompress: the refinement gather writes the probe records itself (probe.cuh:
+// x = LSP rank | significance plane << 26, y = sign << 31 | significand bits)
+// and the sign offsets by rank, instead of a significand array that
+// pack_meta would re-read with the other per-coefficient arrays.  Records of
+// coefficients whose sign was never read keep decode_init's all-ones
+// ("never placed").  Narrow records only (ranks below 2^26 - 1).
+__global__ void refine_gather_pack_kernel(MachineBufs mb, uint2* __restrict__ packed,
+                                          uint32_t* __restrict__ sprank) {
+  const int f = blockIdx.y;
+  if (mb.active && !mb.active[f]) return;
+  const int64_t fo = (int64_t)f * mb.stride;
+  const PlaneRec* prec = mb.planes + (int64_t)f * kMaxPlaneRecs;
+  const int pr = mb.out[f].planes_run;
+  const uint32_t nlsp = mb.out[f].lsp_count;
+  const uint64_t limit = mb.limit[f];
+  const uint32_t* bits = mb.bits + (int64_t)f * mb.bit_stride;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)nlsp;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = mb.lsp[fo + i];
+    const uint32_t sp = mb.sign_pos[fo + c];
+    sprank[fo + i] = sp;  // kNone: sign never read (ranks >= lsp_count are never looked at)
+    if (sp == kNone) continue;
+    const uint32_t pi = mb.pinfo[fo + c];
+    const int ps = pi & 0x3f;
+    uint32_t m = 0;
+    for (int p = ps + 1; p < pr && p - ps <= 31; p++) {
+      if ((uint32_t)i >= prec[p].refine_len) break;
+      uint64_t q = (uint64_t)prec[p].refine_start + (uint64_t)i;
+      if (q >= limit) break;
+      m |= (uint32_t)read_bit(bits, q, limit) << (31 - (p - ps));
+    }
+    packed[fo + c] = make_uint2(((uint32_t)i & 0x3ffffffu) | ((uint32_t)ps << 26),
+                                ((pi & 0x80u) << 24) | m);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Deferred encoder LIP passes.  The LIP before plane p's pass is the LIP
 // history H (roots, then every insignificant child in append order) filtered
@@ -1377,14 +1413,17 @@ void emit_lip_host(MachineBufs& mb, cudaStream_t st) {
 }
 
 // decoder init: nothing placed yet
-__global__ void decode_init_kernel(MachineBufs mb) {
+// packed != null (gather_pack follows): the records start out "never placed"
+// (all ones) and the significands are never materialised
+__global__ void decode_init_kernel(MachineBufs mb, uint2* packed) {
   const int f = blockIdx.y;
   const int64_t fo = (int64_t)f * mb.stride;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < mb.stride;
        i += (int64_t)gridDim.x * blockDim.x) {
     mb.sign_pos[fo + i] = kNone;
     mb.pinfo[fo + i] = 0;
-    mb.mant[fo + i] = 0;
+    if (packed) packed[fo + i] = make_uint2(0xffffffffu, 0xffffffffu);
+    else mb.mant[fo + i] = 0;
   }
 }
 
@@ -1567,10 +1606,16 @@ void write_refinement(MachineBufs& mb, int planes, cudaStream_t st) {
   refine_write_kernel<<<dim3(blocks, mb.nfields), 256, 0, st>>>(mb, planes);
 }
 
-void decode_init(MachineBufs& mb, cudaStream_t st) {
+void decode_init(MachineBufs& mb, cudaStream_t st, uint2* packed) {
   int blocks = (int)((mb.stride + 255) / 256);
   if (blocks > 1024) blocks = 1024;
-  decode_init_kernel<<<dim3(blocks, mb.nfields), 256, 0, st>>>(mb);
+  decode_init_kernel<<<dim3(blocks, mb.nfields), 256, 0, st>>>(mb, packed);
+}
+
+void gather_pack(MachineBufs& mb, uint2* packed, uint32_t* sprank, cudaStream_t st) {
+  int blocks = (int)((mb.stride + 255) / 256);
+  if (blocks > 1024) blocks = 1024;
+  refine_gather_pack_kernel<<<dim3(blocks, mb.nfields), 256, 0, st>>>(mb, packed, sprank);
 }
 
 void gather_refinement(MachineBufs& mb, cudaStream_t st) {

@@ -97,7 +97,11 @@ void emit_lip(MachineBufs& mb, int planes, cudaStream_t st);
 // encoder refinement bits (fully parallel over LSP)
 void write_refinement(MachineBufs& mb, int planes, cudaStream_t st);
 // decoder: reset per-coefficient metadata before run_machine(decode=true)
-void decode_init(MachineBufs& mb, cudaStream_t st);
+// packed != null: records preset to "never placed" for gather_pack
+void decode_init(MachineBufs& mb, cudaStream_t st, uint2* packed = nullptr);
+// decompress (narrow records): refinement gather straight into the probe
+// records + sign offsets by rank (replaces gather_refinement + pack_meta)
+void gather_pack(MachineBufs& mb, uint2* packed, uint32_t* sprank, cudaStream_t st);
 // decoder: gather refinement bits into mant[] (in LSP order)
 void gather_refinement(MachineBufs& mb, cudaStream_t st);
 
