@@ -15,6 +15,8 @@
 // a (rows, cols) or (cols, rows) pair the data is back in the first buffer
 // with the untouched detail bands still in place.
 #include "lift.cuh"
+#include "fdwt_fused.cuh"
+#include <cstdlib>
 
 namespace ebcc {
 
@@ -47,13 +49,42 @@ void inverse_level_rows(const double* b, double* a, int64_t field_stride, int nf
   launch_pass<true>(b, a, field_stride, nfields, g.cols, g.lr[k], g.lc[k], false, st);
 }
 
+namespace {
+// Every level by the fused row + column kernel (fdwt_fused.cuh).  A level
+// cannot run in place (CTAs read their neighbours' halo), so the levels
+// ping-pong: level k reads its region from the buffer level k-1 wrote (src
+// for level 0) and writes all four quadrants to the other of a / b; what a
+// level leaves in b is copied to a afterwards -- its detail bands, and the LL
+// band too after the last level -- so the pyramid ends up in a.  Degenerate
+// regions (a single row or column at some level) keep the separable passes.
+bool fused_forward(const double* src, double* a, double* b, int64_t field_stride, int nfields,
+                   const Geo& g, cudaStream_t st) {
+  static const bool on = !(getenv("EBCC_FDWT") && getenv("EBCC_FDWT")[0] == '0');
+  if (!on) return false;
+  for (int k = 0; k < g.levels; k++)
+    if (g.lr[k] < 2 || g.lc[k] < 2) return false;
+  const double* cur = src;
+  for (int k = 0; k < g.levels; k++) {
+    double* out = (cur == a) ? b : a;
+    fdwt::launch_level(cur, out, field_stride, nfields, g.cols, g.lr[k], g.lc[k], st);
+    if (out != a)
+      fdwt::copy_bands(out, a, field_stride, nfields, g.cols, g.lr[k], g.lc[k],
+                       k == g.levels - 1, st);
+    cur = out;
+  }
+  return true;
+}
+}  // namespace
+
 void forward_dwt(double* a, double* b, int64_t field_stride, int nfields, const Geo& g,
                  cudaStream_t st) {
+  if (fused_forward(a, a, b, field_stride, nfields, g, st)) return;
   for (int k = 0; k < g.levels; k++) forward_level(a, b, field_stride, nfields, g, k, st);
 }
 
 void forward_dwt_from(const double* src, double* a, double* b, int64_t field_stride, int nfields,
                       const Geo& g, cudaStream_t st) {
+  if (fused_forward(src, a, b, field_stride, nfields, g, st)) return;
   // level 0: rows src -> b, columns b -> a (the whole array is the region)
   const int r = g.lr[0], c = g.lc[0];
   launch_pass<false>(src, b, field_stride, nfields, g.cols, r, c, false, st);
