@@ -51,7 +51,10 @@ __device__ __forceinline__ int fold(int t, int n) {
 
 // region R x C (R, C > 1) of `in` (row stride cols, fields fstride apart) ->
 // the same region of `out` in the [s | d] x [s | d] layout
-__global__ void __launch_bounds__(THREADS, 3)
+#ifndef EBCC_FDWT_MINB
+#define EBCC_FDWT_MINB 5  // 46 registers: 5 CTAs/SM hide the load -> shuffle -> barrier chain (148 fields: -0.6 ms vs 3)
+#endif
+__global__ void __launch_bounds__(THREADS, EBCC_FDWT_MINB)
     level_kernel(const double* __restrict__ in, double* __restrict__ out, int64_t fstride, int cols,
                  int R, int C, int th) {
   extern __shared__ double dyn[];
