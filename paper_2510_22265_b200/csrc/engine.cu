@@ -645,6 +645,9 @@ void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const do
   Workspace& w = c->ws;
   CK(cudaGetLastError());  // surface anything deferred from before this encode
   MachineBufs mb = machine_bufs(w, nfields, residual);
+  // the stream's probe tables by LSP rank, written where the ranks are assigned
+  mb.lsp = w.lspn[packed_residual ? 1 : 0];
+  mb.sprank = packed_residual ? w.sprank2 : w.sprank;
   if (active) {
     std::vector<MachineOut> init(nfields);
     for (auto& m : init) { m = MachineOut{}; m.n_max = kExpNone; }
@@ -662,8 +665,10 @@ void encode_launch(ebcc_ctx* c, int nfields, bool residual, int planes, const do
   CK(cudaGetLastError());
   write_refinement(mb, planes, st);
   CK(cudaGetLastError());
-  pack_meta(mb, packed_residual ? w.packed2 : w.packed, packed_residual ? w.sprank2 : w.sprank,
-            st, w.lspn[packed_residual ? 1 : 0], packed_residual ? w.rank_hi2 : w.rank_hi);
+  // (the encoder wrote the sign offsets and nodes by LSP rank itself:
+  // MachineBufs::sprank, and its LSP list is the stream's lspn buffer)
+  pack_meta(mb, packed_residual ? w.packed2 : w.packed, nullptr, st, nullptr,
+            packed_residual ? w.rank_hi2 : w.rank_hi);
   c->stats.kernel_launches += 9 + w.g.levels;
   CK(cudaGetLastError());
 }

@@ -159,7 +159,7 @@ __global__ void pack_meta_kernel(MachineBufs mb, uint2* packed, uint32_t* sprank
     packed[fo + i] = make_uint2((rank & kRankNone) | ((pi & 0x3fu) << kRankBits),
                                 ((pi & 0x80u) << 24) | (mb.mant[fo + i] & 0x7fffffffu));
     if (rank_hi) rank_hi[fo + i] = (uint8_t)(rank >> kRankBits);
-    if (sp != kNone) {
+    if (sprank && sp != kNone) {  // (null: the encoder wrote both by rank already)
       sprank[fo + rank] = sp;
       if (lspn) lspn[fo + rank] = (uint32_t)i;
     }
@@ -615,7 +615,7 @@ void selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_
 
 void pack_meta(const MachineBufs& mb, uint2* packed, uint32_t* sprank, cudaStream_t st,
                uint32_t* lspn, uint8_t* rank_hi) {
-  cudaMemsetAsync(sprank, 0xff, sizeof(uint32_t) * mb.stride * mb.nfields, st);
+  if (sprank) cudaMemsetAsync(sprank, 0xff, sizeof(uint32_t) * mb.stride * mb.nfields, st);
   pack_meta_kernel<<<dim3(grid_for(mb.stride, 1024), mb.nfields), 256, 0, st>>>(mb, packed,
                                                                                  sprank, lspn, rank_hi);
 }

@@ -429,6 +429,7 @@ __global__ void __launch_bounds__(MT, MINB) machine_kernel(MachineBufs mb, Geo g
   uint64_t* wav_a = mb.w0 + fo;
   uint64_t* wav_b = mb.w1 + fo;
   uint32_t* lsp = mb.lsp + fo;
+  uint32_t* sprank = (!DECODE && mb.sprank) ? mb.sprank + fo : nullptr;
   uint32_t* bits = mb.bits + (int64_t)f * mb.bit_stride;
   PlaneRec* prec = mb.planes + (int64_t)f * kMaxPlaneRecs;
   const int n_max = mb.out[f].n_max;
@@ -656,6 +657,7 @@ __global__ void __launch_bounds__(MT, MINB) machine_kernel(MachineBufs mb, Geo g
             } else {
               sign_pos[c] = (uint32_t)sp;
               pinfo[c] = (uint8_t)((e_neg(ent[k]) << 7) | p);
+              if (sprank) sprank[rank] = (uint32_t)sp;
             }
             r++;
           } else {
@@ -955,6 +957,7 @@ __global__ void __launch_bounds__(MT, MINB) machine_kernel(MachineBufs mb, Geo g
                   } else {
                     sign_pos[c] = (uint32_t)sp;
                     pinfo[c] = (uint8_t)((e_neg(cin[k][s]) << 7) | p);
+                    if (sprank) sprank[rank] = (uint32_t)sp;
                   }
                   sg++;
                 } else {
@@ -1276,7 +1279,10 @@ __global__ void __launch_bounds__(1024) lip_scan_kernel(MachineBufs mb, uint32_t
 }
 
 template <bool LIS>
-__global__ void __launch_bounds__(ET) lip_emit_kernel(MachineBufs mb, const uint32_t* hist,
+#ifndef EBCC_EMIT_MINB
+#define EBCC_EMIT_MINB 2  // 32 registers, two 1024-thread CTAs per SM (148 fields: compress -0.7 ms)
+#endif
+__global__ void __launch_bounds__(ET, EBCC_EMIT_MINB) lip_emit_kernel(MachineBufs mb, const uint32_t* hist,
                                                       int tiles) {
   const int f = blockIdx.y;
   if (emit_skip(mb, f)) return;
@@ -1392,6 +1398,7 @@ __global__ void __launch_bounds__(ET) lip_emit_kernel(MachineBufs mb, const uint
       const uint32_t c = (uint32_t)ent[k];
       const uint32_t rank = s_ref[b] + (uint32_t)eq;
       mb.lsp[fo + rank] = c;
+      if (mb.sprank) mb.sprank[fo + rank] = (uint32_t)sp;
       mb.lsp_rank[fo + c] = rank;
       mb.sign_pos[fo + c] = (uint32_t)sp;
       mb.pinfo[fo + c] = (uint8_t)((neg << 7) | b);

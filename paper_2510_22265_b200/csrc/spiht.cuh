@@ -58,6 +58,9 @@ struct MachineBufs {
   const uint64_t* ginfo;     // geometry-only node info (decode; shared by all fields)
   // lists (capacity `stride` each)
   uint64_t* lip; uint64_t* lis0; uint64_t* lis1; uint64_t* w0; uint64_t* w1; uint32_t* lsp;
+  // encoder, optional: sign bit offset by LSP rank, written with the LSP
+  // entry (Meta::sprank; pack_meta then has nothing to scatter)
+  uint32_t* sprank;
   uint8_t* hrel;             // encoder: significance plane of each LIS history entry
   // stream bits
   uint32_t* bits;
