@@ -38,7 +38,7 @@ constexpr int THREADS = GROUPS * PC;
 constexpr int TW = GROUPS * GW;      // 224 region columns per CTA
 constexpr int CH = 8;                // rows per shared-memory chunk
 constexpr int KB = CH / 2;
-constexpr int TH = 96;               // region rows per CTA (multiple of CH)
+constexpr int TH = 192;              // region rows per CTA (multiple of CH)
 
 __device__ __forceinline__ int fold(int t, int n) {
   if (t >= 0 && t < n) return t;
