@@ -1088,7 +1088,8 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
       ebcot_probe_decode(egeo, *eb, w.prm, nfields, nfields, w.A, st);
       base_to_residue(mj2, w.prm, w.B, w.eb.ll, g, nfields, w.norm, w.base_dec, w.norm, st);
     } else {
-      base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st);
+      // (like the probes: a normalised field's exponents stay in the normal range)
+      base_to_residue(mbase, w.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, st, false);
     }
     forward_dwt_from(w.norm, w.A2, w.B2, N, nfields, g, st);
     CK(cudaEventRecord(c->ev_s0, st));
@@ -1196,7 +1197,7 @@ int compress_batch(ebcc_ctx* c, int nfields, double eps_rel, double q, double r0
         ebcot_probe_decode(egeo, *eb, ar.prm, nfields, nfields, w.A, s0);
         base_to_residue(mj2, ar.prm, w.B, w.eb.ll, g, nfields, w.norm, w.base_dec, w.norm, s0);
       } else {
-        base_to_residue(mr, ar.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, s0);
+        base_to_residue(mr, ar.prm, w.A, w.B, g, nfields, w.norm, w.base_dec, w.norm, s0, false);
       }
     }
     forward_dwt_from(w.norm, w.A2, w.B2, N, nfields, g, s0);

@@ -695,9 +695,9 @@ void inc_capacity(const Geo& g, int64_t* tiles, int64_t* tiles0) {
 
 void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                      int nfields, const double* norm, double* base_dec, double* resid,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool xe) {
   ResidueEpi e{norm, base_dec, resid, prm, g.n};
-  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false);
+  fused::inverse_fused(m, prm, a, b, g, nfields, st, e, false, xe);
 }
 
 void decode_field(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,

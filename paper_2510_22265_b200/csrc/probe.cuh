@@ -174,7 +174,7 @@ void inc_capacity(const Geo& g, int64_t* tiles, int64_t* tiles0);
 // decode the chosen base prefix; write base_dec and resid = norm - base_dec
 void base_to_residue(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
                      int nfields, const double* norm, double* base_dec, double* resid,
-                     cudaStream_t st);
+                     cudaStream_t st, bool xe = true);
 
 // decompress: decode a stream to a float64 field (out), optionally midpoint
 void decode_field(const Meta& m, const ProbeParam* prm, double* a, double* b, const Geo& g,
