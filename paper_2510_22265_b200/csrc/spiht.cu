@@ -205,7 +205,14 @@ __global__ void coef_prepare_kernel(const double* __restrict__ coef, int64_t cst
     int y = __shfl_xor_sync(0xffffffffu, best, o);
     best = y > best ? y : best;
   }
-  if ((threadIdx.x & 31) == 0) atomicMax(&out[f].n_max, best);
+  // one atomic per CTA (the warps meet in shared memory)
+  __shared__ int s_best[32];
+  if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)((blockDim.x + 31) >> 5); w++) best = s_best[w] > best ? s_best[w] : best;
+    atomicMax(&out[f].n_max, best);
+  }
 }
 
 // e_d / e_l for the parents of one level (spiht.py:182-195 over exponents)
