@@ -2328,7 +2328,10 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
         h2d_small(c, w.dec2.active, mact.data(), nb, c->side);
         decode_init(rb, c->side, w.rank_hi2 ? nullptr : w.packed2);
         // one CTA per chunk: fits beside the base machine's clusters
-        run_machine(true, rb, g, w.tt, kMaxDecodePlanes, c->side, 1);
+        // (EBCC_DEC_RES_CLUSTER: A/B runs)
+        static const int res_cluster =
+            getenv("EBCC_DEC_RES_CLUSTER") ? std::max(1, atoi(getenv("EBCC_DEC_RES_CLUSTER"))) : 1;
+        run_machine(true, rb, g, w.tt, kMaxDecodePlanes, c->side, res_cluster);
         if (w.rank_hi2) {  // wide records: significands, then pack_meta
           gather_refinement(rb, c->side);
           pack_meta(rb, w.packed2, w.sprank2, c->side, nullptr, w.rank_hi2);
