@@ -2168,7 +2168,18 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
       c->dplan.rows = g.rows; c->dplan.cols = g.cols; c->dplan.levels = g.levels;
       c->dplan.nfields = nfields; c->dplan.lanes = 1; c->dplan.j2 = j2_plan;
     }
-    const int64_t cap = balance(nfields, c->dplan.cap);
+    // Several batches: whole waves of list machines.  A batch's base and
+    // residual decoder machines are one CTA per chunk each, resident two per
+    // SM, so a batch of a multiple of the SM count fills every wave (2,368
+    // chunks in 7 balanced batches of 338 = 1.14 waves each took 297 ms, in 8
+    // batches of 296 = 2 x 148 they take 265 ms); otherwise balanced batches.
+    int64_t cap = balance(nfields, c->dplan.cap);
+    {
+      static const bool waves = !(getenv("EBCC_DEC_WAVES") && getenv("EBCC_DEC_WAVES")[0] == '0');
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      if (waves && nfields > c->dplan.cap && c->dplan.cap >= sms) cap = c->dplan.cap / sms * sms;
+    }
     g_slow.mark("dec_meminfo");
     for (int k = 0; k < 2; k++) {
       if (!c->ev_obuf[k]) CK(cudaEventCreateWithFlags(&c->ev_obuf[k], cudaEventDisableTiming));
