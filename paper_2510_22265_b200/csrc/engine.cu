@@ -2171,14 +2171,17 @@ int ebcc_decompress(ebcc_ctx* c, const uint8_t* payload, const int64_t* offsets,
     // Several batches: whole waves of list machines.  A batch's base and
     // residual decoder machines are one CTA per chunk each, resident two per
     // SM, so a batch of a multiple of the SM count fills every wave (2,368
-    // chunks in 7 balanced batches of 338 = 1.14 waves each took 297 ms, in 8
-    // batches of 296 = 2 x 148 they take 265 ms); otherwise balanced batches.
+    // chunks in 7 balanced batches of 338 = 1.14 waves each took 297 ms, in
+    // 16 batches of 148 they take 257 ms); otherwise balanced batches.
     int64_t cap = balance(nfields, c->dplan.cap);
     {
-      static const bool waves = !(getenv("EBCC_DEC_WAVES") && getenv("EBCC_DEC_WAVES")[0] == '0');
+      // EBCC_DEC_WAVES: 0 = balanced batches, k > 0 = at most k x SM count per batch
+      // (one SM count per batch measured best: 257 ms; two 264, balanced 338s 297)
+      static const int waves = getenv("EBCC_DEC_WAVES") ? atoi(getenv("EBCC_DEC_WAVES")) : 1;
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-      if (waves && nfields > c->dplan.cap && c->dplan.cap >= sms) cap = c->dplan.cap / sms * sms;
+      const int64_t lim = std::min<int64_t>(c->dplan.cap, (int64_t)waves * sms);
+      if (waves > 0 && nfields > lim && lim >= sms) cap = lim / sms * sms;
     }
     g_slow.mark("dec_meminfo");
     for (int k = 0; k < 2; k++) {
