@@ -36,6 +36,9 @@ namespace {
 #define EBCC_MT 512
 #endif
 constexpr int MT = EBCC_MT;      // machine threads
+#ifndef EBCC_MACH_CHILD_PREFETCH
+#define EBCC_MACH_CHILD_PREFETCH 1  // 296 chunks: compress 134.0 -> 132.9 ms, 37: 23.9 -> 23.55
+#endif
 #ifndef EBCC_MACH_PRELOAD
 #define EBCC_MACH_PRELOAD 1  // 148 chunks: decompress 16.3 -> 16.0 ms, compress the same
 #endif
@@ -887,6 +890,25 @@ __global__ void __launch_bounds__(MT, MINB) machine_kernel(MachineBufs mb, Geo g
                                           ((uint64_t)nxts << 32) |
                                           (DECODE ? 0ull : ((uint64_t)nsig << 48)));
           const uint64_t ex1 = s1.ex, tot1 = s1.total;
+#if EBCC_MACH_PRELOAD && EBCC_MACH_CHILD_PREFETCH
+          // encoder: the node info of the next tile's children on its way to
+          // L2 (the preloaded entries have arrived behind the scan's barrier;
+          // the per-field info array is not L2-resident, the decoder's shared
+          // geometry table is)
+          if (!DECODE) {
+#pragma unroll
+            for (int k = 0; k < MI; k++) {
+              const uint64_t e = pre[k];
+              const int lev = (int)((e >> ninfo::LEVEL) & 7);
+              if (e && lev > 0 && e_rel(e, e_isb(e) ? ninfo::RELL : ninfo::RELD) <= p) {
+                const int o = (int)((e >> ninfo::ORIENT) & 3);
+                const uint32_t c0 = (uint32_t)(2 * (int64_t)(uint32_t)e + s_K[lev * 3 + o]);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(info + c0));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(info + c0 + (uint32_t)g.cols));
+              }
+            }
+          }
+#endif
           if (single) {
             TC = lane16(tot1, 1);
             sg_seg0 = pos + segw + TC;
